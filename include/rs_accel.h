@@ -1,0 +1,271 @@
+/*
+ * rs_accel.h — C-ABI of the B200-native accelerator path for DeepRecSched
+ * (DeepRecSys, arXiv 2001.02772).
+ *
+ * The reference (`/root/reference/proj`, library `recsim`) models the
+ * accelerator as a pure cost function; this header is the drop-in boundary
+ * that replaces that model with real execution on a B200. Every entry point
+ * names the reference interface it replaces or mirrors (file:line under
+ * /root/reference/). Plain C types only: no torch, no C++ across the ABI,
+ * no exceptions.
+ *
+ * Error convention: every function returns RS_OK (0) or a negative RS_E_*
+ * code; rs_last_error() returns a thread-local message for the last failure
+ * on the calling thread.
+ */
+#ifndef RS_ACCEL_H
+#define RS_ACCEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+/* ---- error codes -------------------------------------------------------- */
+enum {
+  RS_OK = 0,
+  RS_E_INVALID = -1,        /* std::invalid_argument in the reference        */
+  RS_E_UNKNOWN_MODEL = -2,  /* recsim::UnknownModel (model_zoo.hpp:15-18)    */
+  RS_E_CONFIG = -3,         /* recsim::ConfigError (sim.hpp:15-17)           */
+  RS_E_DISTRIBUTION = -4,   /* recsim::InvalidDistribution (loadgen.hpp:12)  */
+  RS_E_CUDA = -5,           /* CUDA runtime / driver failure                 */
+  RS_E_OOM = -6,            /* device or pinned allocation failed            */
+  RS_E_INDEX = -7,          /* embedding index outside [0, rows_per_table)   */
+  RS_E_NO_DEVICE = -8,      /* no sm_100 device / extension cannot run       */
+  RS_E_CAPACITY = -9,       /* query larger than the handle's max_query_size */
+  RS_E_EMPTY = -10          /* recsim::EmptyResult (sim.hpp:19-21)           */
+};
+
+/* ---- operator API: mirror of recsim::ModelSpec -------------------------- */
+/* Pooling — recsim::Pooling (proj/include/recsim/model_zoo.hpp:20).        */
+enum {
+  RS_POOL_SUM = 0,
+  RS_POOL_CONCAT = 1,
+  RS_POOL_ATTENTION_FC = 2,
+  RS_POOL_ATTENTION_RNN = 3
+};
+
+/* OpCategory — recsim::OpCategory (model_zoo.hpp:22-31), same ordinals.    */
+enum {
+  RS_OP_DENSE_FC = 0,
+  RS_OP_PREDICT_FC = 1,
+  RS_OP_EMBEDDING_LOOKUP = 2,
+  RS_OP_POOLING = 3,
+  RS_OP_ATTENTION = 4,
+  RS_OP_RECURRENT = 5,
+  RS_OP_INTERACTION = 6,
+  RS_NUM_OP_CATEGORIES = 7
+};
+
+#define RS_MAX_LAYERS 8
+#define RS_NAME_LEN 32
+
+/* recsim::LayerStack (model_zoo.hpp:39-44): ordered output widths.         */
+typedef struct rs_layer_stack {
+  int32_t n;                      /* number of layers (0 = absent stack)     */
+  int64_t dims[RS_MAX_LAYERS];
+} rs_layer_stack;
+
+/* recsim::ModelSpec (model_zoo.hpp:54-65) + EmbeddingConfig (:46-52).
+ * `has_dense_fc` encodes std::optional<LayerStack> dense_fc;
+ * `recurrent_hidden_dim` = 0 encodes an empty std::optional.              */
+typedef struct rs_model_desc {
+  char name[RS_NAME_LEN];
+  int32_t has_dense_fc;
+  rs_layer_stack dense_fc;
+  rs_layer_stack predict_fc;
+  int64_t num_parallel_predict_stacks;
+  int64_t num_tables;
+  int64_t lookups_per_table;
+  int64_t embedding_dim;
+  int32_t pooling;                /* RS_POOL_*                               */
+  int64_t dense_input_dim;
+  int64_t recurrent_hidden_dim;   /* 0 = absent                              */
+} rs_model_desc;
+
+/* recsim::OpWork / WorkBreakdown (model_zoo.hpp:67-84).                    */
+typedef struct rs_work_breakdown {
+  double flops[RS_NUM_OP_CATEGORIES];
+  double bytes[RS_NUM_OP_CATEGORIES];
+  double gather_stream;
+} rs_work_breakdown;
+
+/* Host-only mirrors of the reference's model/operator API (no GPU needed). */
+
+/* builtin_model() — proj/src/model_zoo.cpp:141-170. RS_E_UNKNOWN_MODEL.    */
+int rs_model_builtin(const char* name, rs_model_desc* out);
+/* zoo_names() — model_zoo.cpp:172-175. Writes up to `cap` names.           */
+int rs_zoo_names(const char** names, int cap, int* count);
+/* ModelSpec::validate() — model_zoo.cpp:41-59. RS_E_INVALID.               */
+int rs_model_validate(const rs_model_desc* m);
+/* work(m, batch) — model_zoo.cpp:177-245. RS_E_INVALID for batch < 1.      */
+int rs_work(const rs_model_desc* m, int64_t batch, rs_work_breakdown* out);
+/* predict_input_dim(m) — model_zoo.cpp:113-137 (anonymous in reference).   */
+int rs_predict_input_dim(const rs_model_desc* m, int64_t* out);
+/* accel_input_bytes(m, S) — proj/src/platform.cpp:105-111.                 */
+int rs_accel_input_bytes(const rs_model_desc* m, int64_t query_size, double* out);
+/* sla_target(name, level) — proj/src/autotune.cpp:73-88 (seconds).        */
+int rs_sla_target(const char* model_name, const char* level, double* out);
+
+/* ---- scheduler interface (host-only) ------------------------------------ */
+/* Routing of one arriving query — the decision in simulate()
+ * (proj/src/sim.cpp:178-188): offload iff threshold > 0 && S > threshold
+ * (strictly greater); otherwise floor(S/B) requests of B items then one of
+ * S mod B. `threshold` <= 0 encodes an absent std::optional. On return
+ * *offload is 0/1; when 0, requests[0..*n_requests) hold the request sizes
+ * in FIFO push order. RS_E_CAPACITY if more than `cap` requests.           */
+int rs_route(int64_t query_size, int64_t batch_size, int64_t threshold,
+             int32_t* offload, int64_t* requests, int64_t cap,
+             int64_t* n_requests);
+
+/* Query streams — gen_trace() (proj/src/loadgen.cpp:106-125) with the
+ * SizeDistribution kinds of loadgen.hpp:23-45; bit-identical to the
+ * reference for identical (seed, parameters) (mt19937_64, rng.hpp:14-48).  */
+enum {
+  RS_DIST_FIXED = 0,
+  RS_DIST_NORMAL = 1,
+  RS_DIST_LOGNORMAL = 2,
+  RS_DIST_PRODUCTION_HEAVY_TAIL = 3
+};
+typedef struct rs_size_dist {
+  int32_t kind;      /* RS_DIST_*                                           */
+  double p0, p1, p2, p3;
+  int64_t max_size;
+} rs_size_dist;
+/* SizeDistribution::production_heavy_tail() (loadgen.cpp:15-23).           */
+int rs_dist_production(rs_size_dist* out);
+int rs_gen_trace(uint64_t seed, double lambda, const rs_size_dist* dist,
+                 int64_t n, double* arrival_times, int64_t* sizes);
+
+/* QPS under a p95 SLA for a FIFO server pool fed by a trace whose per-query
+ * service times are given (measured on the device). Mirrors the search of
+ * max_qps_under_sla (proj/src/sim.cpp:246-290): evaluate lambda=1, then
+ * `hi`, then geometric bisection to 1%; p95 is the exact order statistic
+ * of summarize() (sim.cpp:217-235) over post-warmup queries.
+ * `service_s[i]` is the service time of query i of the *base* trace; each
+ * evaluation re-times the same size sequence with Poisson gaps at the new
+ * rate (seed base_seed + eval index, as sim.cpp:253). `servers` FIFO
+ * replicas; dispatch = least outstanding work, ties to lowest index.        */
+typedef struct rs_qps_result {
+  double qps;        /* achieved QPS of the accepted evaluation            */
+  double at_lambda;  /* offered rate that met the SLA (0 if none)           */
+  double p95;        /* seconds                                             */
+  double p50;
+  int32_t evaluations;
+} rs_qps_result;
+int rs_qps_under_sla(const double* service_s, int64_t n, int32_t servers,
+                     double sla_s, double warmup_fraction, uint64_t base_seed,
+                     double lambda_hi, rs_qps_result* out);
+
+/* ---- the accelerator (B200) --------------------------------------------- */
+typedef struct rs_accel rs_accel;
+
+enum {
+  RS_FC_FP32 = 0,  /* FFMA fp32 path (tight parity)                        */
+  RS_FC_TF32 = 1,  /* tcgen05 kind::tf32 (fp32 operands, fp32 accumulate)   */
+  RS_FC_AUTO = 2   /* tcgen05 where the layer shape fills a tile, else FFMA */
+};
+enum { RS_RNN_GRU = 0, RS_RNN_AUGRU = 1 };
+
+/* Deterministic initialisation and capacity. `rows_per_table` is kept
+ * OUTSIDE the model descriptor because recsim::ModelSpec has no row count
+ * (SURVEY.md §0.3 D1).                                                      */
+typedef struct rs_init_desc {
+  uint64_t seed;
+  int64_t rows_per_table;
+  int64_t max_query_size;   /* scratch capacity, items (reference max 1000) */
+  int32_t fc_mode;          /* RS_FC_*                                       */
+  int32_t rnn_cell;         /* RS_RNN_* (AttentionRNN only)                  */
+  int32_t l2_persist_mb;    /* >0: L2 persisting window over table rows     */
+  int32_t reserved;
+} rs_init_desc;
+
+/* One query: S items. dense f32[S * dense_input_dim] and indices
+ * i64[S * num_tables * lookups_per_table] (item-major, then table, then
+ * lookup) — the byte model of accel_input_bytes (platform.cpp:105-111).
+ * location RS_MEM_HOST: pointers are host memory (pinned for async copy);
+ * RS_MEM_DEVICE: pointers are device memory on the handle's GPU.           */
+enum { RS_MEM_HOST = 0, RS_MEM_DEVICE = 1 };
+typedef struct rs_query {
+  int64_t size;
+  const float* dense;
+  const int64_t* indices;
+  int32_t location;
+  int32_t reserved;
+} rs_query;
+
+/* Per-call timing (CUDA events on the call's stream), milliseconds.        */
+typedef struct rs_timing {
+  double h2d_ms;
+  double compute_ms;
+  double d2h_ms;
+  double total_ms;
+} rs_timing;
+
+typedef struct rs_accel_info {
+  int32_t device;
+  int32_t sm_count;
+  int32_t kernels_per_forward;     /* kernel nodes in one forward graph    */
+  int32_t fc_layers_tcgen05;       /* FC layers routed to tcgen05          */
+  int64_t predict_input_dim;
+  int64_t output_dim;              /* per item: stacks * last predict dim  */
+  int64_t pooled_dim;              /* per item: rs_pooled width            */
+  int64_t table_bytes;
+  int64_t weight_bytes;
+  int64_t l2_bytes;
+} rs_accel_info;
+
+/* Create one model replica on one GPU: allocate and initialise tables and
+ * weights on the device (seeded). One handle = one model
+ * on one device. Replaces the AcceleratorSpec value that the reference
+ * passes around (platform.hpp:48-58).                                       */
+int rs_accel_create(const rs_model_desc* model, const rs_init_desc* init,
+                    int device, rs_accel** out);
+int rs_accel_destroy(rs_accel* a);
+int rs_accel_info_get(const rs_accel* a, rs_accel_info* out);
+
+/* Whole-query forward: the real execution behind accel_service_time
+ * (platform.cpp:113-136). Writes logits f32[S * stacks * out_dim] to `out`
+ * (same location kind as the query). `stream` is a cudaStream_t (NULL =
+ * the handle's own stream). When `timing` is non-NULL the call records
+ * events and waits for completion; otherwise it is asynchronous on
+ * `stream` and the caller owns synchronisation. Inputs and outputs must
+ * stay valid until the stream reaches the end of this call.                */
+int rs_forward(rs_accel* a, const rs_query* q, float* out, void* stream,
+               rs_timing* timing);
+
+/* Embedding stage only (parity hook): writes the pooled sparse features
+ * f32[S * pooled_dim] — [S,T,D] sums (Sum), [S,T*L*D] (Concat),
+ * [S,T,D] attention-weighted sums (AttentionFC), [S,T,h] final GRU
+ * states (AttentionRNN).                                                    */
+int rs_pooled(rs_accel* a, const rs_query* q, float* out, void* stream,
+              rs_timing* timing);
+
+/* Measured whole-query service time for S items (seconds), memoised per S
+ * like the accel_time cache of simulate() (proj/src/sim.cpp:81-88):
+ * host-staged synthetic inputs, H2D + forward + D2H, median of 5 runs.     */
+int rs_service_time(rs_accel* a, int64_t query_size, double* seconds);
+
+/* Synthetic query inputs: dense U(-1,1), indices uniform in
+ * [0, rows_per_table), a pure function of (seed, query_id).                */
+int rs_fill_query(const rs_model_desc* m, int64_t rows_per_table,
+                  uint64_t seed, uint64_t query_id, int64_t size,
+                  float* dense, int64_t* indices);
+
+/* Pinned host memory for rs_query buffers.                                  */
+int rs_alloc_pinned(size_t bytes, void** out);
+int rs_free_pinned(void* p);
+
+int rs_device_count(int* out);
+const char* rs_last_error(void);
+int rs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RS_ACCEL_H */

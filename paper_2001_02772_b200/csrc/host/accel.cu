@@ -1,0 +1,634 @@
+// accel.cu — rs_accel: one model replica on one B200, behind the C-ABI of
+// include/rs_accel.h. Replaces the modeled accelerator of the reference
+// (AcceleratorSpec + accel_service_time, proj/include/recsim/platform.hpp:48-68,
+// proj/src/platform.cpp:113-136) with real execution.
+//
+// Execution model:
+//  * tables and weights are device-resident for the handle's lifetime
+//    (one allocation for all T tables, [T][rows][D] fp32);
+//  * each CUDA stream that calls in gets a scratch SLOT (staging buffers,
+//    activations, a device query descriptor) and a CUDA graph captured once
+//    for that slot. All kernels read the item count S from the device
+//    descriptor, so one graph serves every query size <= max_query_size;
+//  * a call = async H2D of the query's dense features and indices (pinned
+//    host memory) + 16-byte descriptor update + cudaGraphLaunch + async D2H
+//    of the logits and the error word, all on the caller's stream.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "../kernels/common.cuh"
+#include "../kernels/kernels.hpp"
+#include "internal.hpp"
+
+namespace rs {
+bool gru_supported(int D, int H);
+
+namespace {
+
+#define RS_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      raise(e_ == cudaErrorMemoryAllocation ? RS_E_OOM : RS_E_CUDA,                    \
+            std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+
+constexpr int kDescRing = 256;
+
+struct FcLayer {
+  int64_t in = 0, out = 0, ldk = 0;
+  int relu = 0;
+  int batch = 1;
+  float* W = nullptr;  // [batch][out][ldk]
+  float* b = nullptr;  // [batch][out]
+};
+
+struct Slot {
+  cudaStream_t cap = nullptr;  // capture stream
+  QDesc* d_q = nullptr;
+  QDesc* h_q = nullptr;        // pinned ring [kDescRing]
+  int ring = 0;
+  int* d_err = nullptr;
+  int* h_err = nullptr;        // pinned ring [kDescRing]
+  float* dense_stage = nullptr;
+  int64_t* idx_stage = nullptr;
+  float* act[2] = {nullptr, nullptr};
+  float* pooled = nullptr;
+  float* X = nullptr;
+  float* pact[2] = {nullptr, nullptr};
+  float* out = nullptr;
+  cudaGraphExec_t fwd = nullptr, pool = nullptr;
+  int fwd_kernels = 0, tc_layers = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<void*> allocs;
+};
+
+}  // namespace
+}  // namespace rs
+
+struct rs_accel {
+  rs_model_desc m{};
+  rs_init_desc init{};
+  int device = 0;
+  int sm_count = 0;
+  int64_t l2_bytes = 0;
+  cudaStream_t own = nullptr;
+  // geometry
+  int64_t T = 0, L = 0, D = 0, H = 0, stacks = 1;
+  int64_t dense_in = 0, ld_dense = 0, dense_out = 0;
+  int64_t p_in = 0, ld_x = 0, out_dim = 0, out_w = 0;
+  int64_t pooled_dim = 0;
+  int64_t max_dense_w = 0, max_pred_w = 0;
+  // device state
+  float* tables = nullptr;
+  std::vector<rs::FcLayer> dense_layers, pred_layers;
+  float* att_w = nullptr;
+  float *gru_wih = nullptr, *gru_whh = nullptr, *gru_bih = nullptr, *gru_bhh = nullptr,
+        *gru_watt = nullptr;
+  std::vector<void*> allocs;
+  int64_t table_bytes = 0, weight_bytes = 0;
+  std::mutex mu;
+  std::map<cudaStream_t, std::unique_ptr<rs::Slot>> slots;
+  std::map<int64_t, double> service_memo;
+};
+
+namespace rs {
+namespace {
+
+void* dmalloc(rs_accel* a, std::vector<void*>& list, size_t bytes, bool zero = true) {
+  void* p = nullptr;
+  RS_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  list.push_back(p);
+  if (zero) RS_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+  (void)a;
+  return p;
+}
+
+void upload(void* dst, const std::vector<float>& v) {
+  RS_CUDA(cudaMemcpy(dst, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+float fan_bound(int64_t fan_in) { return 1.0f / sqrtf(static_cast<float>(fan_in)); }
+
+// Weights and biases of one FC stack layer, [batch][out][ldk] with zero pad.
+FcLayer make_layer(rs_accel* a, int64_t in, int64_t out, int relu, int batch,
+                   uint64_t (*wid)(int64_t, int64_t), uint64_t (*bid)(int64_t, int64_t),
+                   int64_t layer) {
+  FcLayer f;
+  f.in = in; f.out = out; f.ldk = round_up(in, 4); f.relu = relu; f.batch = batch;
+  const float bound = fan_bound(in);
+  std::vector<float> w((size_t)(batch * out * f.ldk), 0.f), b((size_t)(batch * out));
+  for (int z = 0; z < batch; ++z) {
+    const uint64_t kw = stream_key(a->init.seed, wid(z, layer));
+    const uint64_t kb = stream_key(a->init.seed, bid(z, layer));
+    for (int64_t o = 0; o < out; ++o) {
+      for (int64_t i = 0; i < in; ++i)
+        w[(size_t)((z * out + o) * f.ldk + i)] = param(kw, (uint64_t)(o * in + i), bound);
+      b[(size_t)(z * out + o)] = param(kb, (uint64_t)o, bound);
+    }
+  }
+  f.W = static_cast<float*>(dmalloc(a, a->allocs, w.size() * sizeof(float), false));
+  f.b = static_cast<float*>(dmalloc(a, a->allocs, b.size() * sizeof(float), false));
+  upload(f.W, w);
+  upload(f.b, b);
+  a->weight_bytes += (int64_t)((w.size() + b.size()) * sizeof(float));
+  return f;
+}
+
+uint64_t dense_wid(int64_t, int64_t l) { return id_dense_w(l); }
+uint64_t dense_bid(int64_t, int64_t l) { return id_dense_b(l); }
+uint64_t pred_wid(int64_t s, int64_t l) { return id_pred_w(s, l); }
+uint64_t pred_bid(int64_t s, int64_t l) { return id_pred_b(s, l); }
+
+std::vector<float> fill_param(uint64_t seed, uint64_t id, int64_t n, float bound) {
+  std::vector<float> v((size_t)n);
+  const uint64_t k = stream_key(seed, id);
+  for (int64_t i = 0; i < n; ++i) v[(size_t)i] = param(k, (uint64_t)i, bound);
+  return v;
+}
+
+void build_model(rs_accel* a) {
+  const rs_model_desc& m = a->m;
+  a->T = m.num_tables;
+  a->L = m.lookups_per_table;
+  a->D = m.embedding_dim;
+  a->H = m.recurrent_hidden_dim;
+  a->stacks = m.num_parallel_predict_stacks;
+  a->dense_in = m.dense_input_dim;
+  a->ld_dense = round_up(std::max<int64_t>(a->dense_in, 1), 4);
+  a->dense_out = dense_out_dim(m);
+  a->p_in = predict_input_dim(m);
+  a->ld_x = round_up(a->p_in, 4);
+  a->out_dim = m.predict_fc.dims[m.predict_fc.n - 1];
+  a->out_w = a->stacks * a->out_dim;
+  switch (m.pooling) {
+    case RS_POOL_SUM: a->pooled_dim = a->T * a->D; break;
+    case RS_POOL_CONCAT: a->pooled_dim = a->T * a->L * a->D; break;
+    case RS_POOL_ATTENTION_FC: a->pooled_dim = a->T * a->D; break;
+    case RS_POOL_ATTENTION_RNN: a->pooled_dim = a->T * a->H; break;
+  }
+  if (m.pooling == RS_POOL_SUM && m.has_dense_fc && a->T > 0 && a->dense_out != a->D)
+    raise(RS_E_INVALID,
+          "dot interaction needs the dense stack output width to equal embedding_dim "
+          "(SURVEY.md D2; the reference never checks this)");
+  if (m.pooling == RS_POOL_ATTENTION_FC && a->T > 0 && !din_supported(a->D))
+    raise(RS_E_INVALID, "AttentionFC requires a power-of-two embedding_dim");
+  if (m.pooling == RS_POOL_ATTENTION_RNN && a->T > 0 && !gru_supported((int)a->D, (int)a->H))
+    raise(RS_E_INVALID, "AttentionRNN shape unsupported (needs embedding_dim % 4 == 0)");
+  if (a->T > 0 && a->init.rows_per_table < 1) raise(RS_E_INVALID, "rows_per_table < 1");
+
+  // tables
+  if (a->T > 0) {
+    a->table_bytes = a->T * a->init.rows_per_table * a->D * (int64_t)sizeof(float);
+    a->tables = static_cast<float*>(dmalloc(a, a->allocs, (size_t)a->table_bytes, false));
+    launch_init_tables(a->tables, a->T, a->init.rows_per_table, a->D, a->init.seed,
+                       a->sm_count, a->own);
+    RS_CUDA(cudaGetLastError());
+  }
+  // dense stack: ReLU after every layer (DLRM bottom MLP)
+  if (m.has_dense_fc) {
+    int64_t in = a->dense_in;
+    for (int l = 0; l < m.dense_fc.n; ++l) {
+      a->dense_layers.push_back(make_layer(a, in, m.dense_fc.dims[l], 1, 1, dense_wid, dense_bid, l));
+      in = m.dense_fc.dims[l];
+      a->max_dense_w = std::max(a->max_dense_w, round_up(in, 4));
+    }
+  }
+  // predict stacks: ReLU on hidden layers, identity on the last (logits)
+  {
+    int64_t in = a->p_in;
+    for (int l = 0; l < m.predict_fc.n; ++l) {
+      const int relu = l + 1 < m.predict_fc.n ? 1 : 0;
+      a->pred_layers.push_back(make_layer(a, in, m.predict_fc.dims[l], relu, (int)a->stacks,
+                                          pred_wid, pred_bid, l));
+      in = m.predict_fc.dims[l];
+      a->max_pred_w = std::max(a->max_pred_w, round_up(in, 4));
+    }
+  }
+  if (m.pooling == RS_POOL_ATTENTION_FC && a->T > 0) {
+    std::vector<float> w;
+    for (int64_t t = 0; t < a->T; ++t) {
+      auto v = fill_param(a->init.seed, id_att_w(t), a->D * a->D, fan_bound(a->D));
+      w.insert(w.end(), v.begin(), v.end());
+    }
+    a->att_w = static_cast<float*>(dmalloc(a, a->allocs, w.size() * 4, false));
+    upload(a->att_w, w);
+    a->weight_bytes += (int64_t)w.size() * 4;
+  }
+  if (m.pooling == RS_POOL_ATTENTION_RNN && a->T > 0) {
+    const int64_t H3 = 3 * a->H;
+    std::vector<float> wih, whh, bih, bhh, watt;
+    for (int64_t t = 0; t < a->T; ++t) {
+      auto p0 = fill_param(a->init.seed, id_gru(t, 0), H3 * a->D, fan_bound(a->H));
+      auto p1 = fill_param(a->init.seed, id_gru(t, 1), H3 * a->H, fan_bound(a->H));
+      auto p2 = fill_param(a->init.seed, id_gru(t, 2), H3, fan_bound(a->H));
+      auto p3 = fill_param(a->init.seed, id_gru(t, 3), H3, fan_bound(a->H));
+      auto p4 = fill_param(a->init.seed, id_gru(t, 4), a->D * a->D, fan_bound(a->D));
+      wih.insert(wih.end(), p0.begin(), p0.end());
+      whh.insert(whh.end(), p1.begin(), p1.end());
+      bih.insert(bih.end(), p2.begin(), p2.end());
+      bhh.insert(bhh.end(), p3.begin(), p3.end());
+      watt.insert(watt.end(), p4.begin(), p4.end());
+    }
+    auto put = [&](float*& dst, const std::vector<float>& v) {
+      dst = static_cast<float*>(dmalloc(a, a->allocs, v.size() * 4, false));
+      upload(dst, v);
+      a->weight_bytes += (int64_t)v.size() * 4;
+    };
+    put(a->gru_wih, wih); put(a->gru_whh, whh); put(a->gru_bih, bih);
+    put(a->gru_bhh, bhh); put(a->gru_watt, watt);
+  }
+  if (m.pooling == RS_POOL_SUM && a->T > 0) {
+    const size_t smem = interaction_smem((int)a->T, (int)a->D);
+    if (smem > 200 * 1024) raise(RS_E_INVALID, "too many tables for the interaction kernel");
+  }
+  RS_CUDA(cudaStreamSynchronize(a->own));
+}
+
+GruArgs gru_args(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off) {
+  GruArgs g{};
+  g.tables = a->tables; g.rows = a->init.rows_per_table;
+  g.T = (int)a->T; g.L = (int)a->L; g.D = (int)a->D; g.H = (int)a->H;
+  g.w_ih = a->gru_wih; g.w_hh = a->gru_whh; g.b_ih = a->gru_bih; g.b_hh = a->gru_bhh;
+  g.w_att = a->gru_watt; g.augru = a->init.rnn_cell == RS_RNN_AUGRU ? 1 : 0;
+  g.out = out; g.ld_out = ld; g.col_off = off; g.err = s->d_err;
+  return g;
+}
+
+// Enqueue the pooling stage writing into out[item*ld + off ...].
+void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off,
+                     cudaStream_t st) {
+  const rs_model_desc& m = a->m;
+  const int64_t maxS = a->init.max_query_size;
+  const int64_t rows = a->init.rows_per_table;
+  if (a->T == 0) return;
+  switch (m.pooling) {
+    case RS_POOL_SUM:
+      launch_sls_sum(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out + off, ld,
+                     s->d_err, maxS, a->sm_count, st);
+      break;
+    case RS_POOL_CONCAT:
+      launch_gather_concat(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out, ld,
+                           off, s->d_err, maxS, a->sm_count, st);
+      break;
+    case RS_POOL_ATTENTION_FC:
+      launch_din_pool(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, a->att_w, out,
+                      ld, off, s->d_err, maxS, a->sm_count, st);
+      break;
+    case RS_POOL_ATTENTION_RNN: {
+      GruArgs g = gru_args(a, s, out, ld, off);
+      launch_gru(s->d_q, g, maxS, a->sm_count, st);
+      break;
+    }
+  }
+}
+
+// One FC stack: layer l reads `in` and writes the next buffer; the last layer
+// writes `final_out`.
+int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, const float* in0,
+                  int64_t ld_in0, int64_t in0_rows, float* const* tmp, int64_t ld_tmp,
+                  float* final_out, int64_t ld_final, int64_t final_sCz, cudaStream_t st) {
+  const int64_t maxS = a->init.max_query_size;
+  int tc_count = 0;
+  const float* in = in0;
+  int64_t lda = ld_in0, sAz = 0, a_rows = in0_rows;
+  for (size_t l = 0; l < layers.size(); ++l) {
+    const FcLayer& f = layers[l];
+    const bool last = l + 1 == layers.size();
+    FcArgs args{};
+    args.A = in; args.lda = lda; args.sAz = sAz;
+    args.W = f.W; args.ldw = f.ldk; args.sWz = f.out * f.ldk;
+    args.bias = f.b; args.sbz = f.out;
+    if (last) {
+      args.C = final_out; args.ldc = ld_final; args.sCz = final_sCz;
+    } else {
+      args.C = tmp[l & 1]; args.ldc = ld_tmp; args.sCz = maxS * ld_tmp;
+    }
+    args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
+    bool used_tc = false;
+    if (a->init.fc_mode != RS_FC_FP32 && tc_available()) {
+      TcPlan p;
+      if (tc_plan(&p, args, maxS, a_rows)) {
+        launch_fc_tc(s->d_q, p, args, st);
+        used_tc = true;
+        ++tc_count;
+      }
+    }
+    if (!used_tc) launch_fc_ffma(s->d_q, args, maxS, st);
+    in = args.C; lda = args.ldc; sAz = args.sCz; a_rows = maxS;
+  }
+  return tc_count;
+}
+
+cudaGraphExec_t capture(rs_accel* a, Slot* s, bool full, int* kernels, int* tc_layers) {
+  cudaStream_t st = s->cap;
+  cudaGraph_t g = nullptr;
+  RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const rs_model_desc& m = a->m;
+  const int64_t maxS = a->init.max_query_size;
+  int tc = 0;
+  cudaMemsetAsync(s->d_err, 0, sizeof(int), st);
+  if (!full) {
+    enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, st);
+  } else {
+    if (m.has_dense_fc)
+      tc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
+                          a->max_dense_w, s->X, a->ld_x, 0, st);
+    if (m.pooling == RS_POOL_SUM) {
+      if (a->T > 0) {
+        enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, st);
+        launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
+                           a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
+                           a->sm_count, st);
+      }
+    } else {
+      enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, st);
+    }
+    tc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w, s->out,
+                        a->out_w, a->out_dim, st);
+  }
+  cudaError_t le = cudaGetLastError();
+  cudaError_t ce = cudaStreamEndCapture(st, &g);
+  if (le != cudaSuccess) raise(RS_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
+  if (ce != cudaSuccess) raise(RS_E_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+  size_t n = 0;
+  RS_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  RS_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    RS_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty == cudaGraphNodeTypeKernel) ++k;
+  }
+  cudaGraphExec_t exec = nullptr;
+  RS_CUDA(cudaGraphInstantiate(&exec, g, 0));
+  RS_CUDA(cudaGraphDestroy(g));
+  if (kernels) *kernels = k;
+  if (tc_layers) *tc_layers = tc;
+  return exec;
+}
+
+Slot* get_slot(rs_accel* a, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(a->mu);
+  auto it = a->slots.find(st);
+  if (it != a->slots.end()) return it->second.get();
+  RS_CUDA(cudaSetDevice(a->device));
+  auto s = std::make_unique<Slot>();
+  const int64_t maxS = a->init.max_query_size;
+  RS_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
+  s->d_q = static_cast<QDesc*>(dmalloc(a, s->allocs, sizeof(QDesc)));
+  RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_q), sizeof(QDesc) * kDescRing,
+                        cudaHostAllocPortable));
+  RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_err), sizeof(int) * kDescRing,
+                        cudaHostAllocPortable));
+  std::memset(s->h_err, 0, sizeof(int) * kDescRing);
+  s->d_err = static_cast<int*>(dmalloc(a, s->allocs, sizeof(int)));
+  s->dense_stage = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_dense * 4)));
+  s->idx_stage = static_cast<int64_t*>(
+      dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->T * a->L, 1) * 8)));
+  for (int i = 0; i < 2; ++i) {
+    s->act[i] = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->max_dense_w, 4) * 4)));
+    s->pact[i] = static_cast<float*>(dmalloc(
+        a, s->allocs, (size_t)(a->stacks * maxS * std::max<int64_t>(a->max_pred_w, 4) * 4)));
+  }
+  s->pooled = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->pooled_dim, 1) * 4)));
+  s->X = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_x * 4)));
+  s->out = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->out_w * 4)));
+  for (auto& e : s->ev) RS_CUDA(cudaEventCreate(&e));
+  RS_CUDA(cudaDeviceSynchronize());
+  s->fwd = capture(a, s.get(), true, &s->fwd_kernels, &s->tc_layers);
+  s->pool = capture(a, s.get(), false, nullptr, nullptr);
+  Slot* raw = s.get();
+  a->slots.emplace(st, std::move(s));
+  return raw;
+}
+
+void free_slot(Slot* s) {
+  if (s->fwd) cudaGraphExecDestroy(s->fwd);
+  if (s->pool) cudaGraphExecDestroy(s->pool);
+  for (auto e : s->ev) if (e) cudaEventDestroy(e);
+  for (void* p : s->allocs) cudaFree(p);
+  if (s->h_q) cudaFreeHost(s->h_q);
+  if (s->h_err) cudaFreeHost(s->h_err);
+  if (s->cap) cudaStreamDestroy(s->cap);
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* timing,
+        bool full) {
+  return guarded([&] {
+    if (!a || !q || !out) raise(RS_E_INVALID, "null argument");
+    if (q->size < 1) raise(RS_E_INVALID, "query_size < 1");
+    if (q->size > a->init.max_query_size)
+      raise(RS_E_CAPACITY, "query larger than max_query_size");
+    if (q->location != RS_MEM_HOST && q->location != RS_MEM_DEVICE)
+      raise(RS_E_INVALID, "bad memory location");
+    RS_CUDA(cudaSetDevice(a->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->own;
+    Slot* s = get_slot(a, st);
+    const int64_t S = q->size;
+    const bool host = q->location == RS_MEM_HOST;
+    const cudaMemcpyKind in_kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind out_kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (timing) RS_CUDA(cudaEventRecord(s->ev[0], st));
+    // dense features: into the bottom-MLP staging buffer, or straight into
+    // the predict input X[:, 0:dense_in] when there is no dense stack
+    if (full && a->dense_in > 0) {
+      if (!q->dense) raise(RS_E_INVALID, "null dense features");
+      float* dst = a->m.has_dense_fc ? s->dense_stage : s->X;
+      const int64_t ld = a->m.has_dense_fc ? a->ld_dense : a->ld_x;
+      if (ld == a->dense_in)
+        RS_CUDA(cudaMemcpyAsync(dst, q->dense, (size_t)(S * a->dense_in * 4), in_kind, st));
+      else
+        RS_CUDA(cudaMemcpy2DAsync(dst, (size_t)(ld * 4), q->dense, (size_t)(a->dense_in * 4),
+                                  (size_t)(a->dense_in * 4), (size_t)S, in_kind, st));
+    }
+    const int64_t* idx = nullptr;
+    if (a->T > 0) {
+      if (!q->indices) raise(RS_E_INVALID, "null indices");
+      if (host) {
+        RS_CUDA(cudaMemcpyAsync(s->idx_stage, q->indices, (size_t)(S * a->T * a->L * 8),
+                                cudaMemcpyHostToDevice, st));
+        idx = s->idx_stage;
+      } else {
+        idx = q->indices;
+      }
+    }
+    const int slot_i = s->ring;
+    s->ring = (s->ring + 1) % kDescRing;
+    s->h_q[slot_i].S = S;
+    s->h_q[slot_i].idx = idx;
+    RS_CUDA(cudaMemcpyAsync(s->d_q, &s->h_q[slot_i], sizeof(QDesc), cudaMemcpyHostToDevice, st));
+    if (timing) RS_CUDA(cudaEventRecord(s->ev[1], st));
+    RS_CUDA(cudaGraphLaunch(full ? s->fwd : s->pool, st));
+    if (timing) RS_CUDA(cudaEventRecord(s->ev[2], st));
+    const int64_t w = full ? a->out_w : a->pooled_dim;
+    const float* src = full ? s->out : s->pooled;
+    RS_CUDA(cudaMemcpyAsync(out, src, (size_t)(S * w * 4), out_kind, st));
+    RS_CUDA(cudaMemcpyAsync(&s->h_err[slot_i], s->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (timing) {
+      RS_CUDA(cudaEventRecord(s->ev[3], st));
+      RS_CUDA(cudaEventSynchronize(s->ev[3]));
+      timing->h2d_ms = elapsed(s->ev[0], s->ev[1]);
+      timing->compute_ms = elapsed(s->ev[1], s->ev[2]);
+      timing->d2h_ms = elapsed(s->ev[2], s->ev[3]);
+      timing->total_ms = elapsed(s->ev[0], s->ev[3]);
+      if (s->h_err[slot_i] & kErrIndex)
+        raise(RS_E_INDEX, "embedding index outside [0, rows_per_table)");
+    }
+  });
+}
+
+}  // namespace
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" int rs_device_count(int* out) {
+  return guarded([&] {
+    if (!out) raise(RS_E_INVALID, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    *out = n;
+  });
+}
+
+extern "C" int rs_alloc_pinned(size_t bytes, void** out) {
+  return guarded([&] {
+    if (!out) raise(RS_E_INVALID, "null argument");
+    RS_CUDA(cudaHostAlloc(out, std::max<size_t>(bytes, 16), cudaHostAllocPortable));
+  });
+}
+
+extern "C" int rs_free_pinned(void* p) {
+  return guarded([&] {
+    if (p) RS_CUDA(cudaFreeHost(p));
+  });
+}
+
+extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* init, int device,
+                               rs_accel** out) {
+  rs_accel* a = nullptr;
+  int rc = guarded([&] {
+    if (!model || !init || !out) raise(RS_E_INVALID, "null argument");
+    *out = nullptr;
+    validate_model(*model);
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      raise(RS_E_NO_DEVICE, "no CUDA device visible");
+    if (device < 0 || device >= n) raise(RS_E_NO_DEVICE, "device ordinal out of range");
+    cudaDeviceProp prop;
+    RS_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      raise(RS_E_NO_DEVICE, "this library is built for sm_100a (B200) only");
+    if (init->max_query_size < 1) raise(RS_E_INVALID, "max_query_size < 1");
+    if (init->fc_mode < RS_FC_FP32 || init->fc_mode > RS_FC_AUTO)
+      raise(RS_E_INVALID, "bad fc_mode");
+    RS_CUDA(cudaSetDevice(device));
+    a = new rs_accel();
+    a->m = *model;
+    a->init = *init;
+    a->device = device;
+    a->sm_count = prop.multiProcessorCount;
+    a->l2_bytes = prop.l2CacheSize;
+    RS_CUDA(cudaStreamCreateWithFlags(&a->own, cudaStreamNonBlocking));
+    build_model(a);
+    *out = a;
+  });
+  if (rc != RS_OK && a) {
+    for (void* p : a->allocs) cudaFree(p);
+    if (a->own) cudaStreamDestroy(a->own);
+    delete a;
+  }
+  return rc;
+}
+
+extern "C" int rs_accel_destroy(rs_accel* a) {
+  return guarded([&] {
+    if (!a) return;
+    cudaSetDevice(a->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : a->slots) free_slot(kv.second.get());
+    a->slots.clear();
+    for (void* p : a->allocs) cudaFree(p);
+    if (a->own) cudaStreamDestroy(a->own);
+    delete a;
+  });
+}
+
+extern "C" int rs_accel_info_get(const rs_accel* ca, rs_accel_info* out) {
+  return guarded([&] {
+    if (!ca || !out) raise(RS_E_INVALID, "null argument");
+    rs_accel* a = const_cast<rs_accel*>(ca);
+    Slot* s = get_slot(a, a->own);
+    rs_accel_info i{};
+    i.device = a->device;
+    i.sm_count = a->sm_count;
+    i.kernels_per_forward = s->fwd_kernels;
+    i.fc_layers_tcgen05 = s->tc_layers;
+    i.predict_input_dim = a->p_in;
+    i.output_dim = a->out_w;
+    i.pooled_dim = a->pooled_dim;
+    i.table_bytes = a->table_bytes;
+    i.weight_bytes = a->weight_bytes;
+    i.l2_bytes = a->l2_bytes;
+    *out = i;
+  });
+}
+
+extern "C" int rs_forward(rs_accel* a, const rs_query* q, float* out, void* stream,
+                          rs_timing* timing) {
+  return run(a, q, out, stream, timing, true);
+}
+
+extern "C" int rs_pooled(rs_accel* a, const rs_query* q, float* out, void* stream,
+                         rs_timing* timing) {
+  return run(a, q, out, stream, timing, false);
+}
+
+extern "C" int rs_service_time(rs_accel* a, int64_t query_size, double* seconds) {
+  return guarded([&] {
+    if (!a || !seconds) raise(RS_E_INVALID, "null argument");
+    if (query_size < 1) raise(RS_E_INVALID, "query_size < 1");
+    {
+      std::lock_guard<std::mutex> lock(a->mu);
+      auto it = a->service_memo.find(query_size);
+      if (it != a->service_memo.end()) {
+        *seconds = it->second;
+        return;
+      }
+    }
+    const int64_t S = query_size;
+    void *dense = nullptr, *idx = nullptr, *out = nullptr;
+    RS_CUDA(cudaHostAlloc(&dense, (size_t)std::max<int64_t>(S * a->dense_in * 4, 16), 0));
+    RS_CUDA(cudaHostAlloc(&idx, (size_t)std::max<int64_t>(S * a->T * a->L * 8, 16), 0));
+    RS_CUDA(cudaHostAlloc(&out, (size_t)(S * a->out_w * 4), 0));
+    std::vector<double> t;
+    int rc = rs_fill_query(&a->m, a->init.rows_per_table, a->init.seed ^ 0x5E41CEull, 0, S,
+                           static_cast<float*>(dense), static_cast<int64_t*>(idx));
+    for (int i = 0; rc == RS_OK && i < 6; ++i) {
+      rs_query q{S, static_cast<float*>(dense), static_cast<int64_t*>(idx), RS_MEM_HOST, 0};
+      rs_timing tm{};
+      rc = rs_forward(a, &q, static_cast<float*>(out), nullptr, &tm);
+      if (i > 0) t.push_back(tm.total_ms * 1e-3);
+    }
+    cudaFreeHost(dense); cudaFreeHost(idx); cudaFreeHost(out);
+    if (rc != RS_OK) raise(rc, rs_last_error());
+    std::sort(t.begin(), t.end());
+    const double med = t[t.size() / 2];
+    std::lock_guard<std::mutex> lock(a->mu);
+    a->service_memo[query_size] = med;
+    *seconds = med;
+  });
+}

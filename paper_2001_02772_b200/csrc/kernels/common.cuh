@@ -1,0 +1,55 @@
+// common.cuh — device-side shared types and helpers for the sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../spec.h"
+
+namespace rs {
+
+// Device-resident query descriptor. Every kernel of the forward graph reads
+// the item count (and the index pointer) from here, so ONE captured CUDA
+// graph per scratch slot serves every query size up to max_query_size:
+// the grid is sized for capacity and blocks past S exit at once.
+struct QDesc {
+  int64_t S;
+  const int64_t* idx;  // [S, T, L] int64 (device)
+  int64_t pad[2];
+};
+
+// Error bits accumulated by kernels and read back with the logits.
+enum : int { kErrIndex = 1 };
+
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  // Table rows are touched once per query: stream them past L1.
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float ldg_stream1(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+
+__device__ __forceinline__ float4 shfl_xor4(const float4& v, int off) {
+  float4 r;
+  r.x = __shfl_xor_sync(0xffffffffu, v.x, off);
+  r.y = __shfl_xor_sync(0xffffffffu, v.y, off);
+  r.z = __shfl_xor_sync(0xffffffffu, v.z, off);
+  r.w = __shfl_xor_sync(0xffffffffu, v.w, off);
+  return r;
+}
+
+__host__ __device__ __forceinline__ int64_t round_up(int64_t x, int64_t m) {
+  return (x + m - 1) / m * m;
+}
+
+}  // namespace rs

@@ -1,0 +1,418 @@
+// embedding.cu — the HBM-bound half of the offloaded forward pass.
+//
+//   sls_sum        SparseLengthsSum / embedding-bag Sum pooling
+//                  (EmbeddingLookup + Pooling::Sum, proj/src/model_zoo.cpp:192-201)
+//   gather_concat  Pooling::Concat gather into the predict-FC input (:202-206)
+//   din_pool       DIN local-activation attention pooling (AttentionFC, :207-216)
+//   interaction    DLRM pairwise dots + summed embedding (Interaction, :231-238;
+//                  feature layout of predict_input_dim, :113-137)
+//   init_tables    seeded table fill
+//
+// Layout in HBM: all T tables of a model in ONE allocation, [T][rows][D]
+// fp32 row-major, so a row is one contiguous D*4-byte segment (128 B at the
+// zoo's D=32, 256 B at cfg3's D=64). Indices arrive item-major [S][T][L]
+// int64 exactly as the reference's byte model ships them
+// (proj/src/platform.cpp:105-111), so bag (item, t) is L contiguous int64.
+//
+// SLS design: one warp per bag, grid-stride over S*T bags (S read from the
+// device-side query descriptor). The warp stages the bag's index list in
+// shared memory, then reads rows with 128-bit non-allocating loads: LPR =
+// D/4 lanes cover one row, so R = 32/LPR rows land per warp instruction and
+// U unrolled instructions keep R*U rows (R*U*D*4 bytes) in flight per warp.
+// Lane group g accumulates rows g, g+R, g+2R, ... in order; groups combine by
+// an xor-shuffle tree. That order is the canonical SLS summation order that
+// oracle/forward.c restates, so pooled sums are bit-identical to the oracle.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace rs {
+
+namespace {
+
+constexpr int kWarps = 8;      // warps per CTA for warp-per-bag kernels
+constexpr int kIdxChunk = 256; // staged indices per warp per pass
+
+template <int LPR, int VPL, int U>
+__global__ void __launch_bounds__(kWarps * 32)
+sls_sum_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
+               int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err) {
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  __shared__ int64_t sidx[kWarps][kIdxChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t S = qd->S;
+  const int64_t* __restrict__ idx = qd->idx;
+  const int64_t bags = S * T;
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  for (int64_t bag = (int64_t)blockIdx.x * kWarps + warp; bag < bags; bag += stride) {
+    const int t = (int)(bag % T);
+    const float4* __restrict__ tab =
+        reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
+    const int64_t* __restrict__ bidx = idx + bag * L;
+    float4 acc[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < L; c0 += kIdxChunk) {
+      const int n = min(kIdxChunk, L - c0);
+      __syncwarp();
+      for (int l = lane; l < n; l += 32) sidx[warp][l] = __ldg(bidx + c0 + l);
+      __syncwarp();
+      for (int j = 0; j < n; j += R * U) {
+        float4 v[U][VPL];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int l = j + u * R + g;
+          ok[u] = false;
+          if (l < n) {
+            const int64_t r = sidx[warp][l];
+            if ((uint64_t)r < (uint64_t)rows) {
+              ok[u] = true;
+              const float4* p = tab + r * (D / 4) + c;
+#pragma unroll
+              for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream(p + k * LPR);
+            } else {
+              atomicOr(err, kErrIndex);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
+          }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
+    if (g == 0) {
+      float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
+    }
+  }
+}
+
+// Any D (not a power of two in [8,256]): lane-per-column, sequential in l.
+__global__ void __launch_bounds__(kWarps * 32)
+sls_sum_scalar_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
+                      int64_t rows, int T, int L, int D, float* __restrict__ out,
+                      int64_t ld_out, int* __restrict__ err) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bags = qd->S * T;
+  const int64_t* __restrict__ idx = qd->idx;
+  for (int64_t bag = (int64_t)blockIdx.x * kWarps + warp; bag < bags;
+       bag += (int64_t)gridDim.x * kWarps) {
+    const int t = (int)(bag % T);
+    const float* tab = tables + (int64_t)t * rows * D;
+    for (int c = lane; c < D; c += 32) {
+      float acc = 0.f;
+      for (int l = 0; l < L; ++l) {
+        const int64_t r = __ldg(idx + bag * L + l);
+        if ((uint64_t)r < (uint64_t)rows) acc += ldg_stream1(tab + r * D + c);
+        else if (c == lane) atomicOr(err, kErrIndex);
+      }
+      out[(bag / T) * ld_out + (int64_t)t * D + c] = acc;
+    }
+  }
+}
+
+// Concat gather: out[item, col_off + (t*L + l)*D + c] = E_t[idx[item,t,l], c].
+__global__ void __launch_bounds__(256)
+gather_concat_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
+                     int64_t rows, int T, int L, int D, float* __restrict__ out,
+                     int64_t ld_out, int64_t col_off, int vec, int* __restrict__ err) {
+  const int64_t S = qd->S;
+  const int64_t* __restrict__ idx = qd->idx;
+  const int64_t TL = (int64_t)T * L;
+  const int W = vec ? D / 4 : D;  // work units per row
+  const int64_t total = S * TL * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rowi = i / W;      // flat (item, t, l)
+    const int w = (int)(i - rowi * W);
+    const int64_t item = rowi / TL;
+    const int64_t tl = rowi - item * TL;
+    const int t = (int)(tl / L);
+    const int64_t r = __ldg(idx + rowi);
+    float* dst = out + item * ld_out + col_off + tl * D;
+    if ((uint64_t)r >= (uint64_t)rows) {
+      if (w == 0) atomicOr(err, kErrIndex);
+      continue;
+    }
+    const float* src = tables + ((int64_t)t * rows + r) * D;
+    if (vec) {
+      reinterpret_cast<float4*>(dst)[w] = ldg_stream(reinterpret_cast<const float4*>(src) + w);
+    } else {
+      dst[w] = ldg_stream1(src + w);
+    }
+  }
+}
+
+// DIN attention pooling, one warp per (item, table) bag:
+//   q = e_0 (the bag's first lookup is the candidate), weight
+//   a_l = sigmoid(q^T W_t e_l), pooled = sum_l a_l e_l (unnormalised, as DIN).
+// Computed as u = W_t^T q once per bag, then a_l = sigmoid(<u, e_l>): the same
+// bilinear form with 2D flops per lookup instead of 2D^2, which turns the
+// reference's FFMA-bound Attention category (model_zoo.cpp:207-216) into a
+// pure gather at HBM speed.
+template <int LPR, int VPL, int U>
+__global__ void __launch_bounds__(kWarps * 32)
+din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
+                int T, int L, const float* __restrict__ att_w, float* __restrict__ out,
+                int64_t ld_out, int64_t col_off, int* __restrict__ err) {
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  __shared__ int64_t sidx[kWarps][kIdxChunk];
+  __shared__ float sq[kWarps][D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t bags = qd->S * T;
+  const int64_t* __restrict__ idx = qd->idx;
+  for (int64_t bag = (int64_t)blockIdx.x * kWarps + warp; bag < bags;
+       bag += (int64_t)gridDim.x * kWarps) {
+    const int t = (int)(bag % T);
+    const float4* __restrict__ tab =
+        reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
+    const int64_t* __restrict__ bidx = idx + bag * L;
+    // candidate q = row of lookup 0
+    const int64_t r0 = __ldg(bidx);
+    const bool q_ok = (uint64_t)r0 < (uint64_t)rows;
+    if (!q_ok && lane == 0) atomicOr(err, kErrIndex);
+    __syncwarp();
+    for (int i = lane; i < D; i += 32)
+      sq[warp][i] = q_ok ? __ldg(reinterpret_cast<const float*>(tab + r0 * (D / 4)) + i) : 0.f;
+    __syncwarp();
+    // u = W_t^T q for this lane's columns (W_t row-major [D][D], L2-resident)
+    float4 u[VPL];
+    const float* W = att_w + (int64_t)t * D * D;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) u[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < D; ++i) {
+      const float qi = sq[warp][i];
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(W + (int64_t)i * D) + c + k * LPR);
+        u[k].x = fmaf(qi, w.x, u[k].x);
+        u[k].y = fmaf(qi, w.y, u[k].y);
+        u[k].z = fmaf(qi, w.z, u[k].z);
+        u[k].w = fmaf(qi, w.w, u[k].w);
+      }
+    }
+    float4 acc[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < L; c0 += kIdxChunk) {
+      const int n = min(kIdxChunk, L - c0);
+      __syncwarp();
+      for (int l = lane; l < n; l += 32) sidx[warp][l] = __ldg(bidx + c0 + l);
+      __syncwarp();
+      for (int j = 0; j < n; j += R * U) {
+        float4 v[U][VPL];
+        bool ok[U];
+#pragma unroll
+        for (int u2 = 0; u2 < U; ++u2) {
+          const int l = j + u2 * R + g;
+          ok[u2] = false;
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) v[u2][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (l < n) {
+            const int64_t r = sidx[warp][l];
+            if ((uint64_t)r < (uint64_t)rows) {
+              ok[u2] = true;
+              const float4* p = tab + r * (D / 4) + c;
+#pragma unroll
+              for (int k = 0; k < VPL; ++k) v[u2][k] = ldg_stream(p + k * LPR);
+            } else {
+              atomicOr(err, kErrIndex);
+            }
+          }
+        }
+#pragma unroll
+        for (int u2 = 0; u2 < U; ++u2) {
+          float s = 0.f;
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            s = fmaf(u[k].x, v[u2][k].x, s);
+            s = fmaf(u[k].y, v[u2][k].y, s);
+            s = fmaf(u[k].z, v[u2][k].z, s);
+            s = fmaf(u[k].w, v[u2][k].w, s);
+          }
+#pragma unroll
+          for (int off = LPR / 2; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+          s = 1.0f / (1.0f + expf(-s));  // activation-unit weight
+          if (ok[u2]) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+              acc[k].x = fmaf(s, v[u2][k].x, acc[k].x);
+              acc[k].y = fmaf(s, v[u2][k].y, acc[k].y);
+              acc[k].z = fmaf(s, v[u2][k].z, acc[k].z);
+              acc[k].w = fmaf(s, v[u2][k].w, acc[k].w);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
+    if (g == 0) {
+      float* o = out + (bag / T) * ld_out + col_off + (int64_t)t * D;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int cc = (c + k * LPR) * 4;
+        o[cc + 0] = acc[k].x; o[cc + 1] = acc[k].y; o[cc + 2] = acc[k].z; o[cc + 3] = acc[k].w;
+      }
+    }
+  }
+}
+
+// DLRM interaction, one CTA per item (grid-stride):
+//   X[item, sum_off + c]  = sum_{t=1..T} v_t[c]              (sequential in t)
+//   X[item, dot_off + p]  = <v_i, v_j>, i = 1..T, j = 0..i-1  (p = i(i-1)/2 + j)
+// with v_0 = X[item, 0:D] (bottom-MLP output already written there) and
+// v_t = pooled[item, t-1, :]. Pairs exist only when has_dense (the
+// reference counts them only for Sum pooling with a dense stack).
+__global__ void __launch_bounds__(128)
+interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
+                   int64_t ld_pooled, int T, int D, float* __restrict__ X, int64_t ld_x,
+                   int64_t sum_off, int64_t dot_off, int has_dense) {
+  extern __shared__ float sv[];  // [(T+1)][D+1]
+  const int P = has_dense ? (T + 1) * T / 2 : 0;
+  const int ldv = D + 1;
+  for (int64_t item = blockIdx.x; item < qd->S; item += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < (T + 1) * D; i += blockDim.x) {
+      const int v = i / D, c = i - v * D;
+      float x;
+      if (v == 0) x = has_dense ? X[item * ld_x + c] : 0.f;
+      else x = pooled[item * ld_pooled + (int64_t)(v - 1) * D + c];
+      sv[v * ldv + c] = x;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      float s = 0.f;
+      for (int t = 1; t <= T; ++t) s += sv[t * ldv + c];
+      X[item * ld_x + sum_off + c] = s;
+    }
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      int i = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)p)) * 0.5f);
+      while (i * (i - 1) / 2 > p) --i;
+      while ((i + 1) * i / 2 <= p) ++i;
+      const int j = p - i * (i - 1) / 2;
+      float d = 0.f;
+      for (int c = 0; c < D; ++c) d = fmaf(sv[i * ldv + c], sv[j * ldv + c], d);
+      X[item * ld_x + dot_off + p] = d;
+    }
+  }
+}
+
+__global__ void init_tables_kernel(float* __restrict__ tables, int64_t T, int64_t rows,
+                                   int64_t D, uint64_t seed) {
+  const int64_t per_table = rows * D;
+  const int64_t total = T * per_table;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < total;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    const int64_t t = i / per_table;
+    const int64_t e = i - t * per_table;
+    const uint64_t key = stream_key(seed, id_table(t));
+    if (i + 3 < total && (e + 3) < per_table) {
+      float4 v;
+      v.x = param(key, (uint64_t)e + 0, kTableScale);
+      v.y = param(key, (uint64_t)e + 1, kTableScale);
+      v.z = param(key, (uint64_t)e + 2, kTableScale);
+      v.w = param(key, (uint64_t)e + 3, kTableScale);
+      *reinterpret_cast<float4*>(tables + i) = v;
+    } else {
+      for (int64_t k = i; k < i + 4 && k < total; ++k) {
+        const int64_t tk = k / per_table;
+        tables[k] = param(stream_key(seed, id_table(tk)), (uint64_t)(k - tk * per_table),
+                          kTableScale);
+      }
+    }
+  }
+}
+
+bool pow2_dim(int64_t D) {
+  return D == 8 || D == 16 || D == 32 || D == 64 || D == 128 || D == 256;
+}
+
+int grid_for(int64_t units, int per_block, int sm_count, int blocks_per_sm) {
+  const int64_t need = (units + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sm_count * blocks_per_sm));
+}
+
+}  // namespace
+
+bool sls_vector_path(int64_t D) { return pow2_dim(D); }
+
+void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
+                    float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                    cudaStream_t s) {
+  const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
+  const dim3 blk(kWarps * 32);
+  switch (D) {
+    case 8: sls_sum_kernel<2, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
+    case 16: sls_sum_kernel<4, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
+    case 32: sls_sum_kernel<8, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
+    case 64: sls_sum_kernel<16, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
+    case 128: sls_sum_kernel<32, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
+    case 256: sls_sum_kernel<32, 2, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
+    default:
+      sls_sum_scalar_kernel<<<grid, blk, 0, s>>>(qd, tables, rows, T, L, D, out, ld_out, err);
+  }
+}
+
+void launch_gather_concat(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                          int D, float* out, int64_t ld_out, int64_t col_off, int* err,
+                          int64_t max_items, int sm_count, cudaStream_t s) {
+  const int vec = (D % 4 == 0 && col_off % 4 == 0 && ld_out % 4 == 0) ? 1 : 0;
+  const int64_t units = max_items * T * L * (vec ? D / 4 : D);
+  const int grid = grid_for(units, 256, sm_count, 8);
+  gather_concat_kernel<<<grid, 256, 0, s>>>(qd, tables, rows, T, L, D, out, ld_out, col_off,
+                                            vec, err);
+}
+
+bool din_supported(int64_t D) { return pow2_dim(D); }
+
+void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
+                     const float* att_w, float* out, int64_t ld_out, int64_t col_off, int* err,
+                     int64_t max_items, int sm_count, cudaStream_t s) {
+  const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
+  const dim3 blk(kWarps * 32);
+  switch (D) {
+    case 8: din_pool_kernel<2, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 16: din_pool_kernel<4, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 32: din_pool_kernel<8, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 64: din_pool_kernel<16, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 128: din_pool_kernel<32, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 256: din_pool_kernel<32, 2, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+  }
+}
+
+void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
+                        float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
+                        int64_t max_items, int sm_count, cudaStream_t s) {
+  const size_t smem = (size_t)(T + 1) * (D + 1) * sizeof(float);
+  const int grid = grid_for(max_items, 1, sm_count, 16);
+  interaction_kernel<<<grid, 128, smem, s>>>(qd, pooled, ld_pooled, T, D, X, ld_x, sum_off,
+                                             dot_off, has_dense);
+}
+
+size_t interaction_smem(int T, int D) { return (size_t)(T + 1) * (D + 1) * sizeof(float); }
+
+void launch_init_tables(float* tables, int64_t T, int64_t rows, int64_t D, uint64_t seed,
+                        int sm_count, cudaStream_t s) {
+  const int64_t total = T * rows * D;
+  const int grid = grid_for((total + 3) / 4, 256, sm_count, 16);
+  init_tables_kernel<<<grid, 256, 0, s>>>(tables, T, rows, D, seed);
+}
+
+}  // namespace rs

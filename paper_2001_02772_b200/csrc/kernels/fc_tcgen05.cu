@@ -1,0 +1,328 @@
+// fc_tcgen05.cu — FC layers (DenseFC / PredictFC, proj/src/model_zoo.cpp:187-190,
+// 240-243) on the 5th-generation tensor cores.
+//
+//   C[z][m][n] = act( sum_k A[z][m][k] * W[z][n][k] + bias[z][n] )
+//
+// kind::tf32: the fp32 activations and weights are consumed straight from
+// shared memory (no conversion pass, no second copy of the weights), the
+// tensor core rounds operands to tf32 and accumulates in fp32 in TMEM.
+// Tolerance for this path is stated in tests/test_gpu_parity.py.
+//
+// One 128 x BN output tile per CTA, 8 warps with fixed roles:
+//   warp 0  TMA producer: K slabs of 32 fp32 (=128 B, one SWIZZLE_128B atom
+//           row) for A (128 rows) and W (BN rows) into a STAGES-deep ring
+//   warp 1  MMA issuer: one elected lane issues 4 x tcgen05.mma (K = 8 each)
+//           per slab, tcgen05.commit frees the slab / signals the epilogue
+//   warp 2  TMEM allocator (BN fp32 columns x 128 lanes)
+//   warps 4-7  epilogue: tcgen05.ld 32x32b.x32 (warp w%4 owns TMEM lanes
+//           32(w%4)..+31 = tile rows), + bias, ReLU, 128-bit stores
+// Rows >= S (device query descriptor) are masked at the store; the tile's
+// K tail is zero-filled by TMA.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace rs {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per K slab (128 bytes)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm100 format):
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major, 1),
+// SBO>>4 [32,46) = 1024 B between 8-row groups, version 1 at [46,48),
+// layout type SWIZZLE_128B = 2 at [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+// Instruction descriptor: D f32 [4,6)=1, A tf32 [7,10)=2, B tf32 [10,13)=2,
+// both K-major, N>>3 at [17,23), M>>4 at [24,29).
+template <int BN>
+__device__ __forceinline__ uint32_t idesc_tf32() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+
+template <int BN, int STAGES>
+struct TcSmem {
+  alignas(1024) float a[STAGES][BM * BK];
+  alignas(1024) float b[STAGES][BN * BK];
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tmem_full;
+  uint32_t tmem_base;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap map_a,
+             const __grid_constant__ CUtensorMap map_w, FcArgs a, int a_batched) {
+  extern __shared__ uint8_t smem_raw[];
+  TcSmem<BN, STAGES>& sm = *reinterpret_cast<TcSmem<BN, STAGES>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int64_t M = qd->S;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, z = blockIdx.z;
+  if (m0 >= M) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (a.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    mbar_init(&sm.tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    constexpr uint32_t kBytes = (BM + BN) * BK * sizeof(float);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+      mbar_wait(&sm.empty[s], ph ^ 1u);
+      mbar_expect_tx(&sm.full[s], kBytes);
+      if (a_batched) tma_load_3d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0, z);
+      else tma_load_2d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0);
+      tma_load_3d(sm.b[s], &map_w, &sm.full[s], kb * BK, n0, z);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer (single thread) ----
+    const uint32_t idesc = idesc_tf32<BN>();
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+      mbar_wait(&sm.full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sa = smem_u32(sm.a[s]), sb = smem_u32(sm.b[s]);
+#pragma unroll
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint64_t da = sw128_desc(sa + kk * 32);
+        const uint64_t db = sw128_desc(sb + kk * 32);
+        const uint32_t acc = (kb | kk) ? 1u : 0u;
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc)
+            : "memory");
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              smem_u32(&sm.empty[s]))
+          : "memory");
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&sm.tmem_full))
+        : "memory");
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM -> registers -> bias/ReLU -> global ----
+    mbar_wait(&sm.tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quad = warp & 3;
+    const int64_t m = m0 + quad * 32 + lane;
+    float* __restrict__ C = a.C + (int64_t)z * a.sCz + m * a.ldc;
+    const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
+    const bool vec_ok = (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0) &&
+                        (a.sCz % 4 == 0);
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+            "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+            "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+            "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+            "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (m < M) {
+        const int nb = n0 + c * 32;
+        float y[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int n = nb + i;
+          float val = __uint_as_float(v[i]) + (n < a.N ? __ldg(bias + n) : 0.f);
+          y[i] = a.relu ? fmaxf(val, 0.f) : val;
+        }
+        if (vec_ok && nb + 32 <= a.N) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(C + nb)[i] =
+                make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < a.N) C[nb + i] = y[i];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN)
+                 : "memory");
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool encode(CUtensorMap* map, const float* base, int rank, const cuuint64_t* dims,
+            const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, (void*)base, dims,
+                  strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES>
+size_t tc_smem_bytes() {
+  return sizeof(TcSmem<BN, STAGES>) + 1024;
+}
+
+template <int BN, int STAGES>
+void set_attr_once() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(fc_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tc_smem_bytes<BN, STAGES>());
+  });
+}
+
+}  // namespace
+
+bool tc_available() { return encode_fn() != nullptr; }
+
+bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch) {
+  if (a.N < 64 || a.K < BK) return false;
+  if (a.lda % 4 || a.ldw % 4 || (a.sAz % 4) || (a.sWz % 4)) return false;
+  if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.W) & 15))
+    return false;
+  p->block_n = a.N >= 128 ? 128 : 64;
+  p->m_tiles = (int)((m_cap + BM - 1) / BM);
+  p->n_tiles = (a.N + p->block_n - 1) / p->block_n;
+  // A: [batch][rows][K] (or shared 2D when sAz == 0)
+  if (a.sAz != 0) {
+    cuuint64_t dims[3] = {(cuuint64_t)a.K, (cuuint64_t)a_rows_per_batch, (cuuint64_t)a.batch};
+    cuuint64_t str[2] = {(cuuint64_t)a.lda * 4, (cuuint64_t)a.sAz * 4};
+    cuuint32_t box[3] = {BK, BM, 1};
+    if (!encode(&p->map_a, a.A, 3, dims, str, box)) return false;
+  } else {
+    cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a_rows_per_batch};
+    cuuint64_t str[1] = {(cuuint64_t)a.lda * 4};
+    cuuint32_t box[2] = {BK, BM};
+    if (!encode(&p->map_a, a.A, 2, dims, str, box)) return false;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)a.K, (cuuint64_t)a.N, (cuuint64_t)a.batch};
+    cuuint64_t str[2] = {(cuuint64_t)a.ldw * 4,
+                         (cuuint64_t)(a.sWz ? a.sWz : (int64_t)a.N * a.ldw) * 4};
+    cuuint32_t box[3] = {BK, (cuuint32_t)p->block_n, 1};
+    if (!encode(&p->map_w, a.W, 3, dims, str, box)) return false;
+  }
+  if (p->block_n == 128) set_attr_once<128, 3>();
+  else set_attr_once<64, 4>();
+  return true;
+}
+
+void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s) {
+  const dim3 grid(p.n_tiles, p.m_tiles, a.batch);
+  const int a_batched = a.sAz != 0 ? 1 : 0;
+  if (p.block_n == 128)
+    fc_tc_kernel<128, 3><<<grid, 256, tc_smem_bytes<128, 3>(), s>>>(qd, p.map_a, p.map_w, a,
+                                                                     a_batched);
+  else
+    fc_tc_kernel<64, 4><<<grid, 256, tc_smem_bytes<64, 4>(), s>>>(qd, p.map_a, p.map_w, a,
+                                                                   a_batched);
+}
+
+}  // namespace rs

@@ -1,0 +1,71 @@
+// kernels.hpp — host-side launchers for the sm_100a kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rs {
+
+struct QDesc;
+
+// ---- embedding.cu ----
+bool sls_vector_path(int64_t D);
+void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
+                    float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                    cudaStream_t s);
+void launch_gather_concat(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                          int D, float* out, int64_t ld_out, int64_t col_off, int* err,
+                          int64_t max_items, int sm_count, cudaStream_t s);
+bool din_supported(int64_t D);
+void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
+                     const float* att_w, float* out, int64_t ld_out, int64_t col_off, int* err,
+                     int64_t max_items, int sm_count, cudaStream_t s);
+void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
+                        float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
+                        int64_t max_items, int sm_count, cudaStream_t s);
+size_t interaction_smem(int T, int D);
+void launch_init_tables(float* tables, int64_t T, int64_t rows, int64_t D, uint64_t seed,
+                        int sm_count, cudaStream_t s);
+
+// ---- fc_ffma.cu ----
+// Batched (over predict stacks, grid z) fp32 FC layer:
+//   C[z][m][n] = act( sum_k A[z][m][k] * W[z][n][k] + bias[z][n] ),  m < S (device)
+struct FcArgs {
+  const float* A; int64_t lda; int64_t sAz;
+  const float* W; int64_t ldw; int64_t sWz;
+  const float* bias; int64_t sbz;
+  float* C; int64_t ldc; int64_t sCz;
+  int N; int K; int relu; int batch;
+};
+void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);
+
+// ---- fc_tcgen05.cu ----
+// Same contract on the 5th-gen tensor cores (kind::tf32, fp32 accumulate in
+// TMEM, operands staged by TMA). Tensor maps are built once per buffer.
+struct TcPlan {
+  CUtensorMap map_a;   // A: [batch][M_cap][K] fp32, box 128 x 32
+  CUtensorMap map_w;   // W: [batch][N][K] fp32, box BN x 32
+  int block_n;         // 64 / 128 / 256
+  int m_tiles, n_tiles;
+};
+bool tc_available();
+bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch);
+void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s);
+
+// ---- gru.cu ----
+struct GruArgs {
+  const float* tables; int64_t rows; int T; int L; int D; int H;
+  const float* w_ih;   // [T][3H][D]
+  const float* w_hh;   // [T][3H][H]
+  const float* b_ih;   // [T][3H]
+  const float* b_hh;   // [T][3H]
+  const float* w_att;  // [T][D][D] (AUGRU only)
+  int augru;
+  float* out; int64_t ld_out; int64_t col_off;
+  int* err;
+};
+void prepare_gru(const GruArgs& g);
+void launch_gru(const QDesc* qd, const GruArgs& g, int64_t max_items, int sm_count,
+                cudaStream_t s);
+
+}  // namespace rs

@@ -1,0 +1,69 @@
+"""The C-ABI library loads and exports every entry point include/rs_accel.h
+declares; error plumbing works without a GPU (no compute calls here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rs_accel.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ["rs_accel_create", "rs_accel_destroy", "rs_forward", "rs_pooled",
+                 "rs_service_time", "rs_alloc_pinned", "rs_free_pinned", "rs_last_error"]:
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(rs):
+    lib = C.CDLL(rs.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert sorted(rs.EXPORTED_SYMBOLS) == declared_functions()
+
+
+def test_abi_version(rs):
+    assert rs._lib.rs_abi_version() == 1
+
+
+def test_errors_cross_the_abi_as_codes(rs):
+    with pytest.raises(rs.UnknownModel):
+        rs.builtin_model("ResNet50")
+    assert "ResNet50" in rs._lib.rs_last_error().decode()
+    with pytest.raises(rs.InvalidArgument):
+        rs.work(rs.builtin_model("NCF"), 0)
+
+
+def test_no_device_is_reported_not_crashed(rs):
+    # In the CPU container there is no GPU: creating an accelerator must fail
+    # with NoDevice (never silently fall back to a CPU path).
+    if rs.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(rs.NoDevice):
+        rs.Accelerator(rs.builtin_model("NCF"), rows_per_table=100)
+
+
+def test_library_is_sm100a_only(rs):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", rs.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    for other in ("sm_80", "sm_90", "sm_120"):
+        assert other + "." not in out
+
+
+def test_tcgen05_and_tma_in_sass(rs):
+    import subprocess
+    sass = subprocess.run(["cuobjdump", "-sass", rs.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert "UTCHMMA" in sass        # tcgen05.mma
+    assert "UTMALDG" in sass        # TMA tensor loads
+    assert "LDTM" in sass           # tcgen05.ld TMEM -> registers

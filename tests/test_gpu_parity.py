@@ -1,0 +1,150 @@
+"""GPU parity: the sm_100a path, called through the C-ABI, against the CPU oracle
+on the same seeded inputs.
+
+Tolerance rule. The oracle computes in fp64 and also returns
+`mag`, the absolute-value forward (sum of |terms| carried through every linear
+stage) — the natural scale of floating-point error for each output:
+  * fp32 FFMA path:   max |gpu - ref| / mag <= 1e-5
+  * tf32 tcgen05 path: max |gpu - ref| / mag <= 1e-2  (10-bit operand mantissa)
+  * SLS pooled sums:  bit-identical to the oracle's canonical fp32 order.
+"""
+import numpy as np
+import pytest
+
+import paper_2001_02772_b200 as rs
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+TF32_TOL = 1e-2
+
+
+def rel_err(got, ref, mag):
+    return float(np.max(np.abs(got.astype(np.float64) - ref) / np.maximum(mag, 1e-30)))
+
+
+def check_forward(spec, rows, S, fc_mode=rs.FC_FP32, augru=False, seed=3, qid=0, tol=FP32_TOL,
+                  max_q=256):
+    acc = rs.Accelerator(spec, rows, seed=seed, max_query_size=max_q, fc_mode=fc_mode,
+                         rnn_cell=rs.RNN_AUGRU if augru else rs.RNN_GRU)
+    orc = Oracle(spec, rows, seed=seed, augru=augru)
+    dense, idx = rs.fill_query(spec, rows, seed=seed + 100, query_id=qid, size=S)
+    out = acc.forward(dense, idx)
+    ref, mag, pref, pmag = orc.forward64(dense, idx)
+    e = rel_err(out, ref, mag)
+    assert e <= tol, f"{spec.name}: logits max|d|/mag = {e:.3g} > {tol}"
+    if spec.embeddings.num_tables > 0:
+        pooled = acc.pooled(idx)
+        if spec.embeddings.pooling == "Sum":
+            assert np.array_equal(pooled, orc.sls_canonical(idx)), "SLS not bit-exact"
+        else:
+            ep = rel_err(pooled, pref, pmag)
+            assert ep <= FP32_TOL, f"{spec.name}: pooled max|d|/mag = {ep:.3g}"
+    acc.close()
+    return e
+
+
+@pytest.mark.parametrize("name", ["NCF", "WND", "MT-WND", "DLRM-RMC1", "DLRM-RMC2",
+                                  "DLRM-RMC3", "DIN", "DIEN"])
+def test_zoo_fp32(name):
+    check_forward(rs.builtin_model(name), rows=20000, S=9)
+
+
+def test_dien_augru():
+    check_forward(rs.builtin_model("DIEN"), rows=5000, S=7, augru=True)
+
+
+@pytest.mark.parametrize("D", [8, 16, 32, 64, 128, 256, 24, 12])
+def test_sls_bit_exact_every_vector_width(D):
+    spec = rs.ModelSpec(f"sls-D{D}", dense_fc=None, predict_fc=rs.LayerStack([4]),
+                        embeddings=rs.EmbeddingConfig(3, 37, D, "Sum"), dense_input_dim=0)
+    check_forward(spec, rows=3001, S=11)
+
+
+def test_cfg1_rmc1_single_query_batch64():
+    """BASELINE configs[0]: DLRM-RMC1, 8 tables x 1M rows x dim 32, 80 lookups,
+    one query of 64 items, fp32."""
+    spec = rs.ModelSpec("cfg1-RMC1", dense_fc=rs.LayerStack([256, 128, 32]),
+                        predict_fc=rs.LayerStack([256, 64, 1]),
+                        embeddings=rs.EmbeddingConfig(8, 80, 32, "Sum"), dense_input_dim=256)
+    check_forward(spec, rows=1_000_000, S=64, max_q=64)
+
+
+@pytest.mark.parametrize("name", ["MT-WND", "WND", "DLRM-RMC3"])
+def test_tf32_tcgen05_path(name):
+    spec = rs.builtin_model(name)
+    acc = rs.Accelerator(spec, 2000, seed=1, max_query_size=300, fc_mode=rs.FC_TF32)
+    assert acc.info.fc_layers_tcgen05 > 0
+    acc.close()
+    for S in (1, 130, 300):
+        check_forward(spec, rows=2000, S=S, fc_mode=rs.FC_TF32, tol=TF32_TOL, max_q=300)
+
+
+def test_edges_sizes_and_errors():
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 1000
+    acc = rs.Accelerator(spec, rows, seed=5, max_query_size=50)
+    orc = Oracle(spec, rows, seed=5)
+    for S in (1, 50):
+        dense, idx = rs.fill_query(spec, rows, 1, S, S)
+        ref, mag, _, _ = orc.forward64(dense, idx)
+        assert rel_err(acc.forward(dense, idx), ref, mag) <= FP32_TOL
+    dense, idx = rs.fill_query(spec, rows, 1, 0, 51)
+    with pytest.raises(rs.CapacityError):
+        acc.forward(dense, idx)
+    dense, idx = rs.fill_query(spec, rows, 1, 0, 4)
+    idx[2, 7, 11] = rows            # out of range
+    with pytest.raises(rs.IndexOutOfRange):
+        acc.forward(dense, idx)
+    idx[2, 7, 11] = -1
+    with pytest.raises(rs.IndexOutOfRange):
+        acc.forward(dense, idx)
+    idx[2, 7, 11] = 0               # the handle recovers
+    ref, mag, _, _ = orc.forward64(dense, idx)
+    assert rel_err(acc.forward(dense, idx), ref, mag) <= FP32_TOL
+    acc.close()
+
+
+def test_device_resident_inputs_and_streams_are_identical():
+    torch = pytest.importorskip("torch")
+    spec = rs.builtin_model("DLRM-RMC2")
+    rows = 4000
+    acc = rs.Accelerator(spec, rows, seed=2, max_query_size=128)
+    dense, idx = rs.fill_query(spec, rows, 4, 0, 100)
+    host = acc.forward(dense, idx)
+    again = acc.forward(dense, idx)
+    assert np.array_equal(host, again)                     # run-to-run bitwise
+    d_dense = torch.from_numpy(dense).cuda()
+    d_idx = torch.from_numpy(idx).cuda()
+    d_out = torch.empty((100, acc.output_dim), device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for st in (s1, s2):
+        o = torch.empty_like(d_out)
+        acc.forward_ptr(100, d_dense.data_ptr(), d_idx.data_ptr(), o.data_ptr(),
+                        rs.MEM_DEVICE, stream=st.cuda_stream)
+        outs.append(o)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy(), host)
+    acc.close()
+
+
+def test_service_time_is_measured_and_memoised():
+    spec = rs.builtin_model("DLRM-RMC1")
+    acc = rs.Accelerator(spec, 10000, seed=2, max_query_size=512)
+    t1 = acc.service_time(300)
+    assert 0 < t1 < 0.1
+    assert acc.service_time(300) == t1
+    assert acc.service_time(1) > 0
+    acc.close()
+
+
+def test_cfg3_rmc2_ten_million_rows():
+    """BASELINE configs[2]: 32 tables x 10M rows x dim 64 (81.9 GB on one B200);
+    parity on a query of 16 items (oracle regenerates the touched rows)."""
+    spec = rs.ModelSpec("cfg3-RMC2", dense_fc=rs.LayerStack([256, 128, 64]),
+                        predict_fc=rs.LayerStack([512, 128, 1]),
+                        embeddings=rs.EmbeddingConfig(32, 80, 64, "Sum"), dense_input_dim=256)
+    check_forward(spec, rows=10_000_000, S=16, max_q=64)
