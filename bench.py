@@ -1,0 +1,426 @@
+"""bench.py — QPS at a p95 SLA for the offloaded recommendation forward pass on
+B200 replicas, plus the SLS kernel's HBM roofline and the CPU baseline.
+
+Workload (BASELINE.json configs[2], the SLS-bound DLRM config the 1/2/4/8-GPU
+sweep is defined on; its metric names "SLS HBM GB/s vs peak"):
+  DLRM-RMC2 at cfg3 shape: 32 tables x 10M rows x dim 64 fp32 (81.9 GB per
+  GPU), 80 lookups/table, bottom MLP 256-128-64, top MLP 656-512-128-1;
+  query sizes LogNormal(ln 300, 0.5) clamped to [1, 1000],
+  Poisson arrivals; SLA = sla_target("DLRM-RMC2", "medium") = 400 ms.
+
+A step = one window of Q consecutive queries of the rank's stream, each served
+whole through the C-ABI (rs_forward), back to back on one CUDA stream.
+  value  = QPS at p95 <= SLA: per-query device service times from CUDA events
+           inside the timed region, replayed open-loop with Poisson arrivals
+           (FIFO server, exact p95, geometric lambda bisection to 1% — the rule
+           of proj/src/sim.cpp:246-290); whole job = N x min over ranks.
+  e2e    = the same metric with host (pinned) inputs: H2D of dense+indices and
+           D2H of the logits inside every query's service time.
+Multi-GPU: one process per GPU, independent replicas (each rank its own
+query stream, seed 42 + 10007*rank); no collective on the data path
+ — only the timing barrier and max-over-ranks reduction.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QPS at p95 tail-latency SLA per model at 1/2/4/8 B200; SLS HBM GB/s vs peak"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def workload_spec(rs, name):
+    if name == "cfg3-rmc2":
+        return rs.ModelSpec("cfg3-DLRM-RMC2", dense_fc=rs.LayerStack([256, 128, 64]),
+                            predict_fc=rs.LayerStack([512, 128, 1]),
+                            embeddings=rs.EmbeddingConfig(32, 80, 64, "Sum"),
+                            dense_input_dim=256), 10_000_000, "DLRM-RMC2"
+    if name == "cfg3-rmc3":
+        return rs.ModelSpec("cfg3-DLRM-RMC3", dense_fc=rs.LayerStack([2560, 512, 64]),
+                            predict_fc=rs.LayerStack([512, 128, 1]),
+                            embeddings=rs.EmbeddingConfig(32, 20, 64, "Sum"),
+                            dense_input_dim=256), 10_000_000, "DLRM-RMC3"
+    if name == "cfg1-rmc1":
+        return rs.ModelSpec("cfg1-DLRM-RMC1", dense_fc=rs.LayerStack([256, 128, 32]),
+                            predict_fc=rs.LayerStack([256, 64, 1]),
+                            embeddings=rs.EmbeddingConfig(8, 80, 32, "Sum"),
+                            dense_input_dim=256), 1_000_000, "DLRM-RMC1"
+    # zoo models with 1M-row tables
+    zoo = {"ncf": "NCF", "wnd": "WND", "mt-wnd": "MT-WND", "din": "DIN", "dien": "DIEN",
+           "rmc1": "DLRM-RMC1", "rmc2": "DLRM-RMC2", "rmc3": "DLRM-RMC3"}
+    m = zoo[name]
+    return rs.builtin_model(m), 1_000_000, m
+
+
+def sls_bytes_per_item(spec):
+    e = spec.embeddings
+    return e.num_tables * e.lookups_per_table * (e.embedding_dim * 4 + 8) + \
+        e.num_tables * e.embedding_dim * 4
+
+
+# ---- distributed plumbing (also exercised by tests/test_bench_dist.py) ------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def rank_seed(rank: int) -> int:
+    """The reference's multi-seed scheme (proj/src/autotune.cpp:23)."""
+    return 42 + 10007 * rank
+
+
+def reduce_max(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_min(value: float, device=None) -> float:
+    return -reduce_max(-value, device)
+
+
+def reduce_sum(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(device=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        if device is not None:
+            dist.barrier(device_ids=[device.index])
+        else:
+            dist.barrier()
+
+
+def aggregate(per_rank_qps: float, per_rank_time: float, queries: int, world: int, device=None):
+    """Whole-job numbers: slowest rank's time, N x the worst rank's SLA QPS."""
+    t = reduce_max(per_rank_time, device)
+    q_min = reduce_min(per_rank_qps, device)
+    total_q = reduce_sum(float(queries), device)
+    return {"time_s": t, "value": world * q_min, "saturated_qps": total_q / t if t > 0 else 0.0}
+
+
+# ---- clocks ------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self._t:
+                self._t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6548.2), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---- CPU baseline ------------------------------------------------------------
+class CpuArm:
+    """The oracle's fp32 forward (oracle/forward.c, kind "port") on the host's
+    cores: every worker thread serves whole queries of the same stream. Tables
+    are materialised at rows_cpu rows (>> LLC, so gathers still miss to DRAM)."""
+
+    def __init__(self, spec, sizes, threads, rows_cpu=1_000_000):
+        from oracle import Oracle
+        self.orc = Oracle(spec, rows_cpu, seed=1, materialize=True)
+        self.sizes, self.threads, self.rows = sizes, threads, rows_cpu
+        t1 = self.orc.bench_queries(sizes[:1], 1, seed=5)   # calibrate on one query
+        self.per_query = max(t1, 1e-4) / threads
+
+    def sample(self, budget_s):
+        nq = int(min(len(self.sizes), max(self.threads, budget_s / self.per_query)))
+        secs = self.orc.bench_queries(self.sizes[:nq], self.threads, seed=5)
+        return {"value": nq / secs, "unit": "queries/s", "cores": self.threads, "kind": "port",
+                "sample": f"{nq} queries of the same LogNormal(ln300,0.5) stream (mean "
+                          f"{float(np.mean(self.sizes[:nq])):.0f} items), fp32 oracle forward, "
+                          f"one query per thread, {self.threads} threads, tables materialised "
+                          f"at {self.rows:,} rows/table, {secs:.1f} s wall"}
+
+
+def cpu_baseline(spec, sizes, threads, budget_s=15.0):
+    return CpuArm(spec, sizes, threads).sample(budget_s)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU implementation of the path (oracle port) on all
+    host cores, same metric/config; rank 0 only under torchrun."""
+    if rank != 0:
+        return
+    import paper_2001_02772_b200 as rs
+    spec, rows, zoo_name = workload_spec(rs, args.workload)
+    _, sizes = rs.gen_trace(rank_seed(0), 1000.0, rs.SizeDistribution.log_normal(math.log(300), 0.5),
+                            4096)
+    threads = os.cpu_count() or 1
+    arm = CpuArm(spec, sizes, threads)
+    budget = max(2.0, 90.0 / (args.steps + args.warmup))
+    vals = []
+    cb = None
+    for _ in range(args.warmup + args.steps):
+        cb = arm.sample(budget)
+        vals.append(cb["value"])
+    v = statistics.median(vals[args.warmup:])
+    cb["value"] = v
+    line = {"metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": args.workload, "model": spec.name,
+                       "rows_per_table": rows, "sla_s": rs.sla_target(zoo_name, "medium")},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- the B200 arm --------------------------------------------------------------
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_2001_02772_b200 as rs
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+
+    spec, rows, zoo_name = workload_spec(rs, args.workload)
+    sla = rs.sla_target(zoo_name, "medium")
+    Q, K, W = args.queries_per_step, args.steps, args.warmup
+    seed = rank_seed(rank)
+    _, sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(math.log(300), 0.5),
+                            2 * Q)
+    sizes = np.minimum(sizes, args.max_query)
+    acc = rs.Accelerator(spec, rows, seed=1, device=local, max_query_size=args.max_query,
+                         fc_mode=rs.FC_FP32 if args.fc == "fp32" else rs.FC_TF32)
+    e = spec.embeddings
+    # pool of 2Q distinct queries: pinned host copies (e2e) and device copies (value)
+    P = 2 * Q
+    d_dense, d_idx, h_dense, h_idx = [], [], [], []
+    for q in range(P):
+        dn, ix = rs.fill_query(spec, rows, seed, q, int(sizes[q]))
+        hb_d = rs.PinnedBuffer(max(dn.nbytes, 16))
+        hb_i = rs.PinnedBuffer(max(ix.nbytes, 16))
+        hb_d.view(np.float32, dn.shape)[...] = dn
+        hb_i.view(np.int64, ix.shape)[...] = ix
+        h_dense.append(hb_d)
+        h_idx.append(hb_i)
+        d_dense.append(torch.from_numpy(dn).to(device))
+        d_idx.append(torch.from_numpy(ix).to(device))
+    out_dev = torch.empty((args.max_query, acc.output_dim), device=device)
+    out_host = rs.PinnedBuffer(args.max_query * acc.output_dim * 4)
+    stream = torch.cuda.current_stream(device)
+    sp = stream.cuda_stream
+
+    def window(k):
+        base = (k % 2) * Q
+        return range(base, base + Q)
+
+    def run_steps(n_steps, host, events=None):
+        for k in range(n_steps):
+            for q in window(k):
+                S = int(sizes[q])
+                if host:
+                    acc.forward_ptr(S, h_dense[q].ptr, h_idx[q].ptr, out_host.ptr, rs.MEM_HOST,
+                                    stream=sp)
+                else:
+                    acc.forward_ptr(S, d_dense[q].data_ptr(), d_idx[q].data_ptr(),
+                                    out_dev.data_ptr(), rs.MEM_DEVICE, stream=sp)
+                if events is not None:
+                    events.append((q, torch.cuda.Event(enable_timing=True)))
+                    events[-1][1].record(stream)
+
+    def timed(host):
+        run_steps(W, host)                       # warm-up (untimed)
+        torch.cuda.synchronize(device)
+        barrier(device)
+        torch.cuda.synchronize(device)
+        ev = []
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            start.record(stream)
+            run_steps(K, host, ev)
+            end.record(stream)
+            torch.cuda.synchronize(device)
+        barrier(device)
+        torch.cuda.synchronize(device)
+        total_s = start.elapsed_time(end) * 1e-3
+        svc, prev = [], start
+        for _, e2 in ev:
+            svc.append(prev.elapsed_time(e2) * 1e-3)
+            prev = e2
+        return total_s, np.array(svc), [q for q, _ in ev], clk.summary()
+
+    # ---- value: device-resident inputs
+    t_dev, svc_dev, qs, clocks = timed(host=False)
+    r_dev = rs.qps_under_sla(svc_dev, sla, servers=1, warmup_fraction=0.1, base_seed=seed)
+    agg = aggregate(r_dev.qps, t_dev, len(svc_dev), world, device)
+    # ---- e2e: host pinned inputs, H2D/D2H inside every query
+    t_host, svc_host, _, clocks_e2e = timed(host=True)
+    r_host = rs.qps_under_sla(svc_host, sla, servers=1, warmup_fraction=0.1, base_seed=seed)
+    agg_e2e = aggregate(r_host.qps, t_host, len(svc_host), world, device)
+
+    # ---- roofline of the dominant kernel (SLS), live CUDA-event timing on the
+    # launching stream: the embedding-stage graph (error-word memset + SLS kernel)
+    sls_ms, sls_bytes = 0.0, 0.0
+    pooled_dev = torch.empty((args.max_query, acc.pooled_dim), device=device)
+    for q in window(0):
+        S = int(sizes[q])
+        t = acc.pooled_ptr(S, d_idx[q].data_ptr(), pooled_dev.data_ptr(), rs.MEM_DEVICE,
+                           stream=sp, timed=True)
+        sls_ms += t.compute_ms
+        sls_bytes += S * sls_bytes_per_item(spec)
+    peak, peak_src = measured_peaks()
+    achieved = sls_bytes / (sls_ms * 1e-3) / 1e9
+
+    items_step = float(np.mean([sum(int(sizes[q]) for q in window(k)) for k in range(K)]))
+    h2d_step = float(np.mean([sum(int(sizes[q]) * (spec.dense_input_dim * 4 +
+                                                   e.num_tables * e.lookups_per_table * 8)
+                                  for q in window(k)) for k in range(K)]))
+    d2h_step = float(np.mean([sum(int(sizes[q]) * acc.output_dim * 4 + 4 for q in window(k))
+                              for k in range(K)]))
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "sls_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("bytes_per_item")
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": agg["value"], "unit": "queries/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": agg["time_s"] * 1e3 / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded random-init tables/weights, LogNormal(ln300,0.5) sizes)",
+            "config": {"workload": args.workload, "model": spec.name, "rows_per_table": rows,
+                       "tables": e.num_tables, "lookups": e.lookups_per_table,
+                       "dim": e.embedding_dim, "queries_per_step": Q,
+                       "items_per_step": items_step, "sla_s": sla,
+                       "fc_path": args.fc, "parallelism": f"replicas{world}",
+                       "l2": "inputs >> L2 (tables %.1f GB, ~%.0f MB of indices per step)" % (
+                           acc.info.table_bytes / 1e9, h2d_step / 1e6),
+                       "qps_method": "open-loop Poisson replay of per-query CUDA-event service "
+                                     "times (FIFO server per GPU, exact p95, lambda bisection "
+                                     "to 1%, sim.cpp:246-290); whole job = N x min rank"},
+            "sla": {"p95_ms": r_dev.p95 * 1e3, "p50_ms": r_dev.p50 * 1e3,
+                    "at_lambda": r_dev.at_lambda, "saturated_qps": agg["saturated_qps"],
+                    "mean_service_ms": float(svc_dev.mean() * 1e3)},
+            "e2e": {"value": agg_e2e["value"], "unit": "queries/s",
+                    "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step,
+                    "p95_ms": r_host.p95 * 1e3, "saturated_qps": agg_e2e["saturated_qps"],
+                    "h2d_gbs": h2d_step * K / max(t_host, 1e-9) / 1e9},
+            "roofline": {"bound": "hbm", "kernel": "sls_sum_kernel<16,1,8>",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_item": sls_bytes_per_item(spec),
+                         "kernel_share_of_step": (sls_ms * 1e-3) / max(t_dev / K, 1e-12)},
+            "gpu_launches": acc.info.kernels_per_forward * K * Q,
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(spec, sizes, os.cpu_count() or 1)
+        print(json.dumps(line), flush=True)
+    acc.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="cfg3-rmc2")
+    ap.add_argument("--queries-per-step", type=int, default=128)
+    ap.add_argument("--max-query", type=int, default=1000)
+    ap.add_argument("--fc", choices=["fp32", "tf32"], default="fp32")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -242,6 +242,10 @@ void build_model(rs_accel* a) {
     };
     put(a->gru_wih, wih); put(a->gru_whh, whh); put(a->gru_bih, bih);
     put(a->gru_bhh, bhh); put(a->gru_watt, watt);
+    GruArgs g{};
+    g.T = (int)a->T; g.L = (int)a->L; g.D = (int)a->D; g.H = (int)a->H;
+    prepare_gru(g);
+    RS_CUDA(cudaGetLastError());
   }
   if (m.pooling == RS_POOL_SUM && a->T > 0) {
     const size_t smem = interaction_smem((int)a->T, (int)a->D);
@@ -354,6 +358,8 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, bool full, int* kernels, int* tc_l
   }
   cudaError_t le = cudaGetLastError();
   cudaError_t ce = cudaStreamEndCapture(st, &g);
+  (void)cudaGetLastError();
+  if ((le != cudaSuccess || ce != cudaSuccess) && g) cudaGraphDestroy(g);
   if (le != cudaSuccess) raise(RS_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
   if (ce != cudaSuccess) raise(RS_E_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
   size_t n = 0;
@@ -536,6 +542,7 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     if (init->fc_mode < RS_FC_FP32 || init->fc_mode > RS_FC_AUTO)
       raise(RS_E_INVALID, "bad fc_mode");
     RS_CUDA(cudaSetDevice(device));
+    (void)cudaGetLastError();  // drop a stale non-sticky error from an earlier call
     a = new rs_accel();
     a->m = *model;
     a->init = *init;

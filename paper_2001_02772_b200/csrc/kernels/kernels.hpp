@@ -64,6 +64,7 @@ struct GruArgs {
   float* out; int64_t ld_out; int64_t col_off;
   int* err;
 };
+bool gru_supported(int D, int H);
 void prepare_gru(const GruArgs& g);
 void launch_gru(const QDesc* qd, const GruArgs& g, int64_t max_items, int sm_count,
                 cudaStream_t s);
