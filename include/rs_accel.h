@@ -209,7 +209,8 @@ typedef struct rs_timing {
 typedef struct rs_accel_info {
   int32_t device;
   int32_t sm_count;
-  int32_t kernels_per_forward;     /* kernel nodes in one forward graph    */
+  int32_t kernels_per_forward;     /* kernel nodes, large-batch graph      */
+  int32_t kernels_per_forward_small; /* kernel nodes, small-batch graph     */
   int32_t fc_layers_tcgen05;       /* FC layers routed to tcgen05          */
   int64_t predict_input_dim;
   int64_t output_dim;              /* per item: stacks * last predict dim  */
@@ -232,11 +233,29 @@ int rs_accel_info_get(const rs_accel* a, rs_accel_info* out);
  * (platform.cpp:113-136). Writes logits f32[S * stacks * out_dim] to `out`
  * (same location kind as the query). `stream` is a cudaStream_t (NULL =
  * the handle's own stream). When `timing` is non-NULL the call records
- * events and waits for completion; otherwise it is asynchronous on
- * `stream` and the caller owns synchronisation. Inputs and outputs must
- * stay valid until the stream reaches the end of this call.                */
+ * events, waits for completion and reports index errors; otherwise it is
+ * asynchronous on `stream`, errors stay sticky until rs_sync, and the
+ * caller owns synchronisation. Inputs and outputs must stay valid until the
+ * stream reaches the end of this call. With RS_FC_AUTO, queries of at least
+ * 128 items run the tcgen05 FC graph, smaller ones the FFMA graph.          */
 int rs_forward(rs_accel* a, const rs_query* q, float* out, void* stream,
                rs_timing* timing);
+
+/* Serve n whole queries back to back on `stream`, in order — the FIFO
+ * accelerator server of simulate() (proj/src/sim.cpp:126-136), one query at
+ * a time. outs[i] receives query i's logits. Host-resident queries go
+ * through a two-slot queue: query i+1's H2D runs on an internal copy stream
+ * while query i computes. When service_ms is non-NULL the call records an
+ * event after every query, waits, and returns per-query service times
+ * (ms, completion-to-completion, the first from the call's start) and any
+ * sticky error. All queries must share one memory location. Concurrent
+ * rs_forward_many calls on one handle are serialised.                       */
+int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
+                    float* const* outs, void* stream, double* service_ms);
+
+/* Wait for `stream` and report (then clear) errors that asynchronous calls
+ * left in the handle's sticky error words (e.g. RS_E_INDEX).               */
+int rs_sync(rs_accel* a, void* stream);
 
 /* Embedding stage only (parity hook): writes the pooled sparse features
  * f32[S * pooled_dim] — [S,T,D] sums (Sum), [S,T*L*D] (Concat),

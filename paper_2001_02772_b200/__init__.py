@@ -143,7 +143,8 @@ class CTiming(C.Structure):
 
 class CAccelInfo(C.Structure):
     _fields_ = [("device", C.c_int32), ("sm_count", C.c_int32),
-                ("kernels_per_forward", C.c_int32), ("fc_layers_tcgen05", C.c_int32),
+                ("kernels_per_forward", C.c_int32), ("kernels_per_forward_small", C.c_int32),
+                ("fc_layers_tcgen05", C.c_int32),
                 ("predict_input_dim", C.c_int64), ("output_dim", C.c_int64),
                 ("pooled_dim", C.c_int64), ("table_bytes", C.c_int64),
                 ("weight_bytes", C.c_int64), ("l2_bytes", C.c_int64)]
@@ -178,6 +179,9 @@ _sig("rs_accel_destroy", C.c_int, C.c_void_p)
 _sig("rs_accel_info_get", C.c_int, C.c_void_p, P(CAccelInfo))
 _sig("rs_forward", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_void_p, P(CTiming))
 _sig("rs_pooled", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_void_p, P(CTiming))
+_sig("rs_forward_many", C.c_int, C.c_void_p, C.c_int64, P(CQuery), P(C.c_void_p), C.c_void_p,
+     P(C.c_double))
+_sig("rs_sync", C.c_int, C.c_void_p, C.c_void_p)
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
@@ -189,7 +193,8 @@ EXPORTED_SYMBOLS = [
     "rs_abi_version", "rs_last_error", "rs_model_builtin", "rs_zoo_names", "rs_model_validate",
     "rs_work", "rs_predict_input_dim", "rs_accel_input_bytes", "rs_sla_target", "rs_route",
     "rs_dist_production", "rs_gen_trace", "rs_qps_under_sla", "rs_accel_create",
-    "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_pooled", "rs_service_time",
+    "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
+    "rs_pooled", "rs_service_time",
     "rs_fill_query", "rs_alloc_pinned", "rs_free_pinned", "rs_device_count"]
 
 
@@ -486,6 +491,24 @@ class Accelerator:
         _check(_lib.rs_pooled(self._h, C.byref(q), out_ptr, stream or None,
                               C.byref(t) if timed else None))
         return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms) if timed else None
+
+    def forward_many(self, sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int,
+                     stream: int = 0, timed: bool = True):
+        """rs_forward_many: n whole queries back to back (FIFO) on one stream.
+        Returns per-query service times in ms when timed (else None)."""
+        n = len(sizes)
+        qs = (CQuery * n)()
+        for i in range(n):
+            qs[i] = CQuery(int(sizes[i]), dense_ptrs[i] or None, idx_ptrs[i] or None, location, 0)
+        outs = (C.c_void_p * n)(*[C.c_void_p(p) for p in out_ptrs])
+        svc = np.zeros(n, dtype=np.float64) if timed else None
+        _check(_lib.rs_forward_many(self._h, n, qs, outs, stream or None,
+                                    svc.ctypes.data_as(P(C.c_double)) if timed else None))
+        return svc
+
+    def sync(self, stream: int = 0) -> None:
+        """rs_sync: wait for `stream`, raise any sticky error (e.g. bad index)."""
+        _check(_lib.rs_sync(self._h, stream or None))
 
     def forward(self, dense: np.ndarray, idx: np.ndarray) -> np.ndarray:
         """Host numpy in, host numpy out (synchronous): logits [S, stacks*out]."""

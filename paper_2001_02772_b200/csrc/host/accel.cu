@@ -62,9 +62,11 @@ struct Slot {
   float* X = nullptr;
   float* pact[2] = {nullptr, nullptr};
   float* out = nullptr;
-  cudaGraphExec_t fwd = nullptr, pool = nullptr;
-  int fwd_kernels = 0, tc_layers = 0;
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  int kernels[3] = {0, 0, 0};
+  int tc_layers = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ready = nullptr, free = nullptr;  // pipelined queue hand-off
   std::vector<void*> allocs;
 };
 
@@ -94,6 +96,11 @@ struct rs_accel {
   int64_t table_bytes = 0, weight_bytes = 0;
   std::mutex mu;
   std::map<cudaStream_t, std::unique_ptr<rs::Slot>> slots;
+  std::unique_ptr<rs::Slot> pipe[2];
+  cudaStream_t copy = nullptr;
+  cudaEvent_t copy_gate = nullptr;
+  std::mutex many_mu;
+  std::vector<cudaEvent_t> evpool;
   std::map<int64_t, double> service_memo;
 };
 
@@ -296,7 +303,8 @@ void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off,
 // writes `final_out`.
 int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, const float* in0,
                   int64_t ld_in0, int64_t in0_rows, float* const* tmp, int64_t ld_tmp,
-                  float* final_out, int64_t ld_final, int64_t final_sCz, cudaStream_t st) {
+                  float* final_out, int64_t ld_final, int64_t final_sCz, bool allow_tc,
+                  cudaStream_t st) {
   const int64_t maxS = a->init.max_query_size;
   int tc_count = 0;
   const float* in = in0;
@@ -315,7 +323,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
     }
     args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
     bool used_tc = false;
-    if (a->init.fc_mode != RS_FC_FP32 && tc_available()) {
+    if (allow_tc) {
       TcPlan p;
       if (tc_plan(&p, args, maxS, a_rows)) {
         launch_fc_tc(s->d_q, p, args, st);
@@ -329,20 +337,26 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
   return tc_count;
 }
 
-cudaGraphExec_t capture(rs_accel* a, Slot* s, bool full, int* kernels, int* tc_layers) {
+// Graph kinds per slot: the embedding stage alone (rs_pooled), the whole
+// forward with FFMA FC layers (small batches / fp32 parity) and the whole
+// forward with tcgen05 FC layers wherever the layer shape fills a tile.
+enum GraphKind { kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kNumGraphs = 3 };
+constexpr int64_t kAutoTcMinItems = 128;  // one full UMMA M tile
+
+cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_layers) {
   cudaStream_t st = s->cap;
   cudaGraph_t g = nullptr;
   RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   const rs_model_desc& m = a->m;
   const int64_t maxS = a->init.max_query_size;
-  int tc = 0;
-  cudaMemsetAsync(s->d_err, 0, sizeof(int), st);
-  if (!full) {
+  const bool tc = kind == kGraphLarge;
+  int ntc = 0;
+  if (kind == kGraphPool) {
     enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, st);
   } else {
     if (m.has_dense_fc)
-      tc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
-                          a->max_dense_w, s->X, a->ld_x, 0, st);
+      ntc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
+                           a->max_dense_w, s->X, a->ld_x, 0, tc, st);
     if (m.pooling == RS_POOL_SUM) {
       if (a->T > 0) {
         enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, st);
@@ -353,8 +367,8 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, bool full, int* kernels, int* tc_l
     } else {
       enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, st);
     }
-    tc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w, s->out,
-                        a->out_w, a->out_dim, st);
+    ntc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w,
+                         s->out, a->out_w, a->out_dim, tc, st);
   }
   cudaError_t le = cudaGetLastError();
   cudaError_t ce = cudaStreamEndCapture(st, &g);
@@ -376,14 +390,11 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, bool full, int* kernels, int* tc_l
   RS_CUDA(cudaGraphInstantiate(&exec, g, 0));
   RS_CUDA(cudaGraphDestroy(g));
   if (kernels) *kernels = k;
-  if (tc_layers) *tc_layers = tc;
+  if (tc_layers) *tc_layers = ntc;
   return exec;
 }
 
-Slot* get_slot(rs_accel* a, cudaStream_t st) {
-  std::lock_guard<std::mutex> lock(a->mu);
-  auto it = a->slots.find(st);
-  if (it != a->slots.end()) return it->second.get();
+std::unique_ptr<Slot> make_slot(rs_accel* a) {
   RS_CUDA(cudaSetDevice(a->device));
   auto s = std::make_unique<Slot>();
   const int64_t maxS = a->init.max_query_size;
@@ -399,26 +410,51 @@ Slot* get_slot(rs_accel* a, cudaStream_t st) {
   s->idx_stage = static_cast<int64_t*>(
       dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->T * a->L, 1) * 8)));
   for (int i = 0; i < 2; ++i) {
-    s->act[i] = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->max_dense_w, 4) * 4)));
+    s->act[i] = static_cast<float*>(
+        dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->max_dense_w, 4) * 4)));
     s->pact[i] = static_cast<float*>(dmalloc(
         a, s->allocs, (size_t)(a->stacks * maxS * std::max<int64_t>(a->max_pred_w, 4) * 4)));
   }
-  s->pooled = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->pooled_dim, 1) * 4)));
+  s->pooled = static_cast<float*>(
+      dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->pooled_dim, 1) * 4)));
   s->X = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_x * 4)));
   s->out = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->out_w * 4)));
   for (auto& e : s->ev) RS_CUDA(cudaEventCreate(&e));
+  RS_CUDA(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&s->free, cudaEventDisableTiming));
   RS_CUDA(cudaDeviceSynchronize());
-  s->fwd = capture(a, s.get(), true, &s->fwd_kernels, &s->tc_layers);
-  s->pool = capture(a, s.get(), false, nullptr, nullptr);
+  s->graph[kGraphPool] = capture(a, s.get(), kGraphPool, nullptr, nullptr);
+  if (a->init.fc_mode != RS_FC_TF32 || !tc_available())
+    s->graph[kGraphSmall] = capture(a, s.get(), kGraphSmall, &s->kernels[kGraphSmall], nullptr);
+  if (a->init.fc_mode != RS_FC_FP32 && tc_available())
+    s->graph[kGraphLarge] =
+        capture(a, s.get(), kGraphLarge, &s->kernels[kGraphLarge], &s->tc_layers);
+  return s;
+}
+
+Slot* get_slot(rs_accel* a, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(a->mu);
+  auto it = a->slots.find(st);
+  if (it != a->slots.end()) return it->second.get();
+  auto s = make_slot(a);
   Slot* raw = s.get();
   a->slots.emplace(st, std::move(s));
   return raw;
 }
 
+// The two slots of the pipelined host-input queue (rs_forward_many).
+Slot* get_pipe_slot(rs_accel* a, int i) {
+  std::lock_guard<std::mutex> lock(a->mu);
+  if (!a->pipe[i]) a->pipe[i] = make_slot(a);
+  if (!a->copy) RS_CUDA(cudaStreamCreateWithFlags(&a->copy, cudaStreamNonBlocking));
+  return a->pipe[i].get();
+}
+
 void free_slot(Slot* s) {
-  if (s->fwd) cudaGraphExecDestroy(s->fwd);
-  if (s->pool) cudaGraphExecDestroy(s->pool);
+  for (auto g : s->graph) if (g) cudaGraphExecDestroy(g);
   for (auto e : s->ev) if (e) cudaEventDestroy(e);
+  if (s->ready) cudaEventDestroy(s->ready);
+  if (s->free) cudaEventDestroy(s->free);
   for (void* p : s->allocs) cudaFree(p);
   if (s->h_q) cudaFreeHost(s->h_q);
   if (s->h_err) cudaFreeHost(s->h_err);
@@ -431,58 +467,101 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+void check_query(rs_accel* a, const rs_query* q) {
+  if (!q) raise(RS_E_INVALID, "null query");
+  if (q->size < 1) raise(RS_E_INVALID, "query_size < 1");
+  if (q->size > a->init.max_query_size) raise(RS_E_CAPACITY, "query larger than max_query_size");
+  if (q->location != RS_MEM_HOST && q->location != RS_MEM_DEVICE)
+    raise(RS_E_INVALID, "bad memory location");
+  if (a->T > 0 && !q->indices) raise(RS_E_INVALID, "null indices");
+}
+
+// Stage one query's inputs for slot s on stream st: dense features into the
+// bottom-MLP staging buffer (or straight into X[:, 0:dense_in] when there is
+// no dense stack), indices into the slot's staging buffer (host) or by
+// pointer (device), then the 16-byte device descriptor.
+void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream_t st) {
+  const int64_t S = q->size;
+  const bool host = q->location == RS_MEM_HOST;
+  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if (full && a->dense_in > 0) {
+    if (!q->dense) raise(RS_E_INVALID, "null dense features");
+    float* dst = a->m.has_dense_fc ? s->dense_stage : s->X;
+    const int64_t ld = a->m.has_dense_fc ? a->ld_dense : a->ld_x;
+    if (ld == a->dense_in)
+      RS_CUDA(cudaMemcpyAsync(dst, q->dense, (size_t)(S * a->dense_in * 4), kind, st));
+    else
+      RS_CUDA(cudaMemcpy2DAsync(dst, (size_t)(ld * 4), q->dense, (size_t)(a->dense_in * 4),
+                                (size_t)(a->dense_in * 4), (size_t)S, kind, st));
+  }
+  const int64_t* idx = nullptr;
+  if (a->T > 0) {
+    if (host) {
+      RS_CUDA(cudaMemcpyAsync(s->idx_stage, q->indices, (size_t)(S * a->T * a->L * 8),
+                              cudaMemcpyHostToDevice, st));
+      idx = s->idx_stage;
+    } else {
+      idx = q->indices;
+    }
+  }
+  const int r = s->ring;
+  s->ring = (s->ring + 1) % kDescRing;
+  s->h_q[r].S = S;
+  s->h_q[r].idx = idx;
+  RS_CUDA(cudaMemcpyAsync(s->d_q, &s->h_q[r], sizeof(QDesc), cudaMemcpyHostToDevice, st));
+}
+
+cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full) {
+  if (!full) return s->graph[kGraphPool];
+  cudaGraphExec_t small = s->graph[kGraphSmall], large = s->graph[kGraphLarge];
+  if (!large) return small;
+  if (!small) return large;
+  return S >= kAutoTcMinItems ? large : small;
+}
+
+void launch_stage(rs_accel* a, Slot* s, const rs_query* q, float* out, bool full,
+                  cudaStream_t st) {
+  const int64_t S = q->size;
+  RS_CUDA(cudaGraphLaunch(pick_graph(a, s, S, full), st));
+  const int64_t w = full ? a->out_w : a->pooled_dim;
+  const float* src = full ? s->out : s->pooled;
+  RS_CUDA(cudaMemcpyAsync(out, src, (size_t)(S * w * 4),
+                          q->location == RS_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                     : cudaMemcpyDeviceToDevice,
+                          st));
+}
+
+// Errors are sticky per slot: kernels OR bits into d_err; a synchronising
+// call reads, clears and reports them.
+void collect_errors(Slot* s, cudaStream_t st) {
+  RS_CUDA(cudaMemcpyAsync(s->h_err, s->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  if (s->h_err[0]) {
+    s->h_err[0] = 0;
+    RS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int), st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    raise(RS_E_INDEX, "embedding index outside [0, rows_per_table)");
+  }
+}
+
 int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* timing,
         bool full) {
   return guarded([&] {
-    if (!a || !q || !out) raise(RS_E_INVALID, "null argument");
-    if (q->size < 1) raise(RS_E_INVALID, "query_size < 1");
-    if (q->size > a->init.max_query_size)
-      raise(RS_E_CAPACITY, "query larger than max_query_size");
-    if (q->location != RS_MEM_HOST && q->location != RS_MEM_DEVICE)
-      raise(RS_E_INVALID, "bad memory location");
+    if (!a || !out) raise(RS_E_INVALID, "null argument");
+    check_query(a, q);
     RS_CUDA(cudaSetDevice(a->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->own;
     Slot* s = get_slot(a, st);
-    const int64_t S = q->size;
-    const bool host = q->location == RS_MEM_HOST;
-    const cudaMemcpyKind in_kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-    const cudaMemcpyKind out_kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (timing) RS_CUDA(cudaEventRecord(s->ev[0], st));
-    // dense features: into the bottom-MLP staging buffer, or straight into
-    // the predict input X[:, 0:dense_in] when there is no dense stack
-    if (full && a->dense_in > 0) {
-      if (!q->dense) raise(RS_E_INVALID, "null dense features");
-      float* dst = a->m.has_dense_fc ? s->dense_stage : s->X;
-      const int64_t ld = a->m.has_dense_fc ? a->ld_dense : a->ld_x;
-      if (ld == a->dense_in)
-        RS_CUDA(cudaMemcpyAsync(dst, q->dense, (size_t)(S * a->dense_in * 4), in_kind, st));
-      else
-        RS_CUDA(cudaMemcpy2DAsync(dst, (size_t)(ld * 4), q->dense, (size_t)(a->dense_in * 4),
-                                  (size_t)(a->dense_in * 4), (size_t)S, in_kind, st));
-    }
-    const int64_t* idx = nullptr;
-    if (a->T > 0) {
-      if (!q->indices) raise(RS_E_INVALID, "null indices");
-      if (host) {
-        RS_CUDA(cudaMemcpyAsync(s->idx_stage, q->indices, (size_t)(S * a->T * a->L * 8),
-                                cudaMemcpyHostToDevice, st));
-        idx = s->idx_stage;
-      } else {
-        idx = q->indices;
-      }
-    }
-    const int slot_i = s->ring;
-    s->ring = (s->ring + 1) % kDescRing;
-    s->h_q[slot_i].S = S;
-    s->h_q[slot_i].idx = idx;
-    RS_CUDA(cudaMemcpyAsync(s->d_q, &s->h_q[slot_i], sizeof(QDesc), cudaMemcpyHostToDevice, st));
+    stage_inputs(a, s, q, full, st);
     if (timing) RS_CUDA(cudaEventRecord(s->ev[1], st));
-    RS_CUDA(cudaGraphLaunch(full ? s->fwd : s->pool, st));
+    RS_CUDA(cudaGraphLaunch(pick_graph(a, s, q->size, full), st));
     if (timing) RS_CUDA(cudaEventRecord(s->ev[2], st));
     const int64_t w = full ? a->out_w : a->pooled_dim;
-    const float* src = full ? s->out : s->pooled;
-    RS_CUDA(cudaMemcpyAsync(out, src, (size_t)(S * w * 4), out_kind, st));
-    RS_CUDA(cudaMemcpyAsync(&s->h_err[slot_i], s->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaMemcpyAsync(out, full ? s->out : s->pooled, (size_t)(q->size * w * 4),
+                            q->location == RS_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                       : cudaMemcpyDeviceToDevice,
+                            st));
     if (timing) {
       RS_CUDA(cudaEventRecord(s->ev[3], st));
       RS_CUDA(cudaEventSynchronize(s->ev[3]));
@@ -490,8 +569,67 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
       timing->compute_ms = elapsed(s->ev[1], s->ev[2]);
       timing->d2h_ms = elapsed(s->ev[2], s->ev[3]);
       timing->total_ms = elapsed(s->ev[0], s->ev[3]);
-      if (s->h_err[slot_i] & kErrIndex)
-        raise(RS_E_INDEX, "embedding index outside [0, rows_per_table)");
+      collect_errors(s, st);
+    }
+  });
+}
+
+int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, void* stream,
+             double* service_ms) {
+  return guarded([&] {
+    if (!a || !qs || !outs) raise(RS_E_INVALID, "null argument");
+    if (n < 1) raise(RS_E_INVALID, "n < 1");
+    const int loc = qs[0].location;
+    for (int64_t i = 0; i < n; ++i) {
+      check_query(a, &qs[i]);
+      if (qs[i].location != loc) raise(RS_E_INVALID, "mixed memory locations in one batch");
+      if (!outs[i]) raise(RS_E_INVALID, "null output");
+    }
+    RS_CUDA(cudaSetDevice(a->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->own;
+    std::lock_guard<std::mutex> many_lock(a->many_mu);
+    if (service_ms) {
+      while ((int64_t)a->evpool.size() < n + 1) {
+        cudaEvent_t e;
+        RS_CUDA(cudaEventCreate(&e));
+        a->evpool.push_back(e);
+      }
+      RS_CUDA(cudaEventRecord(a->evpool[0], st));
+    }
+    Slot* used[2] = {nullptr, nullptr};
+    if (loc == RS_MEM_DEVICE) {
+      Slot* s = get_slot(a, st);
+      used[0] = s;
+      for (int64_t i = 0; i < n; ++i) {
+        stage_inputs(a, s, &qs[i], true, st);
+        launch_stage(a, s, &qs[i], outs[i], true, st);
+        if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[i + 1], st));
+      }
+    } else {
+      // Host inputs: a two-slot queue. The copy stream stages query i+1's
+      // H2D while the compute stream runs query i; FIFO order is kept on the
+      // compute stream (the single accelerator server of sim.cpp:126-136).
+      Slot* p[2] = {get_pipe_slot(a, 0), get_pipe_slot(a, 1)};
+      used[0] = p[0];
+      used[1] = p[1];
+      RS_CUDA(cudaEventRecord(a->copy_gate, st));
+      RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
+      for (int64_t i = 0; i < n; ++i) {
+        Slot* s = p[i & 1];
+        RS_CUDA(cudaStreamWaitEvent(a->copy, s->free, 0));
+        stage_inputs(a, s, &qs[i], true, a->copy);
+        RS_CUDA(cudaEventRecord(s->ready, a->copy));
+        RS_CUDA(cudaStreamWaitEvent(st, s->ready, 0));
+        launch_stage(a, s, &qs[i], outs[i], true, st);
+        RS_CUDA(cudaEventRecord(s->free, st));
+        if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[i + 1], st));
+      }
+    }
+    if (service_ms) {
+      RS_CUDA(cudaEventSynchronize(a->evpool[n]));
+      for (int64_t i = 0; i < n; ++i) service_ms[i] = elapsed(a->evpool[i], a->evpool[i + 1]);
+      for (Slot* s : used)
+        if (s) collect_errors(s, st);
     }
   });
 }
@@ -550,6 +688,7 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     a->sm_count = prop.multiProcessorCount;
     a->l2_bytes = prop.l2CacheSize;
     RS_CUDA(cudaStreamCreateWithFlags(&a->own, cudaStreamNonBlocking));
+    RS_CUDA(cudaEventCreateWithFlags(&a->copy_gate, cudaEventDisableTiming));
     build_model(a);
     *out = a;
   });
@@ -568,6 +707,11 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
     cudaDeviceSynchronize();
     for (auto& kv : a->slots) free_slot(kv.second.get());
     a->slots.clear();
+    for (auto& p : a->pipe)
+      if (p) free_slot(p.get());
+    for (auto e : a->evpool) cudaEventDestroy(e);
+    if (a->copy_gate) cudaEventDestroy(a->copy_gate);
+    if (a->copy) cudaStreamDestroy(a->copy);
     for (void* p : a->allocs) cudaFree(p);
     if (a->own) cudaStreamDestroy(a->own);
     delete a;
@@ -582,7 +726,8 @@ extern "C" int rs_accel_info_get(const rs_accel* ca, rs_accel_info* out) {
     rs_accel_info i{};
     i.device = a->device;
     i.sm_count = a->sm_count;
-    i.kernels_per_forward = s->fwd_kernels;
+    i.kernels_per_forward = s->kernels[kGraphLarge] ? s->kernels[kGraphLarge] : s->kernels[kGraphSmall];
+    i.kernels_per_forward_small = s->kernels[kGraphSmall];
     i.fc_layers_tcgen05 = s->tc_layers;
     i.predict_input_dim = a->p_in;
     i.output_dim = a->out_w;
@@ -597,6 +742,24 @@ extern "C" int rs_accel_info_get(const rs_accel* ca, rs_accel_info* out) {
 extern "C" int rs_forward(rs_accel* a, const rs_query* q, float* out, void* stream,
                           rs_timing* timing) {
   return run(a, q, out, stream, timing, true);
+}
+
+extern "C" int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
+                               float* const* outs, void* stream, double* service_ms) {
+  return run_many(a, n, queries, outs, stream, service_ms);
+}
+
+extern "C" int rs_sync(rs_accel* a, void* stream) {
+  return guarded([&] {
+    if (!a) raise(RS_E_INVALID, "null handle");
+    RS_CUDA(cudaSetDevice(a->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->own;
+    RS_CUDA(cudaStreamSynchronize(st));
+    Slot* s = get_slot(a, st);
+    collect_errors(s, st);
+    for (auto& p : a->pipe)
+      if (p) collect_errors(p.get(), st);
+  });
 }
 
 extern "C" int rs_pooled(rs_accel* a, const rs_query* q, float* out, void* stream,

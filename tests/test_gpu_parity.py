@@ -148,3 +148,53 @@ def test_cfg3_rmc2_ten_million_rows():
                         predict_fc=rs.LayerStack([512, 128, 1]),
                         embeddings=rs.EmbeddingConfig(32, 80, 64, "Sum"), dense_input_dim=256)
     check_forward(spec, rows=10_000_000, S=16, max_q=64)
+
+
+def test_forward_many_matches_single_calls_and_auto_graphs():
+    """rs_forward_many (pipelined host queue and device path) returns the same
+    logits as one-at-a-time rs_forward; AUTO mode picks the FFMA graph below
+    128 items and the tcgen05 graph at or above, each within its tolerance."""
+    torch = pytest.importorskip("torch")
+    spec = rs.builtin_model("DLRM-RMC3")
+    rows = 3000
+    acc = rs.Accelerator(spec, rows, seed=8, max_query_size=400, fc_mode=rs.FC_AUTO)
+    assert acc.info.fc_layers_tcgen05 > 0
+    assert acc.info.kernels_per_forward_small > 0
+    orc = Oracle(spec, rows, seed=8)
+    sizes = [5, 200, 1, 399, 127, 128]
+    qs = [rs.fill_query(spec, rows, 3, i, S) for i, S in enumerate(sizes)]
+    singles = [acc.forward(d, i) for d, i in qs]
+    for (d, i), out, S in zip(qs, singles, sizes):
+        ref, mag, _, _ = orc.forward64(d, i)
+        tol = TF32_TOL if S >= 128 else FP32_TOL
+        assert rel_err(out, ref, mag) <= tol, S
+    # host path through the two-slot queue
+    hd = [rs.PinnedBuffer(max(d.nbytes, 16)) for d, _ in qs]
+    hi = [rs.PinnedBuffer(i.nbytes) for _, i in qs]
+    ho = [rs.PinnedBuffer(S * acc.output_dim * 4) for S in sizes]
+    for k, (d, i) in enumerate(qs):
+        hd[k].view(np.float32, d.shape)[...] = d
+        hi[k].view(np.int64, i.shape)[...] = i
+    svc = acc.forward_many(sizes, [b.ptr for b in hd], [b.ptr for b in hi], [b.ptr for b in ho],
+                           rs.MEM_HOST)
+    assert len(svc) == len(sizes) and (svc > 0).all()
+    for k, S in enumerate(sizes):
+        assert np.array_equal(ho[k].view(np.float32, (S, acc.output_dim)), singles[k])
+    # device path
+    dd = [torch.from_numpy(d).cuda() for d, _ in qs]
+    di = [torch.from_numpy(i).cuda() for _, i in qs]
+    do = [torch.empty((S, acc.output_dim), device="cuda") for S in sizes]
+    acc.forward_many(sizes, [t.data_ptr() for t in dd], [t.data_ptr() for t in di],
+                     [t.data_ptr() for t in do], rs.MEM_DEVICE)
+    for k in range(len(sizes)):
+        assert np.array_equal(do[k].cpu().numpy(), singles[k])
+    # a bad index in an asynchronous call is reported by rs_sync, then cleared
+    d, i = qs[0]
+    bad = i.copy()
+    bad[0, 0, 0] = rows + 5
+    di_bad = torch.from_numpy(bad).cuda()
+    acc.forward_ptr(5, dd[0].data_ptr(), di_bad.data_ptr(), do[0].data_ptr(), rs.MEM_DEVICE)
+    with pytest.raises(rs.IndexOutOfRange):
+        acc.sync()
+    acc.sync()
+    acc.close()
