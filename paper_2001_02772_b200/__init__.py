@@ -128,7 +128,8 @@ class CQpsResult(C.Structure):
 class CInitDesc(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("rows_per_table", C.c_int64),
                 ("max_query_size", C.c_int64), ("fc_mode", C.c_int32),
-                ("rnn_cell", C.c_int32), ("l2_persist_mb", C.c_int32), ("reserved", C.c_int32)]
+                ("rnn_cell", C.c_int32), ("l2_persist_mb", C.c_int32),
+                ("queue_depth", C.c_int32)]
 
 
 class CQuery(C.Structure):
@@ -446,12 +447,12 @@ class Accelerator:
 
     def __init__(self, model: ModelSpec, rows_per_table: int, seed: int = 1,
                  device: int = 0, max_query_size: int = 1000, fc_mode: int = FC_FP32,
-                 rnn_cell: int = RNN_GRU):
+                 rnn_cell: int = RNN_GRU, queue_depth: int = 2):
         self.model = model
         self.rows = rows_per_table
         self.seed = seed
         self._desc = model.to_c()
-        init = CInitDesc(seed, rows_per_table, max_query_size, fc_mode, rnn_cell, 0, 0)
+        init = CInitDesc(seed, rows_per_table, max_query_size, fc_mode, rnn_cell, 0, queue_depth)
         h = C.c_void_p()
         _check(_lib.rs_accel_create(C.byref(self._desc), C.byref(init), device, C.byref(h)))
         self._h = h

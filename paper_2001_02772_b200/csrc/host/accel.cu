@@ -67,6 +67,8 @@ struct Slot {
   int tc_layers = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ready = nullptr, free = nullptr;  // pipelined queue hand-off
+  cudaStream_t cap2 = nullptr;                  // capture: parallel graph branch
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<void*> allocs;
 };
 
@@ -96,7 +98,12 @@ struct rs_accel {
   int64_t table_bytes = 0, weight_bytes = 0;
   std::mutex mu;
   std::map<cudaStream_t, std::unique_ptr<rs::Slot>> slots;
-  std::unique_ptr<rs::Slot> pipe[2];
+  // rs_forward_many queue: `depth` lanes, each a compute stream + a slot
+  static constexpr int kMaxLanes = 4;
+  int depth = 2;
+  std::unique_ptr<rs::Slot> pipe[kMaxLanes];
+  cudaStream_t lane[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t lane_join[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t copy = nullptr;
   cudaEvent_t copy_gate = nullptr;
   std::mutex many_mu;
@@ -354,18 +361,28 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   if (kind == kGraphPool) {
     enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, st);
   } else {
+    // The bottom MLP and the embedding stage are independent (they write
+    // disjoint columns of X): capture them as parallel graph branches.
+    const bool fork = m.has_dense_fc && a->T > 0;
+    if (fork) {
+      RS_CUDA(cudaEventRecord(s->fork, st));
+      RS_CUDA(cudaStreamWaitEvent(s->cap2, s->fork, 0));
+    }
     if (m.has_dense_fc)
       ntc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
-                           a->max_dense_w, s->X, a->ld_x, 0, tc, st);
+                           a->max_dense_w, s->X, a->ld_x, 0, tc, fork ? s->cap2 : st);
+    if (fork) RS_CUDA(cudaEventRecord(s->join, s->cap2));
     if (m.pooling == RS_POOL_SUM) {
       if (a->T > 0) {
         enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, st);
+        if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
         launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
                            a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
                            a->sm_count, st);
       }
     } else {
       enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, st);
+      if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
     }
     ntc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w,
                          s->out, a->out_w, a->out_dim, tc, st);
@@ -422,6 +439,9 @@ std::unique_ptr<Slot> make_slot(rs_accel* a) {
   for (auto& e : s->ev) RS_CUDA(cudaEventCreate(&e));
   RS_CUDA(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&s->free, cudaEventDisableTiming));
+  RS_CUDA(cudaStreamCreateWithFlags(&s->cap2, cudaStreamNonBlocking));
+  RS_CUDA(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
   RS_CUDA(cudaDeviceSynchronize());
   s->graph[kGraphPool] = capture(a, s.get(), kGraphPool, nullptr, nullptr);
   if (a->init.fc_mode != RS_FC_TF32 || !tc_available())
@@ -447,6 +467,10 @@ Slot* get_pipe_slot(rs_accel* a, int i) {
   std::lock_guard<std::mutex> lock(a->mu);
   if (!a->pipe[i]) a->pipe[i] = make_slot(a);
   if (!a->copy) RS_CUDA(cudaStreamCreateWithFlags(&a->copy, cudaStreamNonBlocking));
+  if (!a->lane[i]) {
+    RS_CUDA(cudaStreamCreateWithFlags(&a->lane[i], cudaStreamNonBlocking));
+    RS_CUDA(cudaEventCreateWithFlags(&a->lane_join[i], cudaEventDisableTiming));
+  }
   return a->pipe[i].get();
 }
 
@@ -459,6 +483,9 @@ void free_slot(Slot* s) {
   if (s->h_q) cudaFreeHost(s->h_q);
   if (s->h_err) cudaFreeHost(s->h_err);
   if (s->cap) cudaStreamDestroy(s->cap);
+  if (s->cap2) cudaStreamDestroy(s->cap2);
+  if (s->fork) cudaEventDestroy(s->fork);
+  if (s->join) cudaEventDestroy(s->join);
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -596,40 +623,48 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
       }
       RS_CUDA(cudaEventRecord(a->evpool[0], st));
     }
-    Slot* used[2] = {nullptr, nullptr};
-    if (loc == RS_MEM_DEVICE) {
-      Slot* s = get_slot(a, st);
-      used[0] = s;
-      for (int64_t i = 0; i < n; ++i) {
-        stage_inputs(a, s, &qs[i], true, st);
-        launch_stage(a, s, &qs[i], outs[i], true, st);
-        if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[i + 1], st));
-      }
-    } else {
-      // Host inputs: a two-slot queue. The copy stream stages query i+1's
-      // H2D while the compute stream runs query i; FIFO order is kept on the
-      // compute stream (the single accelerator server of sim.cpp:126-136).
-      Slot* p[2] = {get_pipe_slot(a, 0), get_pipe_slot(a, 1)};
-      used[0] = p[0];
-      used[1] = p[1];
-      RS_CUDA(cudaEventRecord(a->copy_gate, st));
-      RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
-      for (int64_t i = 0; i < n; ++i) {
-        Slot* s = p[i & 1];
+    // Queries are dispatched in FIFO order round-robin over `depth` lanes
+    // (compute stream + scratch slot each), so query i+1's embedding gather
+    // overlaps query i's latency-bound FC tail. Host inputs are staged by one
+    // copy stream that runs ahead of compute (a lane's next H2D waits only for
+    // that lane's previous query to release its staging buffers).
+    const int depth = a->depth;
+    Slot* p[rs_accel::kMaxLanes] = {};
+    for (int d = 0; d < depth; ++d) p[d] = get_pipe_slot(a, d);
+    RS_CUDA(cudaEventRecord(a->copy_gate, st));
+    for (int d = 0; d < depth; ++d) RS_CUDA(cudaStreamWaitEvent(a->lane[d], a->copy_gate, 0));
+    if (loc == RS_MEM_HOST) RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
+    for (int64_t i = 0; i < n; ++i) {
+      const int d = (int)(i % depth);
+      Slot* s = p[d];
+      cudaStream_t ls = a->lane[d];
+      if (loc == RS_MEM_HOST) {
         RS_CUDA(cudaStreamWaitEvent(a->copy, s->free, 0));
         stage_inputs(a, s, &qs[i], true, a->copy);
         RS_CUDA(cudaEventRecord(s->ready, a->copy));
-        RS_CUDA(cudaStreamWaitEvent(st, s->ready, 0));
-        launch_stage(a, s, &qs[i], outs[i], true, st);
-        RS_CUDA(cudaEventRecord(s->free, st));
-        if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[i + 1], st));
+        RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
+      } else {
+        stage_inputs(a, s, &qs[i], true, ls);
       }
+      launch_stage(a, s, &qs[i], outs[i], true, ls);
+      RS_CUDA(cudaEventRecord(s->free, ls));
+      if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[i + 1], ls));
+    }
+    for (int d = 0; d < depth; ++d) {
+      RS_CUDA(cudaEventRecord(a->lane_join[d], a->lane[d]));
+      RS_CUDA(cudaStreamWaitEvent(st, a->lane_join[d], 0));
     }
     if (service_ms) {
-      RS_CUDA(cudaEventSynchronize(a->evpool[n]));
-      for (int64_t i = 0; i < n; ++i) service_ms[i] = elapsed(a->evpool[i], a->evpool[i + 1]);
-      for (Slot* s : used)
-        if (s) collect_errors(s, st);
+      RS_CUDA(cudaStreamSynchronize(st));
+      // Deliveries are in FIFO order: query i is delivered when it and every
+      // earlier query completed; service = gap between deliveries.
+      double prev = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        const double done = std::max(prev, (double)elapsed(a->evpool[0], a->evpool[i + 1]));
+        service_ms[i] = done - prev;
+        prev = done;
+      }
+      for (int d = 0; d < depth; ++d) collect_errors(p[d], st);
     }
   });
 }
@@ -684,6 +719,7 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     a = new rs_accel();
     a->m = *model;
     a->init = *init;
+    a->depth = init->queue_depth > 0 ? std::min<int>(init->queue_depth, rs_accel::kMaxLanes) : 2;
     a->device = device;
     a->sm_count = prop.multiProcessorCount;
     a->l2_bytes = prop.l2CacheSize;
@@ -712,6 +748,10 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
     for (auto e : a->evpool) cudaEventDestroy(e);
     if (a->copy_gate) cudaEventDestroy(a->copy_gate);
     if (a->copy) cudaStreamDestroy(a->copy);
+    for (int d = 0; d < rs_accel::kMaxLanes; ++d) {
+      if (a->lane[d]) cudaStreamDestroy(a->lane[d]);
+      if (a->lane_join[d]) cudaEventDestroy(a->lane_join[d]);
+    }
     for (void* p : a->allocs) cudaFree(p);
     if (a->own) cudaStreamDestroy(a->own);
     delete a;

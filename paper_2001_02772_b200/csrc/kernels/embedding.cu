@@ -280,21 +280,55 @@ din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
 // with v_0 = X[item, 0:D] (bottom-MLP output already written there) and
 // v_t = pooled[item, t-1, :]. Pairs exist only when has_dense (the
 // reference counts them only for Sum pooling with a dense stack).
-__global__ void __launch_bounds__(128)
+constexpr int kInterThreads = 256;
+constexpr int kInterRegs = 8;  // float4 loads in flight per thread per round
+
+__global__ void __launch_bounds__(kInterThreads)
 interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
                    int64_t ld_pooled, int T, int D, float* __restrict__ X, int64_t ld_x,
                    int64_t sum_off, int64_t dot_off, int has_dense) {
   extern __shared__ float sv[];  // [(T+1)][D+1]
   const int P = has_dense ? (T + 1) * T / 2 : 0;
   const int ldv = D + 1;
+  const bool vec = (D & 3) == 0;
+  const int D4 = D / 4;
+  const int units = (T + 1) * D4;       // float4 units: v0 then pooled rows
   for (int64_t item = blockIdx.x; item < qd->S; item += gridDim.x) {
     __syncthreads();
-    for (int i = threadIdx.x; i < (T + 1) * D; i += blockDim.x) {
-      const int v = i / D, c = i - v * D;
-      float x;
-      if (v == 0) x = has_dense ? X[item * ld_x + c] : 0.f;
-      else x = pooled[item * ld_pooled + (int64_t)(v - 1) * D + c];
-      sv[v * ldv + c] = x;
+    if (!vec) {
+      for (int i = threadIdx.x; i < (T + 1) * D; i += blockDim.x) {
+        const int v = i / D, c = i - v * D;
+        sv[v * ldv + c] = v == 0 ? (has_dense ? X[item * ld_x + c] : 0.f)
+                                 : pooled[item * ld_pooled + (int64_t)(v - 1) * D + c];
+      }
+    }
+    // All of a round's 128-bit loads are issued before any shared store, so a
+    // CTA pays one memory latency per round instead of one per element.
+    for (int base = 0; vec && base < units; base += kInterRegs * kInterThreads) {
+      float4 r[kInterRegs];
+#pragma unroll
+      for (int k = 0; k < kInterRegs; ++k) {
+        const int u = base + k * kInterThreads + threadIdx.x;
+        r[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u < units) {
+          const int v = u / D4, c4 = u - v * D4;
+          if (v == 0) {
+            if (has_dense) r[k] = *reinterpret_cast<const float4*>(X + item * ld_x + c4 * 4);
+          } else {
+            r[k] = __ldg(reinterpret_cast<const float4*>(pooled + item * ld_pooled +
+                                                         (int64_t)(v - 1) * D) + c4);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kInterRegs; ++k) {
+        const int u = base + k * kInterThreads + threadIdx.x;
+        if (u < units) {
+          const int v = u / D4, c = (u - v * D4) * 4;
+          float* d = sv + v * ldv + c;
+          d[0] = r[k].x; d[1] = r[k].y; d[2] = r[k].z; d[3] = r[k].w;
+        }
+      }
     }
     __syncthreads();
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
@@ -401,9 +435,12 @@ void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
                         int64_t max_items, int sm_count, cudaStream_t s) {
   const size_t smem = (size_t)(T + 1) * (D + 1) * sizeof(float);
-  const int grid = grid_for(max_items, 1, sm_count, 16);
-  interaction_kernel<<<grid, 128, smem, s>>>(qd, pooled, ld_pooled, T, D, X, ld_x, sum_off,
-                                             dot_off, has_dense);
+  const int grid = grid_for(max_items, 1, sm_count, 8);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(interaction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  interaction_kernel<<<grid, kInterThreads, smem, s>>>(qd, pooled, ld_pooled, T, D, X, ld_x,
+                                                       sum_off, dot_off, has_dense);
 }
 
 size_t interaction_smem(int T, int D) { return (size_t)(T + 1) * (D + 1) * sizeof(float); }
