@@ -220,22 +220,31 @@ int or_sls_canonical(const or_state* s, int64_t S, const int64_t* idx, float* po
     const int64_t lpr = D / 4 < 32 ? D / 4 : 32;
     R = (int)(32 / lpr);
   }
+  /* Power-of-two D: 32-lookup chunks, R-interleaved partials inside a chunk,
+   * pairwise tree, then chunk sums left to right. Other D: one sequential sum. */
+  const int chunked = R > 1 || (D == 128 || D == 256);
+  const int64_t CH = chunked ? 32 : L;
   float row[256];
   float part[32][256];
+  float total[256];
   for (int64_t bag = 0; bag < S * T; ++bag) {
     const int64_t t = bag % T;
-    for (int g = 0; g < R; ++g)
-      for (int64_t c = 0; c < D; ++c) part[g][c] = 0.0f;
-    for (int64_t l = 0; l < L; ++l) {
-      const float* e = or_row(s, t, idx[bag * L + l], row);
-      if (!e) return -7;
-      float* p = part[l % R];
-      for (int64_t c = 0; c < D; ++c) p[c] = p[c] + e[c];
+    for (int64_t l0 = 0; l0 < L; l0 += CH) {
+      const int64_t n = L - l0 < CH ? L - l0 : CH;
+      for (int g = 0; g < R; ++g)
+        for (int64_t c = 0; c < D; ++c) part[g][c] = 0.0f;
+      for (int64_t l = l0; l < l0 + n; ++l) {
+        const float* e = or_row(s, t, idx[bag * L + l], row);
+        if (!e) return -7;
+        float* p = part[(l - l0) % R];
+        for (int64_t c = 0; c < D; ++c) p[c] = p[c] + e[c];
+      }
+      for (int half = R / 2; half >= 1; half /= 2)
+        for (int g = 0; g < half; ++g)
+          for (int64_t c = 0; c < D; ++c) part[g][c] = part[g][c] + part[g + half][c];
+      for (int64_t c = 0; c < D; ++c) total[c] = l0 == 0 ? part[0][c] : total[c] + part[0][c];
     }
-    for (int half = R / 2; half >= 1; half /= 2)
-      for (int g = 0; g < half; ++g)
-        for (int64_t c = 0; c < D; ++c) part[g][c] = part[g][c] + part[g + half][c];
-    for (int64_t c = 0; c < D; ++c) pooled[bag * D + c] = part[0][c];
+    for (int64_t c = 0; c < D; ++c) pooled[bag * D + c] = total[c];
   }
   return 0;
 }

@@ -14,14 +14,23 @@
 // int64 exactly as the reference's byte model ships them
 // (proj/src/platform.cpp:105-111), so bag (item, t) is L contiguous int64.
 //
-// SLS design: one warp per bag, grid-stride over S*T bags (S read from the
-// device-side query descriptor). The warp stages the bag's index list in
-// shared memory, then reads rows with 128-bit non-allocating loads: LPR =
-// D/4 lanes cover one row, so R = 32/LPR rows land per warp instruction and
-// U unrolled instructions keep R*U rows (R*U*D*4 bytes) in flight per warp.
-// Lane group g accumulates rows g, g+R, g+2R, ... in order; groups combine by
-// an xor-shuffle tree. That order is the canonical SLS summation order that
-// oracle/forward.c restates, so pooled sums are bit-identical to the oracle.
+// SLS design: the unit of work is a CHUNK of 32 consecutive lookups of one
+// bag (a bag of L lookups has ceil(L/32) chunks), so a query of S items has
+// S*T*ceil(L/32) units spread over a persistent grid of warps sized by the
+// occupancy API — fine enough that no warp is left with a whole extra bag
+// while the rest idle (the wave-quantisation loss of warp-per-bag). A warp
+// loads the chunk's 32 indices with one coalesced 256-byte read (lane l holds
+// index l and broadcasts it by shuffle), then reads rows with 128-bit
+// non-allocating loads carrying an L2 evict-first policy (tables are
+// streamed; weights, indices and partials stay cached): LPR = D/4 lanes
+// cover one row, R = 32/LPR rows land per warp instruction, U unrolled
+// instructions keep R*U rows in flight. Lane group g accumulates rows
+// g, g+R, g+2R, ... of the chunk in order; groups combine by an xor-shuffle
+// tree. Multi-chunk bags write their chunk partials to scratch; the warp that
+// completes a bag last (device-scope counter) sums the partials in chunk
+// order. That order — R-interleaved within 32-row chunks, pairwise tree,
+// then chunks left to right — is the canonical SLS order oracle/forward.c
+// restates, so pooled sums are bit-identical to the oracle and run to run.
 #include <algorithm>
 
 #include "common.cuh"
@@ -34,68 +43,96 @@ namespace {
 constexpr int kWarps = 8;      // warps per CTA for warp-per-bag kernels
 constexpr int kIdxChunk = 256; // staged indices per warp per pass
 
-template <int LPR, int VPL, int U>
+constexpr int kChunk = 32;     // lookups per SLS work unit (one index per lane)
+
+template <int LPR, int VPL>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
-               int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err) {
-  constexpr int R = 32 / LPR;
+               int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
+               float* __restrict__ partial, unsigned* __restrict__ arrivals) {
+  constexpr int R = 32 / LPR;           // rows per warp instruction
   constexpr int D = LPR * 4 * VPL;
-  __shared__ int64_t sidx[kWarps][kIdxChunk];
+  constexpr int U = kChunk / R;         // instructions per chunk: all rows in flight
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane / LPR, c = lane % LPR;
   const int64_t S = qd->S;
   const int64_t* __restrict__ idx = qd->idx;
-  const int64_t bags = S * T;
+  const int nch = (L + kChunk - 1) / kChunk;
+  const int64_t units = S * T * nch;
+  const uint64_t pol = l2_evict_first_policy();
   const int64_t stride = (int64_t)gridDim.x * kWarps;
-  for (int64_t bag = (int64_t)blockIdx.x * kWarps + warp; bag < bags; bag += stride) {
+  for (int64_t unit = (int64_t)blockIdx.x * kWarps + warp; unit < units; unit += stride) {
+    const int64_t bag = unit / nch;
+    const int ch = (int)(unit - bag * nch);
     const int t = (int)(bag % T);
+    const int l0 = ch * kChunk;
+    const int n = min(kChunk, L - l0);
     const float4* __restrict__ tab =
         reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
-    const int64_t* __restrict__ bidx = idx + bag * L;
+    const int64_t my_idx = lane < n ? __ldg(idx + bag * L + l0 + lane) : 0;
     float4 acc[VPL];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c0 = 0; c0 < L; c0 += kIdxChunk) {
-      const int n = min(kIdxChunk, L - c0);
-      __syncwarp();
-      for (int l = lane; l < n; l += 32) sidx[warp][l] = __ldg(bidx + c0 + l);
-      __syncwarp();
-      for (int j = 0; j < n; j += R * U) {
-        float4 v[U][VPL];
-        bool ok[U];
+    constexpr int UB = (U * VPL > 16) ? 16 / VPL : U;  // loads in flight per pass
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int l = j + u * R + g;
-          ok[u] = false;
-          if (l < n) {
-            const int64_t r = sidx[warp][l];
-            if ((uint64_t)r < (uint64_t)rows) {
-              ok[u] = true;
-              const float4* p = tab + r * (D / 4) + c;
+    for (int u0 = 0; u0 < U; u0 += UB) {
+      float4 v[UB][VPL];
+      bool ok[UB];
 #pragma unroll
-              for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream(p + k * LPR);
-            } else {
-              atomicOr(err, kErrIndex);
-            }
-          }
+      for (int u = 0; u < UB; ++u) {
+        const int l = (u0 + u) * R + g;
+        const int64_t r = __shfl_sync(0xffffffffu, my_idx, l & 31);
+        ok[u] = l < n && (uint64_t)r < (uint64_t)rows;
+        if (l < n && !ok[u]) atomicOr(err, kErrIndex);
+        if (ok[u]) {
+          const float4* p = tab + r * (D / 4) + c;
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream_hint(p + k * LPR, pol);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (ok[u]) {
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
-          }
       }
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        if (ok[u]) {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
+        }
     }
 #pragma unroll
     for (int off = 16; off >= LPR; off >>= 1)
 #pragma unroll
       for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
-    if (g == 0) {
-      float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
+    float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
+    if (nch == 1) {
+      if (g == 0) {
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
+        for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
+      }
+      continue;
     }
+    // multi-chunk bag: publish this chunk's partial; the last arriver sums
+    // all partials in chunk order and resets the bag's counter.
+    float4* part = reinterpret_cast<float4*>(partial + (bag * nch + ch) * D) + c;
+    if (g == 0) {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) __stcg(part + k * LPR, acc[k]);
+    }
+    __threadfence();
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) prev = atomicAdd(arrivals + bag, 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != (unsigned)(nch - 1)) continue;
+    __threadfence();
+    if (g == 0) {
+      const float4* p0 = reinterpret_cast<const float4*>(partial + bag * nch * D) + c;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        float4 s = __ldcg(p0 + k * LPR);
+        for (int q = 1; q < nch; ++q) add4(s, __ldcg(p0 + q * (D / 4) + k * LPR));
+        o[k * LPR] = s;
+      }
+    }
+    if (lane == 0) arrivals[bag] = 0u;
   }
 }
 
@@ -387,21 +424,46 @@ int grid_for(int64_t units, int per_block, int sm_count, int blocks_per_sm) {
 
 bool sls_vector_path(int64_t D) { return pow2_dim(D); }
 
+template <int LPR, int VPL>
+void launch_sls_vec(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                    float* out, int64_t ld_out, int* err, float* partial, unsigned* arrivals,
+                    int64_t max_items, int sm_count, cudaStream_t s) {
+  // persistent grid: every resident warp slot of the device, no more
+  static const int per_sm = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_sum_kernel<LPR, VPL>, kWarps * 32, 0);
+    return b > 0 ? b : 1;
+  }();
+  const int64_t units = max_items * T * ((L + kChunk - 1) / kChunk);
+  const int grid = grid_for(units, kWarps, sm_count, per_sm);
+  sls_sum_kernel<LPR, VPL><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
+                                                       err, partial, arrivals);
+}
+
+size_t sls_partial_floats(int64_t max_items, int T, int L, int D) {
+  return (size_t)(max_items * T * ((L + kChunk - 1) / kChunk) * D);
+}
+
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
-                    float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
-                    cudaStream_t s) {
-  const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
-  const dim3 blk(kWarps * 32);
+                    float* out, int64_t ld_out, int* err, float* partial, unsigned* arrivals,
+                    int64_t max_items, int sm_count, cudaStream_t s) {
+#define RS_SLS(LPR, VPL) \
+  launch_sls_vec<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, err, partial, arrivals, \
+                           max_items, sm_count, s)
   switch (D) {
-    case 8: sls_sum_kernel<2, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
-    case 16: sls_sum_kernel<4, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
-    case 32: sls_sum_kernel<8, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
-    case 64: sls_sum_kernel<16, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
-    case 128: sls_sum_kernel<32, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
-    case 256: sls_sum_kernel<32, 2, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err); break;
-    default:
-      sls_sum_scalar_kernel<<<grid, blk, 0, s>>>(qd, tables, rows, T, L, D, out, ld_out, err);
+    case 8: RS_SLS(2, 1); break;
+    case 16: RS_SLS(4, 1); break;
+    case 32: RS_SLS(8, 1); break;
+    case 64: RS_SLS(16, 1); break;
+    case 128: RS_SLS(32, 1); break;
+    case 256: RS_SLS(32, 2); break;
+    default: {
+      const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
+      sls_sum_scalar_kernel<<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, D, out, ld_out,
+                                                         err);
+    }
   }
+#undef RS_SLS
 }
 
 void launch_gather_concat(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
