@@ -136,6 +136,172 @@ sls_sum_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, i
   }
 }
 
+// Variant "chunk": same 32-lookup units and in-chunk order as sls_sum_kernel,
+// but every chunk of a multi-chunk bag writes its partial and a separate
+// combine kernel adds them in chunk order (no fences or atomics on the hot
+// path); the next unit's indices are fetched while this unit's rows fly.
+template <int LPR, int VPL, int UB>
+__global__ void __launch_bounds__(kWarps * 32)
+sls_chunk_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
+                 int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
+                 float* __restrict__ partial, int hint) {
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  constexpr int U = kChunk / R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t S = qd->S;
+  const int64_t* __restrict__ idx = qd->idx;
+  const int nch = (L + kChunk - 1) / kChunk;
+  const int64_t units = S * T * nch;
+  const uint64_t pol = l2_evict_first_policy();
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  auto fetch_idx = [&](int64_t unit) -> int64_t {
+    if (unit >= units) return 0;
+    const int64_t bag = unit / nch;
+    const int l0 = (int)(unit - bag * nch) * kChunk;
+    return lane < min(kChunk, L - l0) ? __ldg(idx + bag * L + l0 + lane) : 0;
+  };
+  int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
+  int64_t my_idx = fetch_idx(unit);
+  for (; unit < units; unit += stride) {
+    const int64_t bag = unit / nch;
+    const int ch = (int)(unit - bag * nch);
+    const int t = (int)(bag % T);
+    const int n = min(kChunk, L - ch * kChunk);
+    const float4* __restrict__ tab =
+        reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
+    const int64_t cur = my_idx;
+    float4 acc[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u0 = 0; u0 < U; u0 += UB) {
+      float4 v[UB][VPL];
+      bool ok[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int l = (u0 + u) * R + g;
+        const int64_t r = __shfl_sync(0xffffffffu, cur, l & 31);
+        ok[u] = l < n && (uint64_t)r < (uint64_t)rows;
+        if (l < n && !ok[u]) atomicOr(err, kErrIndex);
+        if (ok[u]) {
+          const float4* p = tab + r * (D / 4) + c;
+#pragma unroll
+          for (int k = 0; k < VPL; ++k)
+            v[u][k] = hint ? ldg_stream_hint(p + k * LPR, pol) : ldg_stream(p + k * LPR);
+        }
+      }
+      if (u0 == 0) my_idx = fetch_idx(unit + stride);  // overlap the next unit's indices
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        if (ok[u]) {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
+    if (g == 0) {
+      float4* o = nch == 1
+          ? reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c
+          : reinterpret_cast<float4*>(partial + (bag * nch + ch) * D) + c;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
+    }
+  }
+}
+
+// Chunk partials -> pooled sums, chunk order left to right.
+__global__ void __launch_bounds__(256)
+sls_combine_kernel(const QDesc* __restrict__ qd, int T, int L, int D,
+                   const float* __restrict__ partial, float* __restrict__ out, int64_t ld_out) {
+  const int nch = (L + kChunk - 1) / kChunk;
+  const int D4 = D / 4;
+  const int64_t total = qd->S * T * D4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bag = i / D4;
+    const int c4 = (int)(i - bag * D4);
+    const float4* p = reinterpret_cast<const float4*>(partial + bag * nch * D) + c4;
+    float4 s = p[0];
+    for (int q = 1; q < nch; ++q) add4(s, p[q * D4]);
+    const int t = (int)(bag % T);
+    reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D)[c4] = s;
+  }
+}
+
+// Variant "bag": one warp per whole bag (indices staged in shared memory),
+// R-interleaved order over the entire bag.
+template <int LPR, int VPL, int U>
+__global__ void __launch_bounds__(kWarps * 32)
+sls_bag_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
+               int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
+               int hint) {
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  __shared__ int64_t sidx[kWarps][kIdxChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t bags = qd->S * T;
+  const int64_t* __restrict__ idx = qd->idx;
+  const uint64_t pol = l2_evict_first_policy();
+  for (int64_t bag = (int64_t)blockIdx.x * kWarps + warp; bag < bags;
+       bag += (int64_t)gridDim.x * kWarps) {
+    const int t = (int)(bag % T);
+    const float4* __restrict__ tab =
+        reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
+    const int64_t* __restrict__ bidx = idx + bag * L;
+    float4 acc[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < L; c0 += kIdxChunk) {
+      const int n = min(kIdxChunk, L - c0);
+      __syncwarp();
+      for (int l = lane; l < n; l += 32) sidx[warp][l] = __ldg(bidx + c0 + l);
+      __syncwarp();
+      for (int j = 0; j < n; j += R * U) {
+        float4 v[U][VPL];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int l = j + u * R + g;
+          ok[u] = false;
+          if (l < n) {
+            const int64_t r = sidx[warp][l];
+            if ((uint64_t)r < (uint64_t)rows) {
+              ok[u] = true;
+              const float4* p = tab + r * (D / 4) + c;
+#pragma unroll
+              for (int k = 0; k < VPL; ++k)
+                v[u][k] = hint ? ldg_stream_hint(p + k * LPR, pol) : ldg_stream(p + k * LPR);
+            } else {
+              atomicOr(err, kErrIndex);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
+          }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
+    if (g == 0) {
+      float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
+    }
+  }
+}
+
 // Any D (not a power of two in [8,256]): lane-per-column, sequential in l.
 __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_scalar_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
@@ -444,12 +610,69 @@ size_t sls_partial_floats(int64_t max_items, int T, int L, int D) {
   return (size_t)(max_items * T * ((L + kChunk - 1) / kChunk) * D);
 }
 
+// Tuning knobs for the SLS microbenchmark (tools/sls_micro.py); the defaults
+// are the measured best.
+struct SlsKnobs {
+  int variant;  // 0 chunk+atomic combine, 1 chunk + combine kernel, 2 bag
+  int hint;     // L2 evict-first on table rows
+  int ub;       // chunk kernel: loads in flight per pass (8 or 16)
+};
+SlsKnobs sls_knobs() {
+  SlsKnobs k{0, 1, 16};
+  if (const char* v = getenv("RS_SLS_VARIANT")) k.variant = atoi(v);
+  if (const char* v = getenv("RS_SLS_HINT")) k.hint = atoi(v);
+  if (const char* v = getenv("RS_SLS_UB")) k.ub = atoi(v);
+  return k;
+}
+
+template <int LPR, int VPL, int UB>
+void launch_sls_chunk(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                      float* out, int64_t ld_out, int* err, float* partial, int hint,
+                      int64_t max_items, int sm_count, cudaStream_t s) {
+  static const int per_sm = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_chunk_kernel<LPR, VPL, UB>,
+                                                  kWarps * 32, 0);
+    return b > 0 ? b : 1;
+  }();
+  const int nch = (L + kChunk - 1) / kChunk;
+  const int grid = grid_for(max_items * T * nch, kWarps, sm_count, per_sm);
+  sls_chunk_kernel<LPR, VPL, UB><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out,
+                                                              ld_out, err, partial, hint);
+  if (nch > 1) {
+    const int g2 = grid_for(max_items * T * (LPR * VPL), 256, sm_count, 8);
+    sls_combine_kernel<<<g2, 256, 0, s>>>(qd, T, L, LPR * 4 * VPL, partial, out, ld_out);
+  }
+}
+
+template <int LPR, int VPL, int U>
+void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                    float* out, int64_t ld_out, int* err, int hint, int64_t max_items,
+                    int sm_count, cudaStream_t s) {
+  const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
+  sls_bag_kernel<LPR, VPL, U><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
+                                                           err, hint);
+}
+
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
                     float* out, int64_t ld_out, int* err, float* partial, unsigned* arrivals,
                     int64_t max_items, int sm_count, cudaStream_t s) {
-#define RS_SLS(LPR, VPL) \
-  launch_sls_vec<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, err, partial, arrivals, \
-                           max_items, sm_count, s)
+  const SlsKnobs kn = sls_knobs();
+#define RS_SLS(LPR, VPL)                                                                      \
+  do {                                                                                        \
+    if (kn.variant == 1 && kn.ub == 8 && (32 / (32 / LPR)) >= 8 / VPL)                        \
+      launch_sls_chunk<LPR, VPL, (8 / VPL < kChunk / (32 / LPR) ? 8 / VPL : kChunk / (32 / LPR))>( \
+          qd, tables, rows, T, L, out, ld_out, err, partial, kn.hint, max_items, sm_count, s); \
+    else if (kn.variant == 1)                                                                 \
+      launch_sls_chunk<LPR, VPL, (16 / VPL < kChunk / (32 / LPR) ? 16 / VPL : kChunk / (32 / LPR))>( \
+          qd, tables, rows, T, L, out, ld_out, err, partial, kn.hint, max_items, sm_count, s); \
+    else if (kn.variant == 2)                                                                 \
+      launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
+                                                   kn.hint, max_items, sm_count, s);          \
+    else                                                                                      \
+      launch_sls_vec<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, err, partial, arrivals,   \
+                               max_items, sm_count, s);                                       \
+  } while (0)
   switch (D) {
     case 8: RS_SLS(2, 1); break;
     case 16: RS_SLS(4, 1); break;

@@ -177,7 +177,9 @@ def test_forward_many_matches_single_calls_and_auto_graphs():
         hi[k].view(np.int64, i.shape)[...] = i
     svc = acc.forward_many(sizes, [b.ptr for b in hd], [b.ptr for b in hi], [b.ptr for b in ho],
                            rs.MEM_HOST)
-    assert len(svc) == len(sizes) and (svc > 0).all()
+    # FIFO delivery gaps: non-negative (a query finishing under its
+    # predecessor on another lane is delivered with it), positive in total
+    assert len(svc) == len(sizes) and (svc >= 0).all() and svc.sum() > 0
     for k, S in enumerate(sizes):
         assert np.array_equal(ho[k].view(np.float32, (S, acc.output_dim)), singles[k])
     # device path
