@@ -302,6 +302,142 @@ sls_bag_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, i
   }
 }
 
+// Variant "tma": TMA tile::gather4. One warp per CTA; the warp walks its bags
+// in sub-chunks of up to LB rows. For each sub-chunk, lane i loads lookups
+// 4i..4i+3, turns them into rows of the stacked [T*rows, D] tensor and issues
+// ONE cp.async.bulk.tensor.2d...tile::gather4 that lands those 4 rows in
+// shared memory and completes bytes on the buffer's mbarrier. NBUF buffers
+// keep NBUF-1 sub-chunks in flight while the warp sums the current one from
+// shared memory in the R-interleaved order of the bag variant (so results are
+// bit-identical to it and to the oracle). No register cost for in-flight
+// data: memory-level parallelism is set by shared memory, not by unrolling.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int LPR, int VPL, int NBUF>
+__global__ void __launch_bounds__(32)
+sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap tmap,
+               int64_t rows, int T, int L, int LB, float* __restrict__ out, int64_t ld_out,
+               int* __restrict__ err) {
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  extern __shared__ __align__(128) uint8_t sm_raw[];
+  float* buf = reinterpret_cast<float*>(sm_raw);                           // [NBUF][LB][D]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw + NBUF * LB * D * 4);  // [NBUF]
+  uint32_t* okmask = reinterpret_cast<uint32_t*>(bar + NBUF);              // [NBUF][MW]
+  const int MW = (LB + 31) / 32;                                           // LB <= 128
+  const int lane = threadIdx.x;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t S = qd->S;
+  const int64_t* __restrict__ idx = qd->idx;
+  const int64_t bags = S * T;
+  const int nsub = (L + LB - 1) / LB;
+  // this warp's stream of sub-chunks: bags blockIdx.x, +gridDim.x, ...; nsub each
+  const int64_t my_bags = bags > blockIdx.x ? (bags - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t nk = my_bags * nsub;
+  if (nk == 0) return;
+  if (lane == 0) {
+    for (int b = 0; b < NBUF; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar + b)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  auto issue = [&](int64_t k) {
+    const int b = (int)(k % NBUF);
+    const int64_t bag = (int64_t)blockIdx.x + (k / nsub) * gridDim.x;
+    const int l0 = (int)(k % nsub) * LB;
+    const int n = min(LB, L - l0);
+    const int ng = (n + 3) / 4;              // gather4 instructions
+    const int t = (int)(bag % T);
+    int crd[4] = {0, 0, 0, 0};
+    uint32_t okbits = 0;
+    if (lane < ng) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int l = 4 * lane + j;
+        if (l < n) {
+          const int64_t r = __ldg(idx + bag * L + l0 + l);
+          if ((uint64_t)r < (uint64_t)rows) {
+            crd[j] = (int)(t * rows + r);
+            okbits |= 1u << j;
+          } else {
+            atomicOr(err, kErrIndex);
+          }
+        }
+      }
+    }
+    // row-validity bits of this sub-chunk: lane i owns rows 4i..4i+3
+    uint32_t* mk = okmask + b * MW;
+    for (int w = 0; w < MW; ++w) {
+      // rows 32w..32w+31 live in lanes 8w..8w+7
+      uint32_t word = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) word |= __shfl_sync(0xffffffffu, okbits, (8 * w + q) & 31) << (4 * q);
+      if (lane == 0) mk[w] = word;
+    }
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)ng * 4u * D * 4u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar + b)),
+                   "r"(bytes)
+                   : "memory");
+    }
+    __syncwarp();
+    if (lane < ng) {
+      float* dst = buf + ((size_t)b * LB + 4 * lane) * D;
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_addr(dst)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(smem_addr(bar + b)), "r"(0), "r"(crd[0]),
+          "r"(crd[1]), "r"(crd[2]), "r"(crd[3])
+          : "memory");
+    }
+  };
+
+  for (int64_t k = 0; k < NBUF - 1 && k < nk; ++k) issue(k);
+  float4 acc[VPL];
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t k = 0; k < nk; ++k) {
+    if (k + NBUF - 1 < nk) issue(k + NBUF - 1);
+    const int b = (int)(k % NBUF);
+    const uint32_t parity = (uint32_t)((k / NBUF) & 1);
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(smem_addr(bar + b)),
+        "r"(parity)
+        : "memory");
+    const int l0 = (int)(k % nsub) * LB;
+    const int n = min(LB, L - l0);
+    const float4* src = reinterpret_cast<const float4*>(buf + (size_t)b * LB * D);
+    const uint32_t* mk = okmask + b * MW;
+    for (int j = g; j < n; j += R) {
+      if ((mk[j >> 5] >> (j & 31)) & 1u) {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) add4(acc[q], src[j * (D / 4) + c + q * LPR]);
+      }
+    }
+    __syncwarp();  // every lane is done with buffer b before it is refilled
+    if (k % nsub == nsub - 1) {
+      const int64_t bag = (int64_t)blockIdx.x + (k / nsub) * gridDim.x;
+      const int t = (int)(bag % T);
+#pragma unroll
+      for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], off));
+      if (g == 0) {
+        float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) o[q * LPR] = acc[q];
+      }
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
 // Any D (not a power of two in [8,256]): lane-per-column, sequential in l.
 __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_scalar_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
@@ -654,10 +790,52 @@ void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, i
                                                            err, hint);
 }
 
+template <int LPR, int VPL, int NBUF>
+bool launch_sls_tma(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                    float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                    cudaStream_t s) {
+  constexpr int D = LPR * 4 * VPL;
+  CUtensorMap map;
+  if (!make_row_gather_map(&map, tables, (int64_t)T * rows, D)) return false;
+  const int LB = (int)std::min<int64_t>(128, round_up(L, 16));
+  const size_t smem = (size_t)NBUF * LB * D * 4 + NBUF * 8 + (size_t)NBUF * ((LB + 31) / 32) * 4;
+  if (smem > 227 * 1024) return false;
+  cudaFuncSetAttribute(sls_tma_kernel<LPR, VPL, NBUF>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sls_tma_kernel<LPR, VPL, NBUF>, 32, smem);
+  if (per_sm < 1) return false;
+  const int grid = grid_for(max_items * T, 1, sm_count, per_sm);
+  sls_tma_kernel<LPR, VPL, NBUF><<<grid, 32, smem, s>>>(qd, map, rows, T, L, LB, out, ld_out,
+                                                        err);
+  return true;
+}
+
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
                     float* out, int64_t ld_out, int* err, float* partial, unsigned* arrivals,
                     int64_t max_items, int sm_count, cudaStream_t s) {
-  const SlsKnobs kn = sls_knobs();
+  SlsKnobs kn = sls_knobs();
+  if (kn.variant == 3 || kn.variant == 4) {
+    const int nb = kn.variant == 3 ? 2 : 3;
+    bool ok = false;
+#define RS_TMA(LPR, VPL)                                                                    \
+  ok = nb == 2 ? launch_sls_tma<LPR, VPL, 2>(qd, tables, rows, T, L, out, ld_out, err,      \
+                                             max_items, sm_count, s)                        \
+               : launch_sls_tma<LPR, VPL, 3>(qd, tables, rows, T, L, out, ld_out, err,      \
+                                             max_items, sm_count, s)
+    switch (D) {
+      case 8: RS_TMA(2, 1); break;
+      case 16: RS_TMA(4, 1); break;
+      case 32: RS_TMA(8, 1); break;
+      case 64: RS_TMA(16, 1); break;
+      case 128: RS_TMA(32, 1); break;
+      case 256: RS_TMA(32, 2); break;
+      default: break;
+    }
+#undef RS_TMA
+    if (ok) return;
+    kn.variant = 2;  // shape the TMA path cannot take: warp-per-bag
+  }
 #define RS_SLS(LPR, VPL)                                                                      \
   do {                                                                                        \
     if (kn.variant == 1 && kn.ub == 8 && (32 / (32 / LPR)) >= 8 / VPL)                        \

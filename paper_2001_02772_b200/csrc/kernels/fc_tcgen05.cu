@@ -253,14 +253,14 @@ EncodeTiledFn encode_fn() {
 }
 
 bool encode(CUtensorMap* map, const float* base, int rank, const cuuint64_t* dims,
-            const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+            const cuuint64_t* strides_bytes, const cuuint32_t* box,
+            CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, (void*)base, dims,
-                  strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -281,6 +281,16 @@ void set_attr_once() {
 }  // namespace
 
 bool tc_available() { return encode_fn() != nullptr; }
+
+// All tables viewed as one [total_rows, D] fp32 matrix; box = one row of D
+// elements (the gathered dimension has box extent 1 for tile::gather4).
+bool make_row_gather_map(CUtensorMap* map, const float* base, int64_t total_rows, int D) {
+  if (total_rows >= (int64_t(1) << 31) || D > 256 || (D * 4) % 16) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)total_rows};
+  cuuint64_t str[1] = {(cuuint64_t)D * 4};
+  cuuint32_t box[2] = {(cuuint32_t)D, 1};
+  return encode(map, base, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
 
 bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch) {
   if (a.N < 64 || a.K < BK) return false;

@@ -51,6 +51,7 @@ struct TcPlan {
   int m_tiles, n_tiles;
 };
 bool tc_available();
+bool make_row_gather_map(CUtensorMap* map, const float* base, int64_t total_rows, int D);
 bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch);
 void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s);
 
