@@ -785,7 +785,13 @@ template <int LPR, int VPL, int U>
 void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                     float* out, int64_t ld_out, int* err, int hint, int64_t max_items,
                     int sm_count, cudaStream_t s) {
-  const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
+  // persistent: exactly the resident warp slots, bags strided across them
+  static const int per_sm = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_bag_kernel<LPR, VPL, U>, kWarps * 32, 0);
+    return b > 0 ? b : 1;
+  }();
+  const int grid = grid_for(max_items * T, kWarps, sm_count, per_sm);
   sls_bag_kernel<LPR, VPL, U><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
                                                            err, hint);
 }
@@ -844,6 +850,12 @@ void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, i
     else if (kn.variant == 1)                                                                 \
       launch_sls_chunk<LPR, VPL, (16 / VPL < kChunk / (32 / LPR) ? 16 / VPL : kChunk / (32 / LPR))>( \
           qd, tables, rows, T, L, out, ld_out, err, partial, kn.hint, max_items, sm_count, s); \
+    else if (kn.variant == 2 && kn.ub == 16)                                                  \
+      launch_sls_bag<LPR, VPL, (VPL == 2 ? 8 : 16)>(qd, tables, rows, T, L, out, ld_out, err, \
+                                                    kn.hint, max_items, sm_count, s);         \
+    else if (kn.variant == 2 && kn.ub == 4)                                                   \
+      launch_sls_bag<LPR, VPL, (VPL == 2 ? 2 : 4)>(qd, tables, rows, T, L, out, ld_out, err,  \
+                                                   kn.hint, max_items, sm_count, s);          \
     else if (kn.variant == 2)                                                                 \
       launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
                                                    kn.hint, max_items, sm_count, s);          \
