@@ -239,7 +239,7 @@ template <int LPR, int VPL, int U>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_bag_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
-               int hint) {
+               int hint, unsigned* __restrict__ queue) {
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   __shared__ int64_t sidx[kWarps][kIdxChunk];
@@ -248,8 +248,15 @@ sls_bag_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, i
   const int64_t bags = qd->S * T;
   const int64_t* __restrict__ idx = qd->idx;
   const uint64_t pol = l2_evict_first_policy();
-  for (int64_t bag = (int64_t)blockIdx.x * kWarps + warp; bag < bags;
-       bag += (int64_t)gridDim.x * kWarps) {
+  // Bag order: a device-wide queue (one atomic per bag) when `queue` is set,
+  // so warps that finish early take the remaining bags; else a static stride.
+  auto next = [&](int64_t cur) -> int64_t {
+    if (!queue) return cur < 0 ? (int64_t)blockIdx.x * kWarps + warp : cur + (int64_t)gridDim.x * kWarps;
+    unsigned b = 0;
+    if (lane == 0) b = atomicAdd(queue, 1u);
+    return (int64_t)__shfl_sync(0xffffffffu, b, 0);
+  };
+  for (int64_t bag = next(-1); bag < bags; bag = next(bag)) {
     const int t = (int)(bag % T);
     const float4* __restrict__ tab =
         reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
@@ -783,17 +790,18 @@ void launch_sls_chunk(const QDesc* qd, const float* tables, int64_t rows, int T,
 
 template <int LPR, int VPL, int U>
 void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
-                    float* out, int64_t ld_out, int* err, int hint, int64_t max_items,
-                    int sm_count, cudaStream_t s) {
-  // persistent: exactly the resident warp slots, bags strided across them
+                    float* out, int64_t ld_out, int* err, int hint, unsigned* queue,
+                    int64_t max_items, int sm_count, cudaStream_t s) {
+  // persistent: exactly the resident warp slots; bags from the queue (or strided)
   static const int per_sm = [] {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_bag_kernel<LPR, VPL, U>, kWarps * 32, 0);
     return b > 0 ? b : 1;
   }();
   const int grid = grid_for(max_items * T, kWarps, sm_count, per_sm);
+  if (queue) cudaMemsetAsync(queue, 0, sizeof(unsigned), s);
   sls_bag_kernel<LPR, VPL, U><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
-                                                           err, hint);
+                                                           err, hint, queue);
 }
 
 template <int LPR, int VPL, int NBUF>
@@ -852,13 +860,16 @@ void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, i
           qd, tables, rows, T, L, out, ld_out, err, partial, kn.hint, max_items, sm_count, s); \
     else if (kn.variant == 2 && kn.ub == 16)                                                  \
       launch_sls_bag<LPR, VPL, (VPL == 2 ? 8 : 16)>(qd, tables, rows, T, L, out, ld_out, err, \
-                                                    kn.hint, max_items, sm_count, s);         \
+                                                    kn.hint, nullptr, max_items, sm_count, s); \
     else if (kn.variant == 2 && kn.ub == 4)                                                   \
       launch_sls_bag<LPR, VPL, (VPL == 2 ? 2 : 4)>(qd, tables, rows, T, L, out, ld_out, err,  \
-                                                   kn.hint, max_items, sm_count, s);          \
+                                                   kn.hint, nullptr, max_items, sm_count, s); \
+    else if (kn.variant == 5)                                                                 \
+      launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
+                                                   kn.hint, arrivals, max_items, sm_count, s); \
     else if (kn.variant == 2)                                                                 \
       launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
-                                                   kn.hint, max_items, sm_count, s);          \
+                                                   kn.hint, nullptr, max_items, sm_count, s); \
     else                                                                                      \
       launch_sls_vec<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, err, partial, arrivals,   \
                                max_items, sm_count, s);                                       \
