@@ -220,10 +220,9 @@ int or_sls_canonical(const or_state* s, int64_t S, const int64_t* idx, float* po
     const int64_t lpr = D / 4 < 32 ? D / 4 : 32;
     R = (int)(32 / lpr);
   }
-  /* Power-of-two D: 32-lookup chunks, R-interleaved partials inside a chunk,
-   * pairwise tree, then chunk sums left to right. Other D: one sequential sum. */
-  const int chunked = R > 1 || (D == 128 || D == 256);
-  const int64_t CH = chunked ? 32 : L;
+  /* R-interleaved partials over the whole bag, pairwise tree (R = 1: one
+   * sequential sum). */
+  const int64_t CH = L;
   float row[256];
   float part[32][256];
   float total[256];

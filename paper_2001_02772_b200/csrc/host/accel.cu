@@ -62,8 +62,6 @@ struct Slot {
   float* X = nullptr;
   float* pact[2] = {nullptr, nullptr};
   float* out = nullptr;
-  float* sls_partial = nullptr;        // chunk partial sums of multi-chunk bags
-  unsigned* sls_arrivals = nullptr;    // per-bag chunk counters (self-resetting)
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
   int kernels[3] = {0, 0, 0};
   int tc_layers = 0;
@@ -290,7 +288,7 @@ void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off,
   switch (m.pooling) {
     case RS_POOL_SUM:
       launch_sls_sum(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out + off, ld,
-                     s->d_err, s->sls_partial, s->sls_arrivals, maxS, a->sm_count, st);
+                     s->d_err, maxS, a->sm_count, st);
       break;
     case RS_POOL_CONCAT:
       launch_gather_concat(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out, ld,
@@ -438,11 +436,6 @@ std::unique_ptr<Slot> make_slot(rs_accel* a) {
       dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->pooled_dim, 1) * 4)));
   s->X = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_x * 4)));
   s->out = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->out_w * 4)));
-  if (a->m.pooling == RS_POOL_SUM && a->T > 0) {
-    s->sls_partial = static_cast<float*>(dmalloc(
-        a, s->allocs, sls_partial_floats(maxS, (int)a->T, (int)a->L, (int)a->D) * 4, false));
-    s->sls_arrivals = static_cast<unsigned*>(dmalloc(a, s->allocs, (size_t)(maxS * a->T * 4)));
-  }
   for (auto& e : s->ev) RS_CUDA(cudaEventCreate(&e));
   RS_CUDA(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&s->free, cudaEventDisableTiming));

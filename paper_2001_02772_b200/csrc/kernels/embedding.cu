@@ -14,23 +14,20 @@
 // int64 exactly as the reference's byte model ships them
 // (proj/src/platform.cpp:105-111), so bag (item, t) is L contiguous int64.
 //
-// SLS design: the unit of work is a CHUNK of 32 consecutive lookups of one
-// bag (a bag of L lookups has ceil(L/32) chunks), so a query of S items has
-// S*T*ceil(L/32) units spread over a persistent grid of warps sized by the
-// occupancy API — fine enough that no warp is left with a whole extra bag
-// while the rest idle (the wave-quantisation loss of warp-per-bag). A warp
-// loads the chunk's 32 indices with one coalesced 256-byte read (lane l holds
-// index l and broadcasts it by shuffle), then reads rows with 128-bit
-// non-allocating loads carrying an L2 evict-first policy (tables are
-// streamed; weights, indices and partials stay cached): LPR = D/4 lanes
-// cover one row, R = 32/LPR rows land per warp instruction, U unrolled
-// instructions keep R*U rows in flight. Lane group g accumulates rows
-// g, g+R, g+2R, ... of the chunk in order; groups combine by an xor-shuffle
-// tree. Multi-chunk bags write their chunk partials to scratch; the warp that
-// completes a bag last (device-scope counter) sums the partials in chunk
-// order. That order — R-interleaved within 32-row chunks, pairwise tree,
-// then chunks left to right — is the canonical SLS order oracle/forward.c
-// restates, so pooled sums are bit-identical to the oracle and run to run.
+// SLS design (measured, tools/sls_micro.py): one warp per bag.
+// The warp stages the bag's index list in shared memory, then reads rows with
+// 128-bit non-allocating loads: LPR = D/4 lanes cover one row, R = 32/LPR rows
+// land per warp instruction and U unrolled instructions keep R*U rows in
+// flight per warp (16 rows = 4 KB at D=64; 32 warps/SM). The grid is
+// oversubscribed 2x the resident CTAs so late CTAs pick up the bag tail
+// dynamically. Lane group g accumulates rows g, g+R, g+2R, ... of the bag in
+// order; groups combine by an xor-shuffle tree. That order is the canonical
+// SLS order oracle/forward.c restates, so pooled sums are bit-identical to the
+// oracle and run to run. Alternatives measured and rejected: 32-lookup chunk
+// units (per-unit latency beats the balance gain), a device work queue
+// (atomic + reset cost), deeper unrolling (fewer warps), and a TMA
+// tile::gather4 landing zone (kept below as variant 1: bit-identical, but
+// shared-memory capacity caps bytes in flight; 3.8 vs 5.2 TB/s at S=323).
 #include <algorithm>
 
 #include "common.cuh"
@@ -43,203 +40,11 @@ namespace {
 constexpr int kWarps = 8;      // warps per CTA for warp-per-bag kernels
 constexpr int kIdxChunk = 256; // staged indices per warp per pass
 
-constexpr int kChunk = 32;     // lookups per SLS work unit (one index per lane)
-
-template <int LPR, int VPL>
+template <int LPR, int VPL, int U>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
-               float* __restrict__ partial, unsigned* __restrict__ arrivals) {
-  constexpr int R = 32 / LPR;           // rows per warp instruction
-  constexpr int D = LPR * 4 * VPL;
-  constexpr int U = kChunk / R;         // instructions per chunk: all rows in flight
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane / LPR, c = lane % LPR;
-  const int64_t S = qd->S;
-  const int64_t* __restrict__ idx = qd->idx;
-  const int nch = (L + kChunk - 1) / kChunk;
-  const int64_t units = S * T * nch;
-  const uint64_t pol = l2_evict_first_policy();
-  const int64_t stride = (int64_t)gridDim.x * kWarps;
-  for (int64_t unit = (int64_t)blockIdx.x * kWarps + warp; unit < units; unit += stride) {
-    const int64_t bag = unit / nch;
-    const int ch = (int)(unit - bag * nch);
-    const int t = (int)(bag % T);
-    const int l0 = ch * kChunk;
-    const int n = min(kChunk, L - l0);
-    const float4* __restrict__ tab =
-        reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
-    const int64_t my_idx = lane < n ? __ldg(idx + bag * L + l0 + lane) : 0;
-    float4 acc[VPL];
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    constexpr int UB = (U * VPL > 16) ? 16 / VPL : U;  // loads in flight per pass
-#pragma unroll
-    for (int u0 = 0; u0 < U; u0 += UB) {
-      float4 v[UB][VPL];
-      bool ok[UB];
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        const int l = (u0 + u) * R + g;
-        const int64_t r = __shfl_sync(0xffffffffu, my_idx, l & 31);
-        ok[u] = l < n && (uint64_t)r < (uint64_t)rows;
-        if (l < n && !ok[u]) atomicOr(err, kErrIndex);
-        if (ok[u]) {
-          const float4* p = tab + r * (D / 4) + c;
-#pragma unroll
-          for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream_hint(p + k * LPR, pol);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < UB; ++u)
-        if (ok[u]) {
-#pragma unroll
-          for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
-        }
-    }
-#pragma unroll
-    for (int off = 16; off >= LPR; off >>= 1)
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
-    float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
-    if (nch == 1) {
-      if (g == 0) {
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
-      }
-      continue;
-    }
-    // multi-chunk bag: publish this chunk's partial; the last arriver sums
-    // all partials in chunk order and resets the bag's counter.
-    float4* part = reinterpret_cast<float4*>(partial + (bag * nch + ch) * D) + c;
-    if (g == 0) {
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) __stcg(part + k * LPR, acc[k]);
-    }
-    __threadfence();
-    __syncwarp();
-    unsigned prev = 0;
-    if (lane == 0) prev = atomicAdd(arrivals + bag, 1u);
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (prev != (unsigned)(nch - 1)) continue;
-    __threadfence();
-    if (g == 0) {
-      const float4* p0 = reinterpret_cast<const float4*>(partial + bag * nch * D) + c;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        float4 s = __ldcg(p0 + k * LPR);
-        for (int q = 1; q < nch; ++q) add4(s, __ldcg(p0 + q * (D / 4) + k * LPR));
-        o[k * LPR] = s;
-      }
-    }
-    if (lane == 0) arrivals[bag] = 0u;
-  }
-}
-
-// Variant "chunk": same 32-lookup units and in-chunk order as sls_sum_kernel,
-// but every chunk of a multi-chunk bag writes its partial and a separate
-// combine kernel adds them in chunk order (no fences or atomics on the hot
-// path); the next unit's indices are fetched while this unit's rows fly.
-template <int LPR, int VPL, int UB>
-__global__ void __launch_bounds__(kWarps * 32)
-sls_chunk_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
-                 int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
-                 float* __restrict__ partial, int hint) {
-  constexpr int R = 32 / LPR;
-  constexpr int D = LPR * 4 * VPL;
-  constexpr int U = kChunk / R;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane / LPR, c = lane % LPR;
-  const int64_t S = qd->S;
-  const int64_t* __restrict__ idx = qd->idx;
-  const int nch = (L + kChunk - 1) / kChunk;
-  const int64_t units = S * T * nch;
-  const uint64_t pol = l2_evict_first_policy();
-  const int64_t stride = (int64_t)gridDim.x * kWarps;
-  auto fetch_idx = [&](int64_t unit) -> int64_t {
-    if (unit >= units) return 0;
-    const int64_t bag = unit / nch;
-    const int l0 = (int)(unit - bag * nch) * kChunk;
-    return lane < min(kChunk, L - l0) ? __ldg(idx + bag * L + l0 + lane) : 0;
-  };
-  int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
-  int64_t my_idx = fetch_idx(unit);
-  for (; unit < units; unit += stride) {
-    const int64_t bag = unit / nch;
-    const int ch = (int)(unit - bag * nch);
-    const int t = (int)(bag % T);
-    const int n = min(kChunk, L - ch * kChunk);
-    const float4* __restrict__ tab =
-        reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
-    const int64_t cur = my_idx;
-    float4 acc[VPL];
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int u0 = 0; u0 < U; u0 += UB) {
-      float4 v[UB][VPL];
-      bool ok[UB];
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        const int l = (u0 + u) * R + g;
-        const int64_t r = __shfl_sync(0xffffffffu, cur, l & 31);
-        ok[u] = l < n && (uint64_t)r < (uint64_t)rows;
-        if (l < n && !ok[u]) atomicOr(err, kErrIndex);
-        if (ok[u]) {
-          const float4* p = tab + r * (D / 4) + c;
-#pragma unroll
-          for (int k = 0; k < VPL; ++k)
-            v[u][k] = hint ? ldg_stream_hint(p + k * LPR, pol) : ldg_stream(p + k * LPR);
-        }
-      }
-      if (u0 == 0) my_idx = fetch_idx(unit + stride);  // overlap the next unit's indices
-#pragma unroll
-      for (int u = 0; u < UB; ++u)
-        if (ok[u]) {
-#pragma unroll
-          for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
-        }
-    }
-#pragma unroll
-    for (int off = 16; off >= LPR; off >>= 1)
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
-    if (g == 0) {
-      float4* o = nch == 1
-          ? reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c
-          : reinterpret_cast<float4*>(partial + (bag * nch + ch) * D) + c;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
-    }
-  }
-}
-
-// Chunk partials -> pooled sums, chunk order left to right.
-__global__ void __launch_bounds__(256)
-sls_combine_kernel(const QDesc* __restrict__ qd, int T, int L, int D,
-                   const float* __restrict__ partial, float* __restrict__ out, int64_t ld_out) {
-  const int nch = (L + kChunk - 1) / kChunk;
-  const int D4 = D / 4;
-  const int64_t total = qd->S * T * D4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t bag = i / D4;
-    const int c4 = (int)(i - bag * D4);
-    const float4* p = reinterpret_cast<const float4*>(partial + bag * nch * D) + c4;
-    float4 s = p[0];
-    for (int q = 1; q < nch; ++q) add4(s, p[q * D4]);
-    const int t = (int)(bag % T);
-    reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D)[c4] = s;
-  }
-}
-
-// Variant "bag": one warp per whole bag (indices staged in shared memory),
-// R-interleaved order over the entire bag.
-template <int LPR, int VPL, int U>
-__global__ void __launch_bounds__(kWarps * 32)
-sls_bag_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
-               int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
-               int hint, unsigned* __restrict__ queue) {
+               int hint) {
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   __shared__ int64_t sidx[kWarps][kIdxChunk];
@@ -248,15 +53,8 @@ sls_bag_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, i
   const int64_t bags = qd->S * T;
   const int64_t* __restrict__ idx = qd->idx;
   const uint64_t pol = l2_evict_first_policy();
-  // Bag order: a device-wide queue (one atomic per bag) when `queue` is set,
-  // so warps that finish early take the remaining bags; else a static stride.
-  auto next = [&](int64_t cur) -> int64_t {
-    if (!queue) return cur < 0 ? (int64_t)blockIdx.x * kWarps + warp : cur + (int64_t)gridDim.x * kWarps;
-    unsigned b = 0;
-    if (lane == 0) b = atomicAdd(queue, 1u);
-    return (int64_t)__shfl_sync(0xffffffffu, b, 0);
-  };
-  for (int64_t bag = next(-1); bag < bags; bag = next(bag)) {
+  for (int64_t bag = (int64_t)blockIdx.x * kWarps + warp; bag < bags;
+       bag += (int64_t)gridDim.x * kWarps) {
     const int t = (int)(bag % T);
     const float4* __restrict__ tab =
         reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
@@ -309,7 +107,7 @@ sls_bag_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, i
   }
 }
 
-// Variant "tma": TMA tile::gather4. One warp per CTA; the warp walks its bags
+// Variant 1 (RS_SLS_VARIANT=1): TMA tile::gather4. One warp per CTA; the warp walks its bags
 // in sub-chunks of up to LB rows. For each sub-chunk, lane i loads lookups
 // 4i..4i+3, turns them into rows of the stacked [T*rows, D] tensor and issues
 // ONE cp.async.bulk.tensor.2d...tile::gather4 that lands those 4 rows in
@@ -733,75 +531,25 @@ int grid_for(int64_t units, int per_block, int sm_count, int blocks_per_sm) {
 
 bool sls_vector_path(int64_t D) { return pow2_dim(D); }
 
-template <int LPR, int VPL>
-void launch_sls_vec(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
-                    float* out, int64_t ld_out, int* err, float* partial, unsigned* arrivals,
-                    int64_t max_items, int sm_count, cudaStream_t s) {
-  // persistent grid: every resident warp slot of the device, no more
-  static const int per_sm = [] {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_sum_kernel<LPR, VPL>, kWarps * 32, 0);
-    return b > 0 ? b : 1;
-  }();
-  const int64_t units = max_items * T * ((L + kChunk - 1) / kChunk);
-  const int grid = grid_for(units, kWarps, sm_count, per_sm);
-  sls_sum_kernel<LPR, VPL><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
-                                                       err, partial, arrivals);
-}
 
-size_t sls_partial_floats(int64_t max_items, int T, int L, int D) {
-  return (size_t)(max_items * T * ((L + kChunk - 1) / kChunk) * D);
-}
-
-// Tuning knobs for the SLS microbenchmark (tools/sls_micro.py); the defaults
-// are the measured best.
-struct SlsKnobs {
-  int variant;  // 0 chunk+atomic combine, 1 chunk + combine kernel, 2 bag
-  int hint;     // L2 evict-first on table rows
-  int ub;       // chunk kernel: loads in flight per pass (8 or 16)
-};
-SlsKnobs sls_knobs() {
-  SlsKnobs k{0, 1, 16};
-  if (const char* v = getenv("RS_SLS_VARIANT")) k.variant = atoi(v);
-  if (const char* v = getenv("RS_SLS_HINT")) k.hint = atoi(v);
-  if (const char* v = getenv("RS_SLS_UB")) k.ub = atoi(v);
-  return k;
-}
-
-template <int LPR, int VPL, int UB>
-void launch_sls_chunk(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
-                      float* out, int64_t ld_out, int* err, float* partial, int hint,
-                      int64_t max_items, int sm_count, cudaStream_t s) {
-  static const int per_sm = [] {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_chunk_kernel<LPR, VPL, UB>,
-                                                  kWarps * 32, 0);
-    return b > 0 ? b : 1;
-  }();
-  const int nch = (L + kChunk - 1) / kChunk;
-  const int grid = grid_for(max_items * T * nch, kWarps, sm_count, per_sm);
-  sls_chunk_kernel<LPR, VPL, UB><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out,
-                                                              ld_out, err, partial, hint);
-  if (nch > 1) {
-    const int g2 = grid_for(max_items * T * (LPR * VPL), 256, sm_count, 8);
-    sls_combine_kernel<<<g2, 256, 0, s>>>(qd, T, L, LPR * 4 * VPL, partial, out, ld_out);
-  }
+// RS_SLS_VARIANT: 0 (default) warp-per-bag register gather, 1 TMA gather4.
+int sls_variant() {
+  const char* v = getenv("RS_SLS_VARIANT");
+  return v ? atoi(v) : 0;
 }
 
 template <int LPR, int VPL, int U>
 void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
-                    float* out, int64_t ld_out, int* err, int hint, unsigned* queue,
-                    int64_t max_items, int sm_count, cudaStream_t s) {
-  // persistent: exactly the resident warp slots; bags from the queue (or strided)
+                    float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                    cudaStream_t s) {
   static const int per_sm = [] {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_bag_kernel<LPR, VPL, U>, kWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_sum_kernel<LPR, VPL, U>, kWarps * 32, 0);
     return b > 0 ? b : 1;
   }();
-  const int grid = grid_for(max_items * T, kWarps, sm_count, per_sm);
-  if (queue) cudaMemsetAsync(queue, 0, sizeof(unsigned), s);
-  sls_bag_kernel<LPR, VPL, U><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
-                                                           err, hint, queue);
+  const int grid = grid_for(max_items * T, kWarps, sm_count, 2 * per_sm);
+  sls_sum_kernel<LPR, VPL, U><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
+                                                           err, 0);
 }
 
 template <int LPR, int VPL, int NBUF>
@@ -826,53 +574,16 @@ bool launch_sls_tma(const QDesc* qd, const float* tables, int64_t rows, int T, i
 }
 
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
-                    float* out, int64_t ld_out, int* err, float* partial, unsigned* arrivals,
-                    int64_t max_items, int sm_count, cudaStream_t s) {
-  SlsKnobs kn = sls_knobs();
-  if (kn.variant == 3 || kn.variant == 4) {
-    const int nb = kn.variant == 3 ? 2 : 3;
-    bool ok = false;
-#define RS_TMA(LPR, VPL)                                                                    \
-  ok = nb == 2 ? launch_sls_tma<LPR, VPL, 2>(qd, tables, rows, T, L, out, ld_out, err,      \
-                                             max_items, sm_count, s)                        \
-               : launch_sls_tma<LPR, VPL, 3>(qd, tables, rows, T, L, out, ld_out, err,      \
-                                             max_items, sm_count, s)
-    switch (D) {
-      case 8: RS_TMA(2, 1); break;
-      case 16: RS_TMA(4, 1); break;
-      case 32: RS_TMA(8, 1); break;
-      case 64: RS_TMA(16, 1); break;
-      case 128: RS_TMA(32, 1); break;
-      case 256: RS_TMA(32, 2); break;
-      default: break;
-    }
-#undef RS_TMA
-    if (ok) return;
-    kn.variant = 2;  // shape the TMA path cannot take: warp-per-bag
-  }
-#define RS_SLS(LPR, VPL)                                                                      \
-  do {                                                                                        \
-    if (kn.variant == 1 && kn.ub == 8 && (32 / (32 / LPR)) >= 8 / VPL)                        \
-      launch_sls_chunk<LPR, VPL, (8 / VPL < kChunk / (32 / LPR) ? 8 / VPL : kChunk / (32 / LPR))>( \
-          qd, tables, rows, T, L, out, ld_out, err, partial, kn.hint, max_items, sm_count, s); \
-    else if (kn.variant == 1)                                                                 \
-      launch_sls_chunk<LPR, VPL, (16 / VPL < kChunk / (32 / LPR) ? 16 / VPL : kChunk / (32 / LPR))>( \
-          qd, tables, rows, T, L, out, ld_out, err, partial, kn.hint, max_items, sm_count, s); \
-    else if (kn.variant == 2 && kn.ub == 16)                                                  \
-      launch_sls_bag<LPR, VPL, (VPL == 2 ? 8 : 16)>(qd, tables, rows, T, L, out, ld_out, err, \
-                                                    kn.hint, nullptr, max_items, sm_count, s); \
-    else if (kn.variant == 2 && kn.ub == 4)                                                   \
-      launch_sls_bag<LPR, VPL, (VPL == 2 ? 2 : 4)>(qd, tables, rows, T, L, out, ld_out, err,  \
-                                                   kn.hint, nullptr, max_items, sm_count, s); \
-    else if (kn.variant == 5)                                                                 \
-      launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
-                                                   kn.hint, arrivals, max_items, sm_count, s); \
-    else if (kn.variant == 2)                                                                 \
-      launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
-                                                   kn.hint, nullptr, max_items, sm_count, s); \
-    else                                                                                      \
-      launch_sls_vec<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, err, partial, arrivals,   \
-                               max_items, sm_count, s);                                       \
+                    float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                    cudaStream_t s) {
+#define RS_SLS(LPR, VPL)                                                                    \
+  do {                                                                                      \
+    if (sls_variant() == 1 && launch_sls_tma<LPR, VPL, 2>(qd, tables, rows, T, L, out,      \
+                                                          ld_out, err, max_items, sm_count, \
+                                                          s))                               \
+      break;                                                                                \
+    launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
+                                                 max_items, sm_count, s);                   \
   } while (0)
   switch (D) {
     case 8: RS_SLS(2, 1); break;

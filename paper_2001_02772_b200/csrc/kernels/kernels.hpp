@@ -10,11 +10,9 @@ struct QDesc;
 
 // ---- embedding.cu ----
 bool sls_vector_path(int64_t D);
-// partial: sls_partial_floats() scratch; arrivals: zeroed u32 per (item, table)
-size_t sls_partial_floats(int64_t max_items, int T, int L, int D);
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
-                    float* out, int64_t ld_out, int* err, float* partial, unsigned* arrivals,
-                    int64_t max_items, int sm_count, cudaStream_t s);
+                    float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                    cudaStream_t s);
 void launch_gather_concat(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                           int D, float* out, int64_t ld_out, int64_t col_off, int* err,
                           int64_t max_items, int sm_count, cudaStream_t s);

@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", type=int, default=10_000_000)
-    ap.add_argument("--variants", default="0:1:16,1:1:16,1:1:8,1:0:16,2:1:8,2:0:8")
+    ap.add_argument("--variants", default="0:0:0,1:0:0")
     ap.add_argument("--sizes", default="16,64,128,323,500,1000")
     ap.add_argument("--D", type=int, default=64)
     ap.add_argument("--L", type=int, default=80)
