@@ -267,7 +267,8 @@ def run_ours(args, rank, world, local):
                             2 * Q)
     sizes = np.minimum(sizes, args.max_query)
     acc = rs.Accelerator(spec, rows, seed=1, device=local, max_query_size=args.max_query,
-                         fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc])
+                         fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc],
+                         queue_depth=args.depth)
     e = spec.embeddings
     # pool of 2Q distinct queries: pinned host copies (e2e) and device copies (value)
     P = 2 * Q
@@ -410,6 +411,7 @@ def main():
     ap.add_argument("--max-query", type=int, default=1000)
     ap.add_argument("--fc", choices=["fp32", "tf32", "auto"], default="auto")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--depth", type=int, default=2, help="queries in flight per GPU (lanes)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
