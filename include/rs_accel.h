@@ -149,7 +149,10 @@ int rs_gen_trace(uint64_t seed, double lambda, const rs_size_dist* dist,
  * `service_s[i]` is the service time of query i of the *base* trace; each
  * evaluation re-times the same size sequence with Poisson gaps at the new
  * rate (seed base_seed + eval index, as sim.cpp:253). `servers` FIFO
- * replicas; dispatch = least outstanding work, ties to lowest index.        */
+ * replicas; dispatch = least outstanding work, ties to lowest index.
+ * `extra_s` (may be NULL): per-query time a query spends in a pipelined
+ * accelerator beyond its service gap (residence - service, clamped at 0);
+ * it is added to that query's latency so pipelining never hides latency.   */
 typedef struct rs_qps_result {
   double qps;        /* achieved QPS of the accepted evaluation            */
   double at_lambda;  /* offered rate that met the SLA (0 if none)           */
@@ -157,9 +160,9 @@ typedef struct rs_qps_result {
   double p50;
   int32_t evaluations;
 } rs_qps_result;
-int rs_qps_under_sla(const double* service_s, int64_t n, int32_t servers,
-                     double sla_s, double warmup_fraction, uint64_t base_seed,
-                     double lambda_hi, rs_qps_result* out);
+int rs_qps_under_sla(const double* service_s, const double* extra_s, int64_t n,
+                     int32_t servers, double sla_s, double warmup_fraction,
+                     uint64_t base_seed, double lambda_hi, rs_qps_result* out);
 
 /* ---- the accelerator (B200) --------------------------------------------- */
 typedef struct rs_accel rs_accel;
@@ -181,7 +184,7 @@ typedef struct rs_init_desc {
   int32_t fc_mode;          /* RS_FC_*                                       */
   int32_t rnn_cell;         /* RS_RNN_* (AttentionRNN only)                  */
   int32_t l2_persist_mb;    /* >0: L2 persisting window over table rows     */
-  int32_t queue_depth;      /* rs_forward_many lanes in flight (0 = 2, <= 4) */
+  int32_t queue_depth;      /* rs_forward_many lanes in flight (0 = 4, <= 8) */
 } rs_init_desc;
 
 /* One query: S items. dense f32[S * dense_input_dim] and indices
@@ -241,17 +244,22 @@ int rs_accel_info_get(const rs_accel* a, rs_accel_info* out);
 int rs_forward(rs_accel* a, const rs_query* q, float* out, void* stream,
                rs_timing* timing);
 
-/* Serve n whole queries back to back on `stream`, in order — the FIFO
- * accelerator server of simulate() (proj/src/sim.cpp:126-136), one query at
- * a time. outs[i] receives query i's logits. Host-resident queries go
- * through a two-slot queue: query i+1's H2D runs on an internal copy stream
- * while query i computes. When service_ms is non-NULL the call records an
- * event after every query, waits, and returns per-query service times
- * (ms, completion-to-completion, the first from the call's start) and any
- * sticky error. All queries must share one memory location. Concurrent
- * rs_forward_many calls on one handle are serialised.                       */
+/* Serve n whole queries on `stream` — the FIFO accelerator server of
+ * simulate() (proj/src/sim.cpp:126-136), made a pipeline: queries are
+ * dispatched in arrival order round-robin over `queue_depth` lanes (each a
+ * compute stream with its own scratch slot), so query i+1's embedding gather
+ * overlaps query i's latency-bound FC tail; results are delivered in FIFO
+ * order. outs[i] receives query i's logits. Host-resident queries are staged
+ * by an internal copy stream that runs ahead of compute. When service_ms is
+ * non-NULL the call waits and returns per-query service times: gaps between
+ * FIFO deliveries (ms; the first from the call's start). latency_ms
+ * (optional, needs service_ms) returns each query's residence in the
+ * accelerator: input staging start to completion. All queries must share
+ * one memory location. Concurrent rs_forward_many calls on one handle are
+ * serialised.                                                               */
 int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
-                    float* const* outs, void* stream, double* service_ms);
+                    float* const* outs, void* stream, double* service_ms,
+                    double* latency_ms);
 
 /* Wait for `stream` and report (then clear) errors that asynchronous calls
  * left in the handle's sticky error words (e.g. RS_E_INDEX).               */

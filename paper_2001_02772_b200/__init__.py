@@ -173,15 +173,15 @@ _sig("rs_route", C.c_int, C.c_int64, C.c_int64, C.c_int64, P(C.c_int32), P(C.c_i
 _sig("rs_dist_production", C.c_int, P(CSizeDist))
 _sig("rs_gen_trace", C.c_int, C.c_uint64, C.c_double, P(CSizeDist), C.c_int64,
      P(C.c_double), P(C.c_int64))
-_sig("rs_qps_under_sla", C.c_int, P(C.c_double), C.c_int64, C.c_int32, C.c_double,
-     C.c_double, C.c_uint64, C.c_double, P(CQpsResult))
+_sig("rs_qps_under_sla", C.c_int, P(C.c_double), P(C.c_double), C.c_int64, C.c_int32,
+     C.c_double, C.c_double, C.c_uint64, C.c_double, P(CQpsResult))
 _sig("rs_accel_create", C.c_int, P(CModelDesc), P(CInitDesc), C.c_int, P(C.c_void_p))
 _sig("rs_accel_destroy", C.c_int, C.c_void_p)
 _sig("rs_accel_info_get", C.c_int, C.c_void_p, P(CAccelInfo))
 _sig("rs_forward", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_void_p, P(CTiming))
 _sig("rs_pooled", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_void_p, P(CTiming))
 _sig("rs_forward_many", C.c_int, C.c_void_p, C.c_int64, P(CQuery), P(C.c_void_p), C.c_void_p,
-     P(C.c_double))
+     P(C.c_double), P(C.c_double))
 _sig("rs_sync", C.c_int, C.c_void_p, C.c_void_p)
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
@@ -407,12 +407,19 @@ class QpsResult:
 
 def qps_under_sla(service_s: Sequence[float], sla: float, servers: int = 1,
                   warmup_fraction: float = 0.1, base_seed: int = 42,
-                  lambda_hi: float = 0.0) -> QpsResult:
-    """max_qps_under_sla (sim.cpp:246-290) over measured per-query service times."""
+                  lambda_hi: float = 0.0, extra_s: Optional[Sequence[float]] = None
+                  ) -> QpsResult:
+    """max_qps_under_sla (sim.cpp:246-290) over measured per-query service times;
+    extra_s adds each query's in-pipeline residence beyond its service gap."""
     s = np.ascontiguousarray(service_s, dtype=np.float64)
+    x = None if extra_s is None else np.ascontiguousarray(extra_s, dtype=np.float64)
+    if x is not None and len(x) != len(s):
+        raise InvalidArgument("extra_s length differs from service_s")
     r = CQpsResult()
-    _check(_lib.rs_qps_under_sla(s.ctypes.data_as(P(C.c_double)), len(s), servers, sla,
-                                 warmup_fraction, base_seed, lambda_hi, C.byref(r)))
+    _check(_lib.rs_qps_under_sla(s.ctypes.data_as(P(C.c_double)),
+                                 x.ctypes.data_as(P(C.c_double)) if x is not None else None,
+                                 len(s), servers, sla, warmup_fraction, base_seed, lambda_hi,
+                                 C.byref(r)))
     return QpsResult(r.qps, r.at_lambda, r.p95, r.p50, r.evaluations)
 
 
@@ -447,7 +454,7 @@ class Accelerator:
 
     def __init__(self, model: ModelSpec, rows_per_table: int, seed: int = 1,
                  device: int = 0, max_query_size: int = 1000, fc_mode: int = FC_FP32,
-                 rnn_cell: int = RNN_GRU, queue_depth: int = 2):
+                 rnn_cell: int = RNN_GRU, queue_depth: int = 4):
         self.model = model
         self.rows = rows_per_table
         self.seed = seed
@@ -494,18 +501,22 @@ class Accelerator:
         return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms) if timed else None
 
     def forward_many(self, sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int,
-                     stream: int = 0, timed: bool = True):
-        """rs_forward_many: n whole queries back to back (FIFO) on one stream.
-        Returns per-query service times in ms when timed (else None)."""
+                     stream: int = 0, timed: bool = True, residence: bool = False):
+        """rs_forward_many: n whole queries, FIFO-dispatched over the handle's
+        lanes. Returns per-query service times in ms when timed (else None);
+        with residence=True returns (service_ms, residence_ms)."""
         n = len(sizes)
         qs = (CQuery * n)()
         for i in range(n):
             qs[i] = CQuery(int(sizes[i]), dense_ptrs[i] or None, idx_ptrs[i] or None, location, 0)
         outs = (C.c_void_p * n)(*[C.c_void_p(p) for p in out_ptrs])
         svc = np.zeros(n, dtype=np.float64) if timed else None
+        lat = np.zeros(n, dtype=np.float64) if (timed and residence) else None
         _check(_lib.rs_forward_many(self._h, n, qs, outs, stream or None,
-                                    svc.ctypes.data_as(P(C.c_double)) if timed else None))
-        return svc
+                                    svc.ctypes.data_as(P(C.c_double)) if timed else None,
+                                    lat.ctypes.data_as(P(C.c_double)) if lat is not None
+                                    else None))
+        return (svc, lat) if residence else svc
 
     def sync(self, stream: int = 0) -> None:
         """rs_sync: wait for `stream`, raise any sticky error (e.g. bad index)."""

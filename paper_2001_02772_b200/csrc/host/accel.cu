@@ -99,15 +99,15 @@ struct rs_accel {
   std::mutex mu;
   std::map<cudaStream_t, std::unique_ptr<rs::Slot>> slots;
   // rs_forward_many queue: `depth` lanes, each a compute stream + a slot
-  static constexpr int kMaxLanes = 4;
+  static constexpr int kMaxLanes = 8;
   int depth = 2;
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
-  cudaStream_t lane[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
-  cudaEvent_t lane_join[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t lane[kMaxLanes] = {};
+  cudaEvent_t lane_join[kMaxLanes] = {};
   cudaStream_t copy = nullptr;
   cudaEvent_t copy_gate = nullptr;
   std::mutex many_mu;
-  std::vector<cudaEvent_t> evpool;
+  std::vector<cudaEvent_t> evpool, evstart;
   std::map<int64_t, double> service_memo;
 };
 
@@ -602,7 +602,7 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
 }
 
 int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, void* stream,
-             double* service_ms) {
+             double* service_ms, double* latency_ms) {
   return guarded([&] {
     if (!a || !qs || !outs) raise(RS_E_INVALID, "null argument");
     if (n < 1) raise(RS_E_INVALID, "n < 1");
@@ -615,11 +615,17 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     RS_CUDA(cudaSetDevice(a->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->own;
     std::lock_guard<std::mutex> many_lock(a->many_mu);
+    if (latency_ms && !service_ms) raise(RS_E_INVALID, "latency_ms needs service_ms");
     if (service_ms) {
       while ((int64_t)a->evpool.size() < n + 1) {
         cudaEvent_t e;
         RS_CUDA(cudaEventCreate(&e));
         a->evpool.push_back(e);
+      }
+      while (latency_ms && (int64_t)a->evstart.size() < n) {
+        cudaEvent_t e;
+        RS_CUDA(cudaEventCreate(&e));
+        a->evstart.push_back(e);
       }
       RS_CUDA(cudaEventRecord(a->evpool[0], st));
     }
@@ -640,10 +646,12 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
       cudaStream_t ls = a->lane[d];
       if (loc == RS_MEM_HOST) {
         RS_CUDA(cudaStreamWaitEvent(a->copy, s->free, 0));
+        if (latency_ms) RS_CUDA(cudaEventRecord(a->evstart[i], a->copy));
         stage_inputs(a, s, &qs[i], true, a->copy);
         RS_CUDA(cudaEventRecord(s->ready, a->copy));
         RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
       } else {
+        if (latency_ms) RS_CUDA(cudaEventRecord(a->evstart[i], ls));
         stage_inputs(a, s, &qs[i], true, ls);
       }
       launch_stage(a, s, &qs[i], outs[i], true, ls);
@@ -663,6 +671,8 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
         const double done = std::max(prev, (double)elapsed(a->evpool[0], a->evpool[i + 1]));
         service_ms[i] = done - prev;
         prev = done;
+        // residence in the accelerator: input staging start -> completion
+        if (latency_ms) latency_ms[i] = elapsed(a->evstart[i], a->evpool[i + 1]);
       }
       for (int d = 0; d < depth; ++d) collect_errors(p[d], st);
     }
@@ -719,7 +729,7 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     a = new rs_accel();
     a->m = *model;
     a->init = *init;
-    a->depth = init->queue_depth > 0 ? std::min<int>(init->queue_depth, rs_accel::kMaxLanes) : 2;
+    a->depth = init->queue_depth > 0 ? std::min<int>(init->queue_depth, rs_accel::kMaxLanes) : 4;
     a->device = device;
     a->sm_count = prop.multiProcessorCount;
     a->l2_bytes = prop.l2CacheSize;
@@ -746,6 +756,7 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
     for (auto& p : a->pipe)
       if (p) free_slot(p.get());
     for (auto e : a->evpool) cudaEventDestroy(e);
+    for (auto e : a->evstart) cudaEventDestroy(e);
     if (a->copy_gate) cudaEventDestroy(a->copy_gate);
     if (a->copy) cudaStreamDestroy(a->copy);
     for (int d = 0; d < rs_accel::kMaxLanes; ++d) {
@@ -785,8 +796,9 @@ extern "C" int rs_forward(rs_accel* a, const rs_query* q, float* out, void* stre
 }
 
 extern "C" int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
-                               float* const* outs, void* stream, double* service_ms) {
-  return run_many(a, n, queries, outs, stream, service_ms);
+                               float* const* outs, void* stream, double* service_ms,
+                               double* latency_ms) {
+  return run_many(a, n, queries, outs, stream, service_ms, latency_ms);
 }
 
 extern "C" int rs_sync(rs_accel* a, void* stream) {

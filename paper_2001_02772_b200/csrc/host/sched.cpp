@@ -94,8 +94,8 @@ struct QpsEval {
 
 // One open-loop replay of the measured stream at rate `lambda` over
 // `servers` FIFO replicas (least outstanding work, ties to lowest index).
-QpsEval replay(const double* service, int64_t n, int servers, double lambda,
-               uint64_t seed, double warmup_fraction, double sla) {
+QpsEval replay(const double* service, const double* extra, int64_t n, int servers,
+               double lambda, uint64_t seed, double warmup_fraction, double sla) {
   Stream gaps(seed);
   std::vector<double> free_at(static_cast<size_t>(servers), 0.0);
   const int64_t warm = static_cast<int64_t>(std::floor(warmup_fraction * static_cast<double>(n)));
@@ -115,7 +115,7 @@ QpsEval replay(const double* service, int64_t n, int servers, double lambda,
     free_at[static_cast<size_t>(best)] = done;
     last_done = std::max(last_done, done);
     if (i == warm) first_pw_arrival = now;
-    if (i >= warm) lat.push_back(done - now);
+    if (i >= warm) lat.push_back(done - now + (extra ? std::max(0.0, extra[i]) : 0.0));
   }
   QpsEval e{};
   if (lat.empty()) raise(RS_E_EMPTY, "no post-warmup queries");
@@ -187,9 +187,9 @@ extern "C" int rs_gen_trace(uint64_t seed, double lambda, const rs_size_dist* di
   });
 }
 
-extern "C" int rs_qps_under_sla(const double* service_s, int64_t n, int32_t servers,
-                                double sla_s, double warmup_fraction, uint64_t base_seed,
-                                double lambda_hi, rs_qps_result* out) {
+extern "C" int rs_qps_under_sla(const double* service_s, const double* extra_s, int64_t n,
+                                int32_t servers, double sla_s, double warmup_fraction,
+                                uint64_t base_seed, double lambda_hi, rs_qps_result* out) {
   return guarded([&] {
     if (!service_s || !out) raise(RS_E_INVALID, "null argument");
     if (n < 1) raise(RS_E_INVALID, "n < 1");
@@ -206,7 +206,8 @@ extern "C" int rs_qps_under_sla(const double* service_s, int64_t n, int32_t serv
     int evals = 0;
     auto eval = [&](double lam) {
       ++evals;
-      return replay(service_s, n, servers, lam, base_seed + idx++, warmup_fraction, sla_s);
+      return replay(service_s, extra_s, n, servers, lam, base_seed + idx++, warmup_fraction,
+                    sla_s);
     };
     double lo = 1.0;
     QpsEval lo_e = eval(lo);
