@@ -292,8 +292,8 @@ def run_ours(args, rank, world, local):
         base = (k % 2) * Q
         return range(base, base + Q)
 
-    def serve(n_steps, host, timed):
-        """One rs_forward_many call over n_steps windows: FIFO, one stream."""
+    def prepare(n_steps, host):
+        """rs_forward_many arguments for n_steps windows (built before timing)."""
         qs = [q for k in range(n_steps) for q in window(k)]
         if host:
             dp = [h_dense[q].ptr for q in qs]
@@ -305,11 +305,14 @@ def run_ours(args, rank, world, local):
             ip = [d_idx[q].data_ptr() for q in qs]
             op = [out_dev.data_ptr()] * len(qs)
             loc = rs.MEM_DEVICE
-        return acc.forward_many([int(sizes[q]) for q in qs], dp, ip, op, loc, stream=sp,
-                                timed=timed, residence=True)
+        return acc.batch([int(sizes[q]) for q in qs], dp, ip, op, loc)
+
+    def serve(batch):
+        return acc.forward_many(None, stream=sp, timed=True, residence=True, prepared=batch)
 
     def timed(host):
-        serve(W, host, timed=True)               # warm-up (untimed), synchronous
+        serve(prepare(W, host))                  # warm-up (untimed), synchronous
+        batch = prepare(K, host)
         torch.cuda.synchronize(device)
         barrier(device)
         torch.cuda.synchronize(device)
@@ -317,7 +320,7 @@ def run_ours(args, rank, world, local):
         end = torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as clk:
             start.record(stream)
-            svc_ms, res_ms = serve(K, host, timed=True)  # per-query CUDA-event times
+            svc_ms, res_ms = serve(batch)        # per-query CUDA-event times
             end.record(stream)
             torch.cuda.synchronize(device)
         barrier(device)
@@ -328,15 +331,22 @@ def run_ours(args, rank, world, local):
         extra = np.maximum(res_ms - svc_ms, 0.0) * 1e-3
         return total_s, svc_ms * 1e-3, extra, clk.summary()
 
+    def sla_qps(svc, extra):
+        # the reference evaluates traces of n = 50,000 queries
+        # (proj/include/recsim/sim.hpp:79): the measured per-query service
+        # times are cycled to that length, so an overloaded rate cannot hide
+        # behind a short trace
+        n = 50_000
+        return rs.qps_under_sla(np.resize(svc, n), sla, servers=1, warmup_fraction=0.1,
+                                base_seed=seed, extra_s=np.resize(extra, n))
+
     # ---- value: device-resident inputs
     t_dev, svc_dev, extra_dev, clocks = timed(host=False)
-    r_dev = rs.qps_under_sla(svc_dev, sla, servers=1, warmup_fraction=0.1, base_seed=seed,
-                             extra_s=extra_dev)
+    r_dev = sla_qps(svc_dev, extra_dev)
     agg = aggregate(r_dev.qps, t_dev, len(svc_dev), world, device)
     # ---- e2e: host pinned inputs, H2D/D2H inside every query
     t_host, svc_host, extra_host, clocks_e2e = timed(host=True)
-    r_host = rs.qps_under_sla(svc_host, sla, servers=1, warmup_fraction=0.1, base_seed=seed,
-                              extra_s=extra_host)
+    r_host = sla_qps(svc_host, extra_host)
     agg_e2e = aggregate(r_host.qps, t_host, len(svc_host), world, device)
 
     # ---- roofline of the dominant kernel (SLS), live CUDA-event timing on the
@@ -376,9 +386,11 @@ def run_ours(args, rank, world, local):
                        "fc_path": args.fc, "parallelism": f"replicas{world}",
                        "l2": "inputs >> L2 (tables %.1f GB, ~%.0f MB of indices per step)" % (
                            acc.info.table_bytes / 1e9, h2d_step / 1e6),
-                       "qps_method": "open-loop Poisson replay of per-query CUDA-event service "
-                                     "times (FIFO server per GPU, exact p95, lambda bisection "
-                                     "to 1%, sim.cpp:246-290); whole job = N x min rank"},
+                       "qps_method": "open-loop Poisson replay (n=50,000, sim.hpp:79) of the "
+                                     "per-query CUDA-event service times measured in the timed "
+                                     "region (FIFO delivery per GPU, in-pipeline residence "
+                                     "added to latency, exact p95, lambda bisection to 1%, "
+                                     "sim.cpp:246-290); whole job = N x min over ranks"},
             "sla": {"p95_ms": r_dev.p95 * 1e3, "p50_ms": r_dev.p50 * 1e3,
                     "at_lambda": r_dev.at_lambda, "saturated_qps": agg["saturated_qps"],
                     "mean_service_ms": float(svc_dev.mean() * 1e3),

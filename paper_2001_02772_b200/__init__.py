@@ -500,16 +500,24 @@ class Accelerator:
                               C.byref(t) if timed else None))
         return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms) if timed else None
 
-    def forward_many(self, sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int,
-                     stream: int = 0, timed: bool = True, residence: bool = False):
-        """rs_forward_many: n whole queries, FIFO-dispatched over the handle's
-        lanes. Returns per-query service times in ms when timed (else None);
-        with residence=True returns (service_ms, residence_ms)."""
+    @staticmethod
+    def batch(sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int):
+        """Pre-built argument arrays for forward_many (keeps Python work out of
+        timed regions)."""
         n = len(sizes)
         qs = (CQuery * n)()
         for i in range(n):
             qs[i] = CQuery(int(sizes[i]), dense_ptrs[i] or None, idx_ptrs[i] or None, location, 0)
         outs = (C.c_void_p * n)(*[C.c_void_p(p) for p in out_ptrs])
+        return n, qs, outs
+
+    def forward_many(self, sizes, dense_ptrs=None, idx_ptrs=None, out_ptrs=None,
+                     location: int = MEM_DEVICE, stream: int = 0, timed: bool = True,
+                     residence: bool = False, prepared=None):
+        """rs_forward_many: n whole queries, FIFO-dispatched over the handle's
+        lanes. Returns per-query service times in ms when timed (else None);
+        with residence=True returns (service_ms, residence_ms)."""
+        n, qs, outs = prepared or self.batch(sizes, dense_ptrs, idx_ptrs, out_ptrs, location)
         svc = np.zeros(n, dtype=np.float64) if timed else None
         lat = np.zeros(n, dtype=np.float64) if (timed and residence) else None
         _check(_lib.rs_forward_many(self._h, n, qs, outs, stream or None,
