@@ -283,8 +283,12 @@ int rs_fill_query(const rs_model_desc* m, int64_t rows_per_table,
                   uint64_t seed, uint64_t query_id, int64_t size,
                   float* dense, int64_t* indices);
 
-/* Pinned host memory for rs_query buffers.                                  */
+/* Pinned host memory for rs_query buffers. rs_alloc_pinned_flags accepts
+ * RS_PINNED_WRITE_COMBINED for input buffers the host only writes (faster
+ * H2D over PCIe; host reads from it are very slow).                         */
+enum { RS_PINNED_DEFAULT = 0, RS_PINNED_WRITE_COMBINED = 1 };
 int rs_alloc_pinned(size_t bytes, void** out);
+int rs_alloc_pinned_flags(size_t bytes, uint32_t flags, void** out);
 int rs_free_pinned(void* p);
 
 int rs_device_count(int* out);

@@ -187,6 +187,7 @@ _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
 _sig("rs_alloc_pinned", C.c_int, C.c_size_t, P(C.c_void_p))
+_sig("rs_alloc_pinned_flags", C.c_int, C.c_size_t, C.c_uint32, P(C.c_void_p))
 _sig("rs_free_pinned", C.c_int, C.c_void_p)
 _sig("rs_device_count", C.c_int, P(C.c_int))
 
@@ -196,7 +197,8 @@ EXPORTED_SYMBOLS = [
     "rs_dist_production", "rs_gen_trace", "rs_qps_under_sla", "rs_accel_create",
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
     "rs_pooled", "rs_service_time",
-    "rs_fill_query", "rs_alloc_pinned", "rs_free_pinned", "rs_device_count"]
+    "rs_fill_query", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
+    "rs_device_count"]
 
 
 # ---- operator API (model_zoo.hpp mirror) ------------------------------------
@@ -557,9 +559,9 @@ class Accelerator:
 class PinnedBuffer:
     """Page-locked host buffer from rs_alloc_pinned, viewable as numpy."""
 
-    def __init__(self, nbytes: int):
+    def __init__(self, nbytes: int, write_combined: bool = False):
         p = C.c_void_p()
-        _check(_lib.rs_alloc_pinned(nbytes, C.byref(p)))
+        _check(_lib.rs_alloc_pinned_flags(nbytes, 1 if write_combined else 0, C.byref(p)))
         self.ptr = p.value
         self.nbytes = nbytes
 

@@ -700,6 +700,15 @@ extern "C" int rs_alloc_pinned(size_t bytes, void** out) {
   });
 }
 
+extern "C" int rs_alloc_pinned_flags(size_t bytes, uint32_t flags, void** out) {
+  return guarded([&] {
+    if (!out) raise(RS_E_INVALID, "null argument");
+    unsigned f = cudaHostAllocPortable;
+    if (flags & RS_PINNED_WRITE_COMBINED) f |= cudaHostAllocWriteCombined;
+    RS_CUDA(cudaHostAlloc(out, std::max<size_t>(bytes, 16), f));
+  });
+}
+
 extern "C" int rs_free_pinned(void* p) {
   return guarded([&] {
     if (p) RS_CUDA(cudaFreeHost(p));

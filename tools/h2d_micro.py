@@ -1,0 +1,50 @@
+"""Host-link microbenchmark: H2D GB/s for query-sized copies (~7 MB, the int64
+indices of a 300-item cfg3 RMC2 query) from regular vs write-combined pinned
+memory (rs_alloc_pinned_flags), back to back on one stream.
+
+  python tools/h2d_micro.py
+"""
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch
+    import paper_2001_02772_b200 as rs
+    out = {}
+    for wc in (False, True):
+        for mb in (1, 7, 32):
+            nbytes = mb << 20
+            bufs = [rs.PinnedBuffer(nbytes, write_combined=wc) for _ in range(4)]
+            srcs = []
+            for b in bufs:
+                b.view(np.uint8, (nbytes,))[...] = 1
+                t = torch.frombuffer((ctypes.c_char * nbytes).from_address(b.ptr), dtype=torch.uint8)
+                srcs.append(t)
+            dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+            reps = max(8, (1 << 30) // nbytes)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for i in range(4):
+                    dst.copy_(srcs[i], non_blocking=True)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                for i in range(reps):
+                    dst.copy_(srcs[i % 4], non_blocking=True)
+                e1.record(s)
+            torch.cuda.synchronize()
+            gbs = reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            out[f"{'wc' if wc else 'pinned'}_{mb}MB"] = round(gbs, 1)
+            out["src_is_pinned"] = bool(srcs[0].is_pinned())
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
