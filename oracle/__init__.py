@@ -187,3 +187,47 @@ if ref is not None:
 
 def ref_available() -> bool:
     return ref is not None
+
+
+# The same reference with accel_service_time wrapped to the B200 path
+# (oracle/ref_b200_adapter.cpp).
+ref_b200 = _load(os.path.join(_HERE, "_ref", "librecsim_ref_b200.so"))
+for _lib_ in (ref, ref_b200):
+    if _lib_ is None:
+        continue
+    _lib_.ref_max_qps_accel.argtypes = [
+        P(OrModel), C.c_char_p, C.c_char_p, C.c_double, C.c_uint64, C.c_int, C.c_double,
+        C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+        P(C.c_double), P(C.c_double), P(C.c_double)]
+    _lib_.ref_tune.argtypes = [
+        P(OrModel), C.c_char_p, C.c_char_p, C.c_double, C.c_uint64, C.c_int, C.c_double,
+        C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int,
+        P(C.c_int64), P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_int64)]
+
+
+def ref_max_qps(lib_, spec, accel: str, cpu: str, sla: float, dist, n: int, batch: int,
+                threshold: int, seed: int = 42):
+    """Reference max_qps_under_sla with a named accelerator ("default" | "b200")."""
+    q, p, f = C.c_double(), C.c_double(), C.c_double()
+    rc = lib_.ref_max_qps_accel(C.byref(model_to_or(spec)), cpu.encode(), accel.encode(), sla,
+                                seed, dist.KINDS[dist.kind], dist.p0, dist.p1, dist.p2,
+                                dist.p3, dist.max_size, n, batch, threshold, C.byref(q),
+                                C.byref(p), C.byref(f))
+    if rc:
+        raise RuntimeError(f"ref_max_qps_accel rc={rc}")
+    return q.value, p.value, f.value
+
+
+def ref_tune(lib_, spec, accel: str, cpu: str, sla: float, dist, n: int, seeds: int = 1,
+             seed: int = 42):
+    """Reference DeepRecSched tune() (autotune.cpp:90-217); accel "" = CPU only."""
+    b, t, steps = C.c_int64(), C.c_int64(), C.c_int64()
+    q, p, f = C.c_double(), C.c_double(), C.c_double()
+    rc = lib_.ref_tune(C.byref(model_to_or(spec)), cpu.encode(), accel.encode(), sla, seed,
+                       dist.KINDS[dist.kind], dist.p0, dist.p1, dist.p2, dist.p3,
+                       dist.max_size, n, seeds, C.byref(b), C.byref(t), C.byref(q),
+                       C.byref(p), C.byref(f), C.byref(steps))
+    if rc:
+        raise RuntimeError(f"ref_tune rc={rc}")
+    return {"batch": b.value, "threshold": t.value, "qps": q.value, "p95": p.value,
+            "accel_work_fraction": f.value, "search_steps": steps.value}

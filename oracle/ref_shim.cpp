@@ -196,4 +196,61 @@ int ref_max_qps(const or_model* m, const char* cpu, double sla, uint64_t seed, i
   });
 }
 
+// Accelerator by name: "default" = the reference's modeled 1080Ti-class spec
+// (platform.cpp:174-183); "b200" = the same positive placeholder fields with
+// the name the integration adapter (ref_b200_adapter.cpp) routes to the GPU.
+static AcceleratorSpec named_accel(const char* name) {
+  AcceleratorSpec a = builtin_accel("default");
+  if (std::strcmp(name, "default") != 0) a.name = name;
+  return a;
+}
+
+// max_qps_under_sla (sim.cpp:246-290) with a named accelerator at threshold T.
+int ref_max_qps_accel(const or_model* m, const char* cpu, const char* accel, double sla,
+                      uint64_t seed, int kind, double p0, double p1, double p2, double p3,
+                      int64_t max_size, int64_t n, int64_t batch, int64_t threshold,
+                      double* qps, double* p95, double* frac) {
+  return guard([&] {
+    SchedulerConfig cfg;
+    cfg.batch_size = batch;
+    cfg.model = to_spec(*m);
+    cfg.cpu = builtin_cpu(cpu);
+    if (threshold > 0) {
+      cfg.offload_threshold = threshold;
+      cfg.accel = named_accel(accel);
+    }
+    TraceGenParams gen;
+    gen.base_seed = seed;
+    gen.dist = make_dist(kind, p0, p1, p2, p3, max_size);
+    gen.n = n;
+    QpsResult r = max_qps_under_sla(cfg, sla, gen);
+    *qps = r.qps;
+    *p95 = r.p95;
+    *frac = r.accel_work_fraction;
+  });
+}
+
+// DeepRecSched tune() (autotune.cpp:90-217) with a named accelerator ("" = CPU only).
+int ref_tune(const or_model* m, const char* cpu, const char* accel, double sla, uint64_t seed,
+             int kind, double p0, double p1, double p2, double p3, int64_t max_size, int64_t n,
+             int seeds, int64_t* batch, int64_t* threshold, double* qps, double* p95,
+             double* frac, int64_t* steps) {
+  return guard([&] {
+    TuneParams tp;
+    tp.gen.base_seed = seed;
+    tp.gen.dist = make_dist(kind, p0, p1, p2, p3, max_size);
+    tp.gen.n = n;
+    tp.seeds_to_average = seeds;
+    std::optional<AcceleratorSpec> a;
+    if (accel && accel[0]) a = named_accel(accel);
+    TunedConfig t = tune(to_spec(*m), builtin_cpu(cpu), a, sla, tp);
+    *batch = t.batch_size;
+    *threshold = t.offload_threshold ? *t.offload_threshold : 0;
+    *qps = t.qps;
+    *p95 = t.p95;
+    *frac = t.accel_work_fraction;
+    *steps = static_cast<int64_t>(t.search_path.size());
+  });
+}
+
 }  // extern "C"

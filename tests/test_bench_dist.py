@@ -1,0 +1,57 @@
+"""bench.py's multi-GPU plumbing on CPU (gloo, world_size 2): independent replica
+streams per rank, slowest-rank timing, whole-job aggregation — the same
+functions bench.py calls under torchrun/NCCL. There is no data-path collective
+(SURVEY §8e): replicas serve independent query streams."""
+import os
+import socket
+
+import pytest
+
+import bench
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        qps = 1000.0 + 100.0 * rank          # rank 0 is the slowest replica
+        t = 2.0 - 0.5 * rank                 # rank 0 takes longest
+        agg = bench.aggregate(qps, t, queries=500 + rank, world=world)
+        q.put((rank, agg, bench.rank_seed(rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_aggregation_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = dict((r, (a, s)) for r, a, s in (q.get() for _ in range(2)))
+    for r in (0, 1):
+        agg, _ = res[r]
+        assert agg["time_s"] == pytest.approx(2.0)            # max over ranks
+        assert agg["value"] == pytest.approx(2 * 1000.0)      # N x min rank QPS
+        assert agg["saturated_qps"] == pytest.approx(1001 / 2.0)
+    assert res[0][1] != res[1][1]                             # independent streams
+    assert res[0][1] == 42 and res[1][1] == 42 + 10007         # autotune.cpp:23 seeds
+
+
+def test_single_process_aggregation_is_identity():
+    agg = bench.aggregate(123.0, 0.5, queries=10, world=1)
+    assert agg == {"time_s": 0.5, "value": 123.0, "saturated_qps": 20.0}
