@@ -297,7 +297,12 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   if (a.lda % 4 || a.ldw % 4 || (a.sAz % 4) || (a.sWz % 4)) return false;
   if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.W) & 15))
     return false;
-  p->block_n = a.N >= 128 ? 128 : 64;
+  // tile/pipeline configuration: 0 <BN128,3 stages> 1 <64,4> 2 <128,6> 3 <64,8>
+  // (RS_TC_CFG overrides, for tools/fc_micro.py)
+  p->cfg = a.N >= 128 ? 0 : 1;
+  if (const char* e = getenv("RS_TC_CFG")) p->cfg = atoi(e) & 3;
+  if (a.N < 128 && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
+  p->block_n = (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
   p->m_tiles = (int)((m_cap + BM - 1) / BM);
   p->n_tiles = (a.N + p->block_n - 1) / p->block_n;
   // A: [batch][rows][K] (or shared 2D when sAz == 0)
@@ -319,20 +324,28 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
     cuuint32_t box[3] = {BK, (cuuint32_t)p->block_n, 1};
     if (!encode(&p->map_w, a.W, 3, dims, str, box)) return false;
   }
-  if (p->block_n == 128) set_attr_once<128, 3>();
-  else set_attr_once<64, 4>();
+  switch (p->cfg) {
+    case 0: set_attr_once<128, 3>(); break;
+    case 1: set_attr_once<64, 4>(); break;
+    case 2: set_attr_once<128, 6>(); break;
+    default: set_attr_once<64, 8>(); break;
+  }
   return true;
 }
 
 void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s) {
   const dim3 grid(p.n_tiles, p.m_tiles, a.batch);
   const int a_batched = a.sAz != 0 ? 1 : 0;
-  if (p.block_n == 128)
-    fc_tc_kernel<128, 3><<<grid, 256, tc_smem_bytes<128, 3>(), s>>>(qd, p.map_a, p.map_w, a,
-                                                                     a_batched);
-  else
-    fc_tc_kernel<64, 4><<<grid, 256, tc_smem_bytes<64, 4>(), s>>>(qd, p.map_a, p.map_w, a,
-                                                                   a_batched);
+#define RS_TC(BN, ST)                                                                     \
+  fc_tc_kernel<BN, ST><<<grid, 256, tc_smem_bytes<BN, ST>(), s>>>(qd, p.map_a, p.map_w, a, \
+                                                                  a_batched)
+  switch (p.cfg) {
+    case 0: RS_TC(128, 3); break;
+    case 1: RS_TC(64, 4); break;
+    case 2: RS_TC(128, 6); break;
+    default: RS_TC(64, 8); break;
+  }
+#undef RS_TC
 }
 
 }  // namespace rs

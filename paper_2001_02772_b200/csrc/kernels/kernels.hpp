@@ -45,7 +45,8 @@ void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStr
 struct TcPlan {
   CUtensorMap map_a;   // A: [batch][M_cap][K] fp32, box 128 x 32
   CUtensorMap map_w;   // W: [batch][N][K] fp32, box BN x 32
-  int block_n;         // 64 / 128 / 256
+  int block_n;         // 64 / 128
+  int cfg;             // tile/pipeline configuration (fc_tcgen05.cu)
   int m_tiles, n_tiles;
 };
 bool tc_available();
