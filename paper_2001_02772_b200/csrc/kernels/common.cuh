@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../spec.h"
 
 namespace rs {
@@ -67,5 +69,36 @@ __device__ __forceinline__ float4 shfl_xor4(const float4& v, int off) {
 __host__ __device__ __forceinline__ int64_t round_up(int64_t x, int64_t m) {
   return (x + m - 1) / m * m;
 }
+
+// Programmatic dependent launch (PDL). Every kernel of the forward graph is
+// launched with programmatic stream serialisation: it lets its successor
+// launch as soon as it starts (pdl_trigger), and blocks on its predecessor
+// (pdl_wait: full completion + memory visibility) only right before it
+// touches data the predecessor wrote. Both are no-ops without a programmatic
+// dependency.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+#if defined(__CUDACC__)
+// Launch with the programmatic-stream-serialisation attribute (captured into
+// a CUDA graph as a programmatic dependency edge).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
 
 }  // namespace rs

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
                int hint) {
+  pdl_trigger();  // let the interaction grid launch behind us
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   __shared__ int64_t sidx[kWarps][kIdxChunk];
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(32)
 sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap tmap,
                int64_t rows, int T, int L, int LB, float* __restrict__ out, int64_t ld_out,
                int* __restrict__ err) {
+  pdl_trigger();
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   extern __shared__ __align__(128) uint8_t sm_raw[];
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_scalar_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
                       int64_t rows, int T, int L, int D, float* __restrict__ out,
                       int64_t ld_out, int* __restrict__ err) {
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t bags = qd->S * T;
   const int64_t* __restrict__ idx = qd->idx;
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(256)
 gather_concat_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
                      int64_t rows, int T, int L, int D, float* __restrict__ out,
                      int64_t ld_out, int64_t col_off, int vec, int* __restrict__ err) {
+  pdl_trigger();
   const int64_t S = qd->S;
   const int64_t* __restrict__ idx = qd->idx;
   const int64_t TL = (int64_t)T * L;
@@ -311,6 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                 int T, int L, const float* __restrict__ att_w, float* __restrict__ out,
                 int64_t ld_out, int64_t col_off, int* __restrict__ err) {
+  pdl_trigger();
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   __shared__ int64_t sidx[kWarps][kIdxChunk];
@@ -431,6 +436,8 @@ __global__ void __launch_bounds__(kInterThreads)
 interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
                    int64_t ld_pooled, int T, int D, float* __restrict__ X, int64_t ld_x,
                    int64_t sum_off, int64_t dot_off, int has_dense) {
+  pdl_trigger();
+  pdl_wait();  // pooled (SLS) and X[:, 0:D] (bottom MLP) are predecessors' outputs
   extern __shared__ float sv[];  // [(T+1)][D+1]
   const int P = has_dense ? (T + 1) * T / 2 : 0;
   const int ldv = D + 1;
@@ -636,8 +643,8 @@ void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled,
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(interaction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  interaction_kernel<<<grid, kInterThreads, smem, s>>>(qd, pooled, ld_pooled, T, D, X, ld_x,
-                                                       sum_off, dot_off, has_dense);
+  launch_pdl(interaction_kernel, dim3(grid), dim3(kInterThreads), smem, s, qd, pooled, ld_pooled,
+             T, D, X, ld_x, sum_off, dot_off, has_dense);
 }
 
 size_t interaction_smem(int T, int D) { return (size_t)(T + 1) * (D + 1) * sizeof(float); }

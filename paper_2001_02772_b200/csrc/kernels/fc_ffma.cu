@@ -38,9 +38,11 @@ __global__ void __launch_bounds__(THREADS)
 fc_ffma_kernel(const QDesc* __restrict__ qd, FcArgs a) {
   __shared__ __align__(16) float As[STAGES][BM][PITCH];
   __shared__ __align__(16) float Bs[STAGES][BN][PITCH];
+  pdl_trigger();
   const int64_t M = qd->S;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, z = blockIdx.z;
   if (m0 >= M) return;
+  pdl_wait();  // A is the previous layer's output
   const float* __restrict__ A = a.A + (int64_t)z * a.sAz;
   const float* __restrict__ W = a.W + (int64_t)z * a.sWz;
   const int tid = threadIdx.x;
@@ -131,7 +133,7 @@ fc_ffma_kernel(const QDesc* __restrict__ qd, FcArgs a) {
 
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s) {
   const dim3 grid((a.N + BN - 1) / BN, (unsigned)((max_items + BM - 1) / BM), a.batch);
-  fc_ffma_kernel<<<grid, THREADS, 0, s>>>(qd, a);
+  launch_pdl(fc_ffma_kernel, grid, dim3(THREADS), 0, s, qd, a);
 }
 
 }  // namespace rs

@@ -104,11 +104,13 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   extern __shared__ uint8_t smem_raw[];
   TcSmem<BN, STAGES>& sm = *reinterpret_cast<TcSmem<BN, STAGES>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  pdl_trigger();
   const int64_t M = qd->S;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, z = blockIdx.z;
   if (m0 >= M) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (a.K + BK - 1) / BK;
+  const int pre = nk < STAGES ? nk : STAGES;  // stages whose weights load before the wait
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -134,18 +136,29 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = sm.tmem_base;
+  constexpr uint32_t kBytes = (BM + BN) * BK * sizeof(float);
+  // Weights do not depend on the previous layer: their first `pre` slabs are
+  // in flight before this grid waits on its predecessor (PDL).
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < pre; ++kb) {
+      mbar_expect_tx(&sm.full[kb], kBytes);
+      tma_load_3d(sm.b[kb], &map_w, &sm.full[kb], kb * BK, n0, z);
+    }
+  }
+  pdl_wait();  // the activations A are the previous layer's output
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
-    constexpr uint32_t kBytes = (BM + BN) * BK * sizeof(float);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-      mbar_wait(&sm.empty[s], ph ^ 1u);
-      mbar_expect_tx(&sm.full[s], kBytes);
+      if (kb >= pre) {
+        mbar_wait(&sm.empty[s], ph ^ 1u);
+        mbar_expect_tx(&sm.full[s], kBytes);
+        tma_load_3d(sm.b[s], &map_w, &sm.full[s], kb * BK, n0, z);
+      }
       if (a_batched) tma_load_3d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0, z);
       else tma_load_2d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0);
-      tma_load_3d(sm.b[s], &map_w, &sm.full[s], kb * BK, n0, z);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread) ----
@@ -336,9 +349,9 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
 void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s) {
   const dim3 grid(p.n_tiles, p.m_tiles, a.batch);
   const int a_batched = a.sAz != 0 ? 1 : 0;
-#define RS_TC(BN, ST)                                                                     \
-  fc_tc_kernel<BN, ST><<<grid, 256, tc_smem_bytes<BN, ST>(), s>>>(qd, p.map_a, p.map_w, a, \
-                                                                  a_batched)
+#define RS_TC(BN, ST)                                                                   \
+  launch_pdl(fc_tc_kernel<BN, ST>, grid, dim3(256), tc_smem_bytes<BN, ST>(), s, qd, p.map_a, \
+             p.map_w, a, a_batched)
   switch (p.cfg) {
     case 0: RS_TC(128, 3); break;
     case 1: RS_TC(64, 4); break;
