@@ -56,6 +56,7 @@ struct Slot {
   int* d_err = nullptr;
   int* h_err = nullptr;        // pinned ring [kDescRing]
   float* dense_stage = nullptr;
+  float* dense_raw = nullptr;   // contiguous H2D landing zone for strided dense
   int64_t* idx_stage = nullptr;
   float* act[2] = {nullptr, nullptr};
   float* pooled = nullptr;
@@ -424,6 +425,8 @@ std::unique_ptr<Slot> make_slot(rs_accel* a) {
   std::memset(s->h_err, 0, sizeof(int) * kDescRing);
   s->d_err = static_cast<int*>(dmalloc(a, s->allocs, sizeof(int)));
   s->dense_stage = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_dense * 4)));
+  s->dense_raw = static_cast<float*>(
+      dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->dense_in, 1) * 4), false));
   s->idx_stage = static_cast<int64_t*>(
       dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->T * a->L, 1) * 8)));
   for (int i = 0; i < 2; ++i) {
@@ -515,11 +518,22 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
     if (!q->dense) raise(RS_E_INVALID, "null dense features");
     float* dst = a->m.has_dense_fc ? s->dense_stage : s->X;
     const int64_t ld = a->m.has_dense_fc ? a->ld_dense : a->ld_x;
-    if (ld == a->dense_in)
+    if (ld == a->dense_in) {
       RS_CUDA(cudaMemcpyAsync(dst, q->dense, (size_t)(S * a->dense_in * 4), kind, st));
-    else
-      RS_CUDA(cudaMemcpy2DAsync(dst, (size_t)(ld * 4), q->dense, (size_t)(a->dense_in * 4),
-                                (size_t)(a->dense_in * 4), (size_t)S, kind, st));
+    } else {
+      // Strided placement: from host, one contiguous H2D into the raw staging
+      // buffer first (a row-by-row 2D DMA over PCIe is several times slower),
+      // then the strided copy on the device.
+      const float* src = q->dense;
+      if (host) {
+        RS_CUDA(cudaMemcpyAsync(s->dense_raw, q->dense, (size_t)(S * a->dense_in * 4),
+                                cudaMemcpyHostToDevice, st));
+        src = s->dense_raw;
+      }
+      RS_CUDA(cudaMemcpy2DAsync(dst, (size_t)(ld * 4), src, (size_t)(a->dense_in * 4),
+                                (size_t)(a->dense_in * 4), (size_t)S, cudaMemcpyDeviceToDevice,
+                                st));
+    }
   }
   const int64_t* idx = nullptr;
   if (a->T > 0) {
@@ -617,16 +631,18 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     std::lock_guard<std::mutex> many_lock(a->many_mu);
     if (latency_ms && !service_ms) raise(RS_E_INVALID, "latency_ms needs service_ms");
     if (service_ms) {
-      while ((int64_t)a->evpool.size() < n + 1) {
-        cudaEvent_t e;
-        RS_CUDA(cudaEventCreate(&e));
-        a->evpool.push_back(e);
-      }
-      while (latency_ms && (int64_t)a->evstart.size() < n) {
-        cudaEvent_t e;
-        RS_CUDA(cudaEventCreate(&e));
-        a->evstart.push_back(e);
-      }
+      // event pools grow in 4096-event chunks so a timed call after a
+      // warm-up call does not pay event creation
+      auto grow = [](std::vector<cudaEvent_t>& pool, int64_t need) {
+        const int64_t target = (need + 4095) / 4096 * 4096;
+        while ((int64_t)pool.size() < target) {
+          cudaEvent_t e;
+          RS_CUDA(cudaEventCreate(&e));
+          pool.push_back(e);
+        }
+      };
+      grow(a->evpool, n + 1);
+      if (latency_ms) grow(a->evstart, n);
       RS_CUDA(cudaEventRecord(a->evpool[0], st));
     }
     // Queries are dispatched in FIFO order round-robin over `depth` lanes
