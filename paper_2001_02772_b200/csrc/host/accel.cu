@@ -280,7 +280,7 @@ GruArgs gru_args(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off) {
 }
 
 // Enqueue the pooling stage writing into out[item*ld + off ...].
-void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off,
+void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off, bool tc,
                      cudaStream_t st) {
   const rs_model_desc& m = a->m;
   const int64_t maxS = a->init.max_query_size;
@@ -301,7 +301,8 @@ void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off,
       break;
     case RS_POOL_ATTENTION_RNN: {
       GruArgs g = gru_args(a, s, out, ld, off);
-      launch_gru(s->d_q, g, maxS, a->sm_count, st);
+      // tensor-core recurrence in the tcgen05 graph, FFMA recurrence otherwise
+      if (!(tc && launch_gru_tc(s->d_q, g, maxS, st))) launch_gru(s->d_q, g, maxS, a->sm_count, st);
       break;
     }
   }
@@ -360,7 +361,7 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   const bool tc = kind == kGraphLarge;
   int ntc = 0;
   if (kind == kGraphPool) {
-    enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, st);
+    enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode == RS_FC_TF32, st);
   } else {
     // The bottom MLP and the embedding stage are independent (they write
     // disjoint columns of X): capture them as parallel graph branches.
@@ -375,14 +376,14 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
     if (fork) RS_CUDA(cudaEventRecord(s->join, s->cap2));
     if (m.pooling == RS_POOL_SUM) {
       if (a->T > 0) {
-        enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, st);
+        enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, tc, st);
         if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
         launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
                            a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
                            a->sm_count, st);
       }
     } else {
-      enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, st);
+      enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, tc, st);
       if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
     }
     ntc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w,

@@ -1,0 +1,298 @@
+// gru_tcgen05.cu — DIEN interest-evolution GRU/AUGRU (AttentionRNN,
+// proj/src/model_zoo.cpp:217-227) on the 5th-generation tensor cores.
+//
+// One CTA owns 128 sequences (items) of one table for all L steps; thread i
+// (of 128) owns sequence i and TMEM lane i. Per step, ONE chain of
+// tcgen05.mma (kind::tf32, M=128, N=4H, K=D+H in 8-wide slices) computes all
+// gate pre-activations at once:
+//
+//   [x_t | h_t] (128 x (D+H), smem, SWIZZLE_128B K-major)
+//     x  [ W_ir W_hr ; W_iz W_hz ; W_in 0 ; 0 W_hn ]^T  ((D+H) x 4H, smem)
+//   -> TMEM columns [r | z | n_x | n_h], fp32
+//
+// Thread i then tcgen05.ld's its row, applies the cell (same equations as
+// gru.cu / DESIGN.md §3, biases folded per gate), and writes h_{t+1} back
+// into the swizzled A operand in shared memory (generic-proxy writes fenced
+// to the async proxy before the next MMA). The next step's embedding rows
+// are prefetched into registers while the MMA runs. The recurrence is serial
+// in t, so the work per step is one MMA chain + one epilogue; tensor cores
+// replace the 18K FFMA per sequence-step of the FFMA kernel.
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace rs {
+namespace {
+
+constexpr int kSeq = 128;  // sequences per CTA = UMMA M = TMEM lanes
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+// byte offset of fp32 element (row, c) inside a 128-row x 32-col SW128 atom
+__device__ __forceinline__ uint32_t sw_off(int row, int c) {
+  return (uint32_t)(row * 128 + ((((c >> 2) ^ row) & 7) << 4) + (c & 3) * 4);
+}
+__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+template <int D, int H>
+struct GruTcSmem {
+  static constexpr int KA = (D + H) / 32;  // K atoms
+  static constexpr int N = 4 * H;
+  alignas(1024) uint8_t b[KA][N * 128];     // weights, per K atom
+  alignas(1024) uint8_t ax[2][D / 32][kSeq * 128];
+  alignas(1024) uint8_t ah[H / 32][kSeq * 128];
+  float bias[N];
+  uint64_t mma_done;
+  uint32_t tmem_base;
+};
+
+template <int D, int H>
+__global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
+  pdl_trigger();
+  using SM = GruTcSmem<D, H>;
+  constexpr int N = SM::N, KA = SM::KA, DA = D / 32;
+  extern __shared__ uint8_t smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int t = blockIdx.y;
+  const int64_t item0 = (int64_t)blockIdx.x * kSeq;
+  const int64_t S = qd->S;
+  if (item0 >= S) return;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t item = item0 + tid;
+  const bool live = item < S;
+  const int L = g.L;
+  const int64_t* __restrict__ idx = qd->idx;
+  const float* __restrict__ tab = g.tables + (int64_t)t * g.rows * D;
+
+  // ---- weights -> swizzled K-major B operand; folded biases ----
+  {
+    const float* Wih = g.w_ih + (int64_t)t * 3 * H * D;
+    const float* Whh = g.w_hh + (int64_t)t * 3 * H * H;
+    for (int e = tid; e < N * (D + H); e += kSeq) {
+      const int n = e / (D + H), k = e - n * (D + H);
+      const int gate = n / H, j = n - gate * H;
+      float v = 0.f;
+      if (k < D) {
+        if (gate < 3) v = __ldg(Wih + (int64_t)(gate * H + j) * D + k);
+      } else {
+        const int kh = k - D;
+        if (gate == 0 || gate == 1) v = __ldg(Whh + (int64_t)(gate * H + j) * H + kh);
+        else if (gate == 3) v = __ldg(Whh + (int64_t)(2 * H + j) * H + kh);
+      }
+      const int atom = k >> 5, c = k & 31;
+      *reinterpret_cast<float*>(sm.b[atom] + n * 128 + ((((c >> 2) ^ n) & 7) << 4) + (c & 3) * 4) = v;
+    }
+    const float* bih = g.b_ih + (int64_t)t * 3 * H;
+    const float* bhh = g.b_hh + (int64_t)t * 3 * H;
+    for (int n = tid; n < N; n += kSeq) {
+      const int gate = n / H, j = n - gate * H;
+      sm.bias[n] = gate == 0 ? bih[j] + bhh[j]
+                 : gate == 1 ? bih[H + j] + bhh[H + j]
+                 : gate == 2 ? bih[2 * H + j] : bhh[2 * H + j];
+    }
+    // h_0 = 0
+    for (int a = 0; a < H / 32; ++a)
+      for (int c4 = 0; c4 < 8; ++c4)
+        *reinterpret_cast<float4*>(sm.ah[a] + tid * 128 + c4 * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     s_u32(&sm.tmem_base)), "r"(N) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&sm.mma_done)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+
+  // ---- x rows of step l for this thread's sequence ----
+  float4 xn[D / 4];
+  auto fetch = [&](int l) {
+#pragma unroll
+    for (int q = 0; q < D / 4; ++q) xn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!live) return;
+    const int64_t r = __ldg(idx + (item * g.T + t) * L + l);
+    if ((uint64_t)r >= (uint64_t)g.rows) {
+      atomicOr(g.err, kErrIndex);
+      return;
+    }
+    const float4* p = reinterpret_cast<const float4*>(tab + r * D);
+#pragma unroll
+    for (int q = 0; q < D / 4; ++q) xn[q] = ldg_stream(p + q);
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < D / 4; ++q)
+      *reinterpret_cast<float4*>(sm.ax[buf][q >> 3] + sw_off(tid, (q & 7) * 4)) = xn[q];
+  };
+  fetch(0);
+  stash(0);
+
+  // AUGRU: ua = W_a^T x_0 for this sequence (kept in registers)
+  float ua[D];
+  float xc[D];
+  if (g.augru) {
+    const float* Wa = g.w_att + (int64_t)t * D * D;
+#pragma unroll
+    for (int c = 0; c < D; ++c) ua[c] = 0.f;
+#pragma unroll
+    for (int q = 0; q < D / 4; ++q) {
+      const float xs[4] = {xn[q].x, xn[q].y, xn[q].z, xn[q].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = q * 4 + u;
+#pragma unroll
+        for (int c = 0; c < D; ++c) ua[c] = fmaf(xs[u], __ldg(Wa + i * D + c), ua[c]);
+      }
+    }
+  }
+
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+                         ((uint32_t)(kSeq >> 4) << 24);
+
+  for (int l = 0; l < L; ++l) {
+    const int xb = l & 1;
+    if (tid == 0) {
+#pragma unroll
+      for (int a = 0; a < KA; ++a) {
+        const uint32_t abase = a < DA ? s_u32(sm.ax[xb][a]) : s_u32(sm.ah[a - DA]);
+        const uint32_t bbase = s_u32(sm.b[a]);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t acc = (a | kk) ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(sw128(abase + kk * 32)), "l"(sw128(bbase + kk * 32)), "r"(idesc), "r"(acc)
+              : "memory");
+        }
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              s_u32(&sm.mma_done))
+          : "memory");
+    }
+    // overlap: keep x_l for AUGRU, prefetch x_{l+1}
+    if (g.augru) {
+#pragma unroll
+      for (int q = 0; q < D / 4; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(sm.ax[xb][q >> 3] + sw_off(tid, (q & 7) * 4));
+        xc[4 * q] = v.x; xc[4 * q + 1] = v.y; xc[4 * q + 2] = v.z; xc[4 * q + 3] = v.w;
+      }
+    }
+    if (l + 1 < L) fetch(l + 1);
+    float att = 1.f;
+    if (g.augru) {
+      float sc = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; ++c) sc = fmaf(ua[c], xc[c], sc);
+      att = sigm(sc);
+    }
+    // wait for the gate pre-activations
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(s_u32(&sm.mma_done)),
+        "r"((uint32_t)(l & 1))
+        : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+    for (int j0 = 0; j0 < H; j0 += 16) {
+      uint32_t v[4][16];
+#pragma unroll
+      for (int gte = 0; gte < 4; ++gte) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[gte][0]), "=r"(v[gte][1]), "=r"(v[gte][2]), "=r"(v[gte][3]),
+              "=r"(v[gte][4]), "=r"(v[gte][5]), "=r"(v[gte][6]), "=r"(v[gte][7]),
+              "=r"(v[gte][8]), "=r"(v[gte][9]), "=r"(v[gte][10]), "=r"(v[gte][11]),
+              "=r"(v[gte][12]), "=r"(v[gte][13]), "=r"(v[gte][14]), "=r"(v[gte][15])
+            : "r"(lane_base + (uint32_t)(gte * H + j0)));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + 4 * q;
+        uint8_t* hp = sm.ah[j >> 5] + sw_off(tid, j & 31);
+        const float4 ho = *reinterpret_cast<const float4*>(hp);
+        const float hold[4] = {ho.x, ho.y, ho.z, ho.w};
+        float hn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int jj = 4 * q + u, jx = j + u;
+          const float r = sigm(__uint_as_float(v[0][jj]) + sm.bias[jx]);
+          const float z = sigm(__uint_as_float(v[1][jj]) + sm.bias[H + jx]);
+          const float n = tanhf(__uint_as_float(v[2][jj]) + sm.bias[2 * H + jx] +
+                                r * (__uint_as_float(v[3][jj]) + sm.bias[3 * H + jx]));
+          if (g.augru) {
+            const float uu = att * (1.0f - z);
+            hn[u] = (1.0f - uu) * hold[u] + uu * n;
+          } else {
+            hn[u] = (1.0f - z) * n + z * hold[u];
+          }
+        }
+        *reinterpret_cast<float4*>(hp) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+      }
+    }
+    if (l + 1 < L) stash(xb ^ 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+
+  if (live) {  // h_L from this sequence's row of the A operand
+    float* o = g.out + item * g.ld_out + g.col_off + (int64_t)t * H;
+#pragma unroll
+    for (int j = 0; j < H; j += 4) {
+      const float4 h = *reinterpret_cast<const float4*>(sm.ah[j >> 5] + sw_off(tid, j & 31));
+      o[j] = h.x; o[j + 1] = h.y; o[j + 2] = h.z; o[j + 3] = h.w;
+    }
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(N)
+                 : "memory");
+}
+
+template <int D, int H>
+void launch_typed(const QDesc* qd, const GruArgs& g, int64_t max_items, cudaStream_t s) {
+  const size_t smem = sizeof(GruTcSmem<D, H>) + 1024;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(gru_tc_kernel<D, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  });
+  const dim3 grid((unsigned)((max_items + kSeq - 1) / kSeq), g.T);
+  gru_tc_kernel<D, H><<<grid, kSeq, smem, s>>>(qd, g);
+}
+
+}  // namespace
+
+bool gru_tc_supported(int D, int H) {
+  return (D == 32 || D == 64) && (H == 32 || H == 64) && tc_available();
+}
+
+bool launch_gru_tc(const QDesc* qd, const GruArgs& g, int64_t max_items, cudaStream_t s) {
+  if (!gru_tc_supported(g.D, g.H)) return false;
+  if (g.D == 32 && g.H == 64) launch_typed<32, 64>(qd, g, max_items, s);
+  else if (g.D == 32 && g.H == 32) launch_typed<32, 32>(qd, g, max_items, s);
+  else if (g.D == 64 && g.H == 64) launch_typed<64, 64>(qd, g, max_items, s);
+  else launch_typed<64, 32>(qd, g, max_items, s);
+  return true;
+}
+
+}  // namespace rs

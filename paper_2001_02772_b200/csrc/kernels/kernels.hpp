@@ -67,6 +67,9 @@ struct GruArgs {
   int* err;
 };
 bool gru_supported(int D, int H);
+// gru_tcgen05.cu: tensor-core recurrence (D, H in {32, 64}); false if unsupported
+bool gru_tc_supported(int D, int H);
+bool launch_gru_tc(const QDesc* qd, const GruArgs& g, int64_t max_items, cudaStream_t s);
 void prepare_gru(const GruArgs& g);
 void launch_gru(const QDesc* qd, const GruArgs& g, int64_t max_items, int sm_count,
                 cudaStream_t s);

@@ -50,8 +50,13 @@ def check_forward(spec, rows, S, fc_mode=rs.FC_FP32, augru=False, seed=3, qid=0,
         if spec.embeddings.pooling == "Sum":
             assert np.array_equal(pooled, orc.sls_canonical(idx)), "SLS not bit-exact"
         else:
+            # the tf32 handle pools DIEN with the tensor-core recurrence
+            tc_rnn = fc_mode == rs.FC_TF32 and spec.embeddings.pooling == "AttentionRNN"
+            ptol = TF32_TOL if tc_rnn else FP32_TOL
             ep = rel_err(pooled, pref, pmag)
-            assert ep <= FP32_TOL, f"{spec.name}: pooled max|d|/mag = {ep:.3g}"
+            assert ep <= ptol, f"{spec.name}: pooled max|d|/mag = {ep:.3g}"
+            if tc_rnn:
+                assert normwise(pooled, pref) <= NORMWISE[TF32_TOL]
     acc.close()
     return e
 
@@ -211,3 +216,16 @@ def test_forward_many_matches_single_calls_and_auto_graphs():
         acc.sync()
     acc.sync()
     acc.close()
+
+
+@pytest.mark.parametrize("augru", [False, True])
+@pytest.mark.parametrize("L", [20, 100])
+def test_dien_tensor_core_recurrence(augru, L):
+    """The tcgen05 GRU/AUGRU (tf32 gate matmuls, fp32 cell math) against the
+    fp64 oracle, zoo DIEN (L=20) and BASELINE configs[4] sequence length 100."""
+    spec = rs.ModelSpec(f"dien-L{L}", predict_fc=rs.LayerStack([200, 80, 2]),
+                        embeddings=rs.EmbeddingConfig(20, L, 32, "AttentionRNN"),
+                        recurrent_hidden_dim=64)
+    for S in (5, 200):
+        check_forward(spec, rows=50000, S=S, fc_mode=rs.FC_TF32, augru=augru, tol=TF32_TOL,
+                      max_q=256)
