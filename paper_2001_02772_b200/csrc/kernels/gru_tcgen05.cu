@@ -1,22 +1,23 @@
 // gru_tcgen05.cu — DIEN interest-evolution GRU/AUGRU (AttentionRNN,
 // proj/src/model_zoo.cpp:217-227) on the 5th-generation tensor cores.
 //
-// One CTA owns 128 sequences (items) of one table for all L steps; thread i
-// (of 128) owns sequence i and TMEM lane i. Per step, ONE chain of
-// tcgen05.mma (kind::tf32, M=128, N=4H, K=D+H in 8-wide slices) computes all
-// gate pre-activations at once:
+// One CTA owns 128 sequences (items) of one table for all L steps. Per step,
+// ONE chain of tcgen05.mma (kind::tf32, M=128, N=4H, K=D+H in 8-wide slices)
+// computes every gate pre-activation of every sequence:
 //
 //   [x_t | h_t] (128 x (D+H), smem, SWIZZLE_128B K-major)
 //     x  [ W_ir W_hr ; W_iz W_hz ; W_in 0 ; 0 W_hn ]^T  ((D+H) x 4H, smem)
 //   -> TMEM columns [r | z | n_x | n_h], fp32
 //
-// Thread i then tcgen05.ld's its row, applies the cell (same equations as
-// gru.cu / DESIGN.md §3, biases folded per gate), and writes h_{t+1} back
-// into the swizzled A operand in shared memory (generic-proxy writes fenced
-// to the async proxy before the next MMA). The next step's embedding rows
-// are prefetched into registers while the MMA runs. The recurrence is serial
-// in t, so the work per step is one MMA chain + one epilogue; tensor cores
-// replace the 18K FFMA per sequence-step of the FFMA kernel.
+// The epilogue is split over two threads per sequence: warps w and w+4 read
+// the same TMEM lanes (sequences 32(w%4)..+31) but different halves of the
+// hidden units. Each thread applies the cell (biases folded per
+// gate) to its units and writes h_{t+1} straight back into the swizzled A
+// operand (generic-proxy writes fenced to the async proxy before the next
+// MMA). The next step's embedding rows are prefetched into registers while
+// the MMA runs. The recurrence is serial in t: per step one MMA chain and one
+// epilogue; the tensor core replaces the 18K FFMA per sequence-step of
+// gru.cu's FFMA kernel.
 #include <algorithm>
 #include <mutex>
 
@@ -26,7 +27,8 @@
 namespace rs {
 namespace {
 
-constexpr int kSeq = 128;  // sequences per CTA = UMMA M = TMEM lanes
+constexpr int kSeq = 128;           // sequences per CTA = UMMA M = TMEM lanes
+constexpr int kThreads = 2 * kSeq;  // two threads per sequence (hidden units split)
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -39,7 +41,12 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
 __device__ __forceinline__ uint32_t sw_off(int row, int c) {
   return (uint32_t)(row * 128 + ((((c >> 2) ^ row) & 7) << 4) + (c & 3) * 4);
 }
-__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
+// Cell nonlinearities on the SFU (ex2.approx): ~1e-6 relative, far inside the
+// tf32 operand rounding this path is toleranced for.
+__device__ __forceinline__ float sigm(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanh_fast(float x) {
+  return 1.0f - __fdividef(2.0f, __expf(2.0f * x) + 1.0f);
+}
 
 template <int D, int H>
 struct GruTcSmem {
@@ -54,28 +61,34 @@ struct GruTcSmem {
 };
 
 template <int D, int H>
-__global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
+__global__ void __launch_bounds__(kThreads, 1)
+gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   pdl_trigger();
   using SM = GruTcSmem<D, H>;
   constexpr int N = SM::N, KA = SM::KA, DA = D / 32;
+  constexpr int HU = H / 2;   // hidden units per thread
+  constexpr int DX = D / 2;   // x elements fetched per thread
   extern __shared__ uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int t = blockIdx.y;
   const int64_t item0 = (int64_t)blockIdx.x * kSeq;
   const int64_t S = qd->S;
   if (item0 >= S) return;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t item = item0 + tid;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, half = warp >> 2;
+  const int row = quad * 32 + lane;          // sequence = TMEM lane
+  const int u0 = half * HU;                  // this thread's hidden units
+  const int64_t item = item0 + row;
   const bool live = item < S;
   const int L = g.L;
   const int64_t* __restrict__ idx = qd->idx;
   const float* __restrict__ tab = g.tables + (int64_t)t * g.rows * D;
 
-  // ---- weights -> swizzled K-major B operand; folded biases ----
+  // ---- weights -> swizzled K-major B operand; folded biases; h_0 = 0 ----
   {
     const float* Wih = g.w_ih + (int64_t)t * 3 * H * D;
     const float* Whh = g.w_hh + (int64_t)t * 3 * H * H;
-    for (int e = tid; e < N * (D + H); e += kSeq) {
+    for (int e = tid; e < N * (D + H); e += kThreads) {
       const int n = e / (D + H), k = e - n * (D + H);
       const int gate = n / H, j = n - gate * H;
       float v = 0.f;
@@ -91,16 +104,16 @@ __global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict
     }
     const float* bih = g.b_ih + (int64_t)t * 3 * H;
     const float* bhh = g.b_hh + (int64_t)t * 3 * H;
-    for (int n = tid; n < N; n += kSeq) {
+    for (int n = tid; n < N; n += kThreads) {
       const int gate = n / H, j = n - gate * H;
       sm.bias[n] = gate == 0 ? bih[j] + bhh[j]
                  : gate == 1 ? bih[H + j] + bhh[H + j]
                  : gate == 2 ? bih[2 * H + j] : bhh[2 * H + j];
     }
-    // h_0 = 0
-    for (int a = 0; a < H / 32; ++a)
-      for (int c4 = 0; c4 < 8; ++c4)
-        *reinterpret_cast<float4*>(sm.ah[a] + tid * 128 + c4 * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < HU; j += 4)
+      *reinterpret_cast<float4*>(sm.ah[(u0 + j) >> 5] + sw_off(row, (u0 + j) & 31)) =
+          make_float4(0.f, 0.f, 0.f, 0.f);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -112,53 +125,49 @@ __global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
 
-  // ---- x rows of step l for this thread's sequence ----
-  float4 xn[D / 4];
+  // ---- this thread's half of the x row of step l ----
+  float4 xn[DX / 4];
   auto fetch = [&](int l) {
 #pragma unroll
-    for (int q = 0; q < D / 4; ++q) xn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < DX / 4; ++q) xn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!live) return;
     const int64_t r = __ldg(idx + (item * g.T + t) * L + l);
     if ((uint64_t)r >= (uint64_t)g.rows) {
-      atomicOr(g.err, kErrIndex);
+      if (half == 0) atomicOr(g.err, kErrIndex);
       return;
     }
-    const float4* p = reinterpret_cast<const float4*>(tab + r * D);
+    const float4* p = reinterpret_cast<const float4*>(tab + r * D + half * DX);
 #pragma unroll
-    for (int q = 0; q < D / 4; ++q) xn[q] = ldg_stream(p + q);
+    for (int q = 0; q < DX / 4; ++q) xn[q] = ldg_stream(p + q);
   };
   auto stash = [&](int buf) {
 #pragma unroll
-    for (int q = 0; q < D / 4; ++q)
-      *reinterpret_cast<float4*>(sm.ax[buf][q >> 3] + sw_off(tid, (q & 7) * 4)) = xn[q];
+    for (int q = 0; q < DX / 4; ++q) {
+      const int c = half * DX + 4 * q;
+      *reinterpret_cast<float4*>(sm.ax[buf][c >> 5] + sw_off(row, c & 31)) = xn[q];
+    }
   };
   fetch(0);
   stash(0);
-
-  // AUGRU: ua = W_a^T x_0 for this sequence (kept in registers)
-  float ua[D];
-  float xc[D];
-  if (g.augru) {
-    const float* Wa = g.w_att + (int64_t)t * D * D;
-#pragma unroll
-    for (int c = 0; c < D; ++c) ua[c] = 0.f;
-#pragma unroll
-    for (int q = 0; q < D / 4; ++q) {
-      const float xs[4] = {xn[q].x, xn[q].y, xn[q].z, xn[q].w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = q * 4 + u;
-#pragma unroll
-        for (int c = 0; c < D; ++c) ua[c] = fmaf(xs[u], __ldg(Wa + i * D + c), ua[c]);
-      }
-    }
-  }
 
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = sm.tmem_base;
+
+  // AUGRU: ua = W_a^T x_0 (full row, both threads of the sequence)
+  float ua[D];
+  if (g.augru) {
+    const float* Wa = g.w_att + (int64_t)t * D * D;
+#pragma unroll
+    for (int c = 0; c < D; ++c) ua[c] = 0.f;
+    for (int i = 0; i < D; ++i) {
+      const float xi = *reinterpret_cast<const float*>(sm.ax[0][i >> 5] + sw_off(row, i & 31));
+#pragma unroll
+      for (int c = 0; c < D; ++c) ua[c] = fmaf(xi, __ldg(Wa + i * D + c), ua[c]);
+    }
+  }
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
                          ((uint32_t)(kSeq >> 4) << 24);
 
@@ -184,23 +193,18 @@ __global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict
               s_u32(&sm.mma_done))
           : "memory");
     }
-    // overlap: keep x_l for AUGRU, prefetch x_{l+1}
-    if (g.augru) {
-#pragma unroll
-      for (int q = 0; q < D / 4; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(sm.ax[xb][q >> 3] + sw_off(tid, (q & 7) * 4));
-        xc[4 * q] = v.x; xc[4 * q + 1] = v.y; xc[4 * q + 2] = v.z; xc[4 * q + 3] = v.w;
-      }
-    }
-    if (l + 1 < L) fetch(l + 1);
     float att = 1.f;
-    if (g.augru) {
+    if (g.augru) {  // a_l = sigmoid(<ua, x_l>) from the x row in shared memory
       float sc = 0.f;
 #pragma unroll
-      for (int c = 0; c < D; ++c) sc = fmaf(ua[c], xc[c], sc);
+      for (int c = 0; c < D; c += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(sm.ax[xb][c >> 5] + sw_off(row, c & 31));
+        sc = fmaf(ua[c], v.x, sc); sc = fmaf(ua[c + 1], v.y, sc);
+        sc = fmaf(ua[c + 2], v.z, sc); sc = fmaf(ua[c + 3], v.w, sc);
+      }
       att = sigm(sc);
     }
-    // wait for the gate pre-activations
+    if (l + 1 < L) fetch(l + 1);  // next step's rows fly during the MMA + epilogue
     asm volatile(
         "{\n.reg .pred p;\nW_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -208,9 +212,9 @@ __global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict
         "r"((uint32_t)(l & 1))
         : "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
 #pragma unroll
-    for (int j0 = 0; j0 < H; j0 += 16) {
+    for (int j0 = 0; j0 < HU; j0 += 16) {
       uint32_t v[4][16];
 #pragma unroll
       for (int gte = 0; gte < 4; ++gte) {
@@ -221,13 +225,13 @@ __global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict
               "=r"(v[gte][4]), "=r"(v[gte][5]), "=r"(v[gte][6]), "=r"(v[gte][7]),
               "=r"(v[gte][8]), "=r"(v[gte][9]), "=r"(v[gte][10]), "=r"(v[gte][11]),
               "=r"(v[gte][12]), "=r"(v[gte][13]), "=r"(v[gte][14]), "=r"(v[gte][15])
-            : "r"(lane_base + (uint32_t)(gte * H + j0)));
+            : "r"(lane_base + (uint32_t)(gte * H + u0 + j0)));
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int j = j0 + 4 * q;
-        uint8_t* hp = sm.ah[j >> 5] + sw_off(tid, j & 31);
+        const int j = u0 + j0 + 4 * q;
+        uint8_t* hp = sm.ah[j >> 5] + sw_off(row, j & 31);
         const float4 ho = *reinterpret_cast<const float4*>(hp);
         const float hold[4] = {ho.x, ho.y, ho.z, ho.w};
         float hn[4];
@@ -236,8 +240,8 @@ __global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict
           const int jj = 4 * q + u, jx = j + u;
           const float r = sigm(__uint_as_float(v[0][jj]) + sm.bias[jx]);
           const float z = sigm(__uint_as_float(v[1][jj]) + sm.bias[H + jx]);
-          const float n = tanhf(__uint_as_float(v[2][jj]) + sm.bias[2 * H + jx] +
-                                r * (__uint_as_float(v[3][jj]) + sm.bias[3 * H + jx]));
+          const float n = tanh_fast(__uint_as_float(v[2][jj]) + sm.bias[2 * H + jx] +
+                                    r * (__uint_as_float(v[3][jj]) + sm.bias[3 * H + jx]));
           if (g.augru) {
             const float uu = att * (1.0f - z);
             hn[u] = (1.0f - uu) * hold[u] + uu * n;
@@ -255,11 +259,12 @@ __global__ void __launch_bounds__(kSeq, 1) gru_tc_kernel(const QDesc* __restrict
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   }
 
-  if (live) {  // h_L from this sequence's row of the A operand
-    float* o = g.out + item * g.ld_out + g.col_off + (int64_t)t * H;
+  if (live) {  // h_L (this thread's units) from the A operand
+    float* o = g.out + item * g.ld_out + g.col_off + (int64_t)t * H + u0;
 #pragma unroll
-    for (int j = 0; j < H; j += 4) {
-      const float4 h = *reinterpret_cast<const float4*>(sm.ah[j >> 5] + sw_off(tid, j & 31));
+    for (int j = 0; j < HU; j += 4) {
+      const int jx = u0 + j;
+      const float4 h = *reinterpret_cast<const float4*>(sm.ah[jx >> 5] + sw_off(row, jx & 31));
       o[j] = h.x; o[j + 1] = h.y; o[j + 2] = h.z; o[j + 3] = h.w;
     }
   }
@@ -277,7 +282,7 @@ void launch_typed(const QDesc* qd, const GruArgs& g, int64_t max_items, cudaStre
                          (int)smem);
   });
   const dim3 grid((unsigned)((max_items + kSeq - 1) / kSeq), g.T);
-  gru_tc_kernel<D, H><<<grid, kSeq, smem, s>>>(qd, g);
+  gru_tc_kernel<D, H><<<grid, kThreads, smem, s>>>(qd, g);
 }
 
 }  // namespace
