@@ -125,12 +125,14 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
 
-  // ---- this thread's half of the x row of step l ----
-  float4 xn[DX / 4];
-  auto fetch = [&](int l) {
+  // ---- this thread's half of the x row of step l (two steps of lookahead:
+  // a random HBM row per sequence per step is the recurrence's only memory
+  // traffic, so its latency must hide behind two MMA + epilogue rounds) ----
+  float4 xa[DX / 4], xb2[DX / 4];
+  auto fetch = [&](int l, float4* xn) {
 #pragma unroll
     for (int q = 0; q < DX / 4; ++q) xn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!live) return;
+    if (!live || l >= L) return;
     const int64_t r = __ldg(idx + (item * g.T + t) * L + l);
     if ((uint64_t)r >= (uint64_t)g.rows) {
       if (half == 0) atomicOr(g.err, kErrIndex);
@@ -140,15 +142,16 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
 #pragma unroll
     for (int q = 0; q < DX / 4; ++q) xn[q] = ldg_stream(p + q);
   };
-  auto stash = [&](int buf) {
+  auto stash = [&](int buf, const float4* xn) {
 #pragma unroll
     for (int q = 0; q < DX / 4; ++q) {
       const int c = half * DX + 4 * q;
       *reinterpret_cast<float4*>(sm.ax[buf][c >> 5] + sw_off(row, c & 31)) = xn[q];
     }
   };
-  fetch(0);
-  stash(0);
+  fetch(0, xa);
+  stash(0, xa);
+  fetch(1, xa);
 
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -204,7 +207,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
       }
       att = sigm(sc);
     }
-    if (l + 1 < L) fetch(l + 1);  // next step's rows fly during the MMA + epilogue
+    fetch(l + 2, xb2);  // rows two steps ahead fly during this MMA + epilogue
     asm volatile(
         "{\n.reg .pred p;\nW_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -252,7 +255,9 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
         *reinterpret_cast<float4*>(hp) = make_float4(hn[0], hn[1], hn[2], hn[3]);
       }
     }
-    if (l + 1 < L) stash(xb ^ 1);
+    if (l + 1 < L) stash(xb ^ 1, xa);
+#pragma unroll
+    for (int q = 0; q < DX / 4; ++q) xa[q] = xb2[q];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
