@@ -68,8 +68,10 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   constexpr int N = SM::N, KA = SM::KA, DA = D / 32;
   constexpr int HU = H / 2;   // hidden units per thread
   constexpr int DX = D / 2;   // x elements fetched per thread
-  extern __shared__ uint8_t smem_raw[];
-  SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // align by offsetting smem_raw itself (not through an integer round trip) so
+  // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+  SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u));
   const int t = blockIdx.y;
   const int64_t item0 = (int64_t)blockIdx.x * kSeq;
   const int64_t S = qd->S;
