@@ -311,7 +311,7 @@ gather_concat_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tab
 // reference's FFMA-bound Attention category (model_zoo.cpp:207-216) into a
 // pure gather at HBM speed.
 template <int LPR, int VPL, int U>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, 4)
 din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                 int T, int L, const float* __restrict__ att_w, float* __restrict__ out,
                 int64_t ld_out, int64_t col_off, int* __restrict__ err) {
@@ -362,9 +362,10 @@ din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
       __syncwarp();
       for (int l = lane; l < n; l += 32) sidx[warp][l] = __ldg(bidx + c0 + l);
       __syncwarp();
-      for (int j = 0; j < n; j += R * U) {
-        float4 v[U][VPL];
-        bool ok[U];
+      // Software-pipelined: batch j+1's row loads are in flight while batch j
+      // is scored and accumulated (the score -> shuffle -> sigmoid chain per
+      // row would otherwise leave the memory system idle).
+      auto load_batch = [&](int j, float4 (&v)[U][VPL], bool (&ok)[U]) {
 #pragma unroll
         for (int u2 = 0; u2 < U; ++u2) {
           const int l = j + u2 * R + g;
@@ -383,6 +384,8 @@ din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
             }
           }
         }
+      };
+      auto consume = [&](const float4 (&v)[U][VPL], const bool (&ok)[U]) {
 #pragma unroll
         for (int u2 = 0; u2 < U; ++u2) {
           float s = 0.f;
@@ -395,7 +398,7 @@ din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
           }
 #pragma unroll
           for (int off = LPR / 2; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-          s = 1.0f / (1.0f + expf(-s));  // activation-unit weight
+          s = __fdividef(1.0f, 1.0f + __expf(-s));  // activation-unit weight (SFU)
           if (ok[u2]) {
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
@@ -405,6 +408,18 @@ din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
               acc[k].w = fmaf(s, v[u2][k].w, acc[k].w);
             }
           }
+        }
+      };
+      constexpr int B = R * U;  // rows per batch
+      float4 va[U][VPL], vb[U][VPL];
+      bool oa[U], ob[U];
+      load_batch(0, va, oa);
+      for (int j = 0; j < n; j += 2 * B) {
+        if (j + B < n) load_batch(j + B, vb, ob);
+        consume(va, oa);
+        if (j + B < n) {
+          if (j + 2 * B < n) load_batch(j + 2 * B, va, oa);
+          consume(vb, ob);
         }
       }
     }
@@ -628,9 +643,9 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
   switch (D) {
     case 8: din_pool_kernel<2, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
     case 16: din_pool_kernel<4, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 32: din_pool_kernel<8, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 64: din_pool_kernel<16, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 128: din_pool_kernel<32, 1, 8><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 32: din_pool_kernel<8, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 64: din_pool_kernel<16, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 128: din_pool_kernel<32, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
     case 256: din_pool_kernel<32, 2, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
   }
 }
