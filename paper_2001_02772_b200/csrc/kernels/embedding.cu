@@ -245,6 +245,96 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
   }
 }
 
+// Variant 2 (RS_SLS_VARIANT=2): warp-per-bag with the two serial latencies of
+// a bag hidden — the NEXT bag's index list is loaded into registers while this
+// bag's rows stream, and row batch j+1 is in flight while batch j accumulates.
+// Same per-lane accumulation order as sls_sum_kernel (bit-identical results).
+// Bags of up to 32*IPL lookups; longer bags use sls_sum_kernel.
+template <int LPR, int VPL, int U, int IPL>
+__global__ void __launch_bounds__(kWarps * 32)
+sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
+                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err) {
+  pdl_trigger();
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  constexpr int B = R * U;  // rows per batch
+  __shared__ int64_t sidx[kWarps][32 * IPL];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t bags = qd->S * T;
+  const int64_t* __restrict__ idx = qd->idx;
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  int64_t nidx[IPL];
+  auto fetch_idx = [&](int64_t bag) {
+#pragma unroll
+    for (int q = 0; q < IPL; ++q) {
+      const int l = q * 32 + lane;
+      nidx[q] = (bag < bags && l < L) ? __ldg(idx + bag * L + l) : 0;
+    }
+  };
+  int64_t bag = (int64_t)blockIdx.x * kWarps + warp;
+  fetch_idx(bag);
+  for (; bag < bags; bag += stride) {
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < IPL; ++q) sidx[warp][q * 32 + lane] = nidx[q];
+    __syncwarp();
+    fetch_idx(bag + stride);  // next bag's indices fly with this bag's rows
+    const int t = (int)(bag % T);
+    const float4* __restrict__ tab =
+        reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
+    auto load_batch = [&](int j, float4 (&v)[U][VPL], bool (&ok)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int l = j + u * R + g;
+        ok[u] = false;
+        if (l < L) {
+          const int64_t r = sidx[warp][l];
+          if ((uint64_t)r < (uint64_t)rows) {
+            ok[u] = true;
+            const float4* p = tab + r * (D / 4) + c;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream(p + k * LPR);
+          } else {
+            atomicOr(err, kErrIndex);
+          }
+        }
+      }
+    };
+    float4 acc[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto consume = [&](const float4 (&v)[U][VPL], const bool (&ok)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) add4(acc[k], v[u][k]);
+        }
+    };
+    float4 va[U][VPL], vb[U][VPL];
+    bool oa[U], ob[U];
+    load_batch(0, va, oa);
+    for (int j = 0; j < L; j += 2 * B) {
+      if (j + B < L) load_batch(j + B, vb, ob);
+      consume(va, oa);
+      if (j + B < L) {
+        if (j + 2 * B < L) load_batch(j + 2 * B, va, oa);
+        consume(vb, ob);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) add4(acc[k], shfl_xor4(acc[k], off));
+    if (g == 0) {
+      float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
+    }
+  }
+}
+
 // Any D (not a power of two in [8,256]): lane-per-column, sequential in l.
 __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_scalar_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
@@ -554,10 +644,45 @@ int grid_for(int64_t units, int per_block, int sm_count, int blocks_per_sm) {
 bool sls_vector_path(int64_t D) { return pow2_dim(D); }
 
 
-// RS_SLS_VARIANT: 0 (default) warp-per-bag register gather, 1 TMA gather4.
+// RS_SLS_VARIANT: 0 (default) warp-per-bag register gather, 1 TMA gather4,
+// 2 pipelined warp-per-bag (RS_SLS_UB = rows-per-batch unroll, 4 or 8).
 int sls_variant() {
   const char* v = getenv("RS_SLS_VARIANT");
   return v ? atoi(v) : 0;
+}
+int sls_ub() {
+  const char* v = getenv("RS_SLS_UB");
+  return v ? atoi(v) : 4;
+}
+
+template <int LPR, int VPL, int U, int IPL>
+void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                     float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                     cudaStream_t s) {
+  static const int per_sm = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_pipe_kernel<LPR, VPL, U, IPL>,
+                                                  kWarps * 32, 0);
+    return b > 0 ? b : 1;
+  }();
+  const int grid = grid_for(max_items * T, kWarps, sm_count, 2 * per_sm);
+  sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out,
+                                                                 ld_out, err);
+}
+
+template <int LPR, int VPL>
+bool try_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L, float* out,
+                  int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s) {
+  if (L > 96) return false;
+  const bool u8 = sls_ub() >= 8;
+  if (L <= 32) {
+    if (u8) launch_sls_pipe<LPR, VPL, (VPL == 2 ? 4 : 8), 1>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
+    else launch_sls_pipe<LPR, VPL, (VPL == 2 ? 2 : 4), 1>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
+  } else {
+    if (u8) launch_sls_pipe<LPR, VPL, (VPL == 2 ? 4 : 8), 3>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
+    else launch_sls_pipe<LPR, VPL, (VPL == 2 ? 2 : 4), 3>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
+  }
+  return true;
 }
 
 template <int LPR, int VPL, int U>
@@ -603,6 +728,9 @@ void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, i
     if (sls_variant() == 1 && launch_sls_tma<LPR, VPL, 2>(qd, tables, rows, T, L, out,      \
                                                           ld_out, err, max_items, sm_count, \
                                                           s))                               \
+      break;                                                                                \
+    if (sls_variant() == 2 && try_sls_pipe<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,   \
+                                                     err, max_items, sm_count, s))          \
       break;                                                                                \
     launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
                                                  max_items, sm_count, s);                   \
