@@ -644,11 +644,12 @@ int grid_for(int64_t units, int per_block, int sm_count, int blocks_per_sm) {
 bool sls_vector_path(int64_t D) { return pow2_dim(D); }
 
 
-// RS_SLS_VARIANT: 0 (default) warp-per-bag register gather, 1 TMA gather4,
-// 2 pipelined warp-per-bag (RS_SLS_UB = rows-per-batch unroll, 4 or 8).
+// RS_SLS_VARIANT: 2 (default) pipelined warp-per-bag (RS_SLS_UB = rows-per-
+// batch unroll, 4 or 8; bags up to 96 lookups, else variant 0), 0 warp-per-bag
+// register gather, 1 TMA gather4. All three are bit-identical.
 int sls_variant() {
   const char* v = getenv("RS_SLS_VARIANT");
-  return v ? atoi(v) : 0;
+  return v ? atoi(v) : 2;
 }
 int sls_ub() {
   const char* v = getenv("RS_SLS_UB");
