@@ -132,6 +132,9 @@ def aggregate(per_rank_qps: float, per_rank_time: float, queries: int, world: in
 
 # ---- clocks ------------------------------------------------------------------
 class ClockSampler:
+    """nvidia-smi clocks/throttle sampler. Started before the warm-up (the tool
+    needs ~0.5 s to produce its first sample); summary() keeps the samples
+    whose host arrival time falls inside the timed window."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -141,22 +144,26 @@ class ClockSampler:
         self.proc = None
         self.lines = []
         self._t = None
+        self.window = (0.0, float("inf"))
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["stdbuf", "-oL", "nvidia-smi", "-i", str(self.dev),
+                 f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except OSError:
             self.proc = None
         return self
 
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc:
@@ -171,7 +178,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = self.window
+        # 20 ms sampling: allow one period of slack on each side of the window
+        inside = [ln for ts, ln in self.lines if t0 - 0.03 <= ts <= t1 + 0.03]
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -320,18 +330,20 @@ def run_ours(args, rank, world, local):
         return acc.forward_many(None, stream=sp, timed=True, residence=True, prepared=batch)
 
     def timed(host):
-        serve(prepare(W, host))                  # warm-up (untimed), synchronous
-        batch = prepare(K, host)
-        torch.cuda.synchronize(device)
-        barrier(device)
-        torch.cuda.synchronize(device)
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk:
+        with ClockSampler(local) as clk:         # started before warm-up (tool start-up)
+            serve(prepare(W, host))              # warm-up (untimed), synchronous
+            batch = prepare(K, host)
+            torch.cuda.synchronize(device)
+            barrier(device)
+            torch.cuda.synchronize(device)
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            t0 = time.time()
             start.record(stream)
             svc_ms, res_ms = serve(batch)        # per-query CUDA-event times
             end.record(stream)
             torch.cuda.synchronize(device)
+            clk.mark(t0, time.time())
         barrier(device)
         torch.cuda.synchronize(device)
         total_s = start.elapsed_time(end) * 1e-3
@@ -377,11 +389,23 @@ def run_ours(args, rank, world, local):
                                   for q in window(k)) for k in range(K)]))
     d2h_step = float(np.mean([sum(int(sizes[q]) * acc.output_dim * 4 + 4 for q in window(k))
                               for k in range(K)]))
-    traffic = None
+    # kernel nodes of the graph each timed query launched (pick_graph in
+    # csrc/host/accel.cu: FC_AUTO takes the tcgen05 graph at >= 128 items)
+    kl, ks = acc.info.kernels_per_forward, acc.info.kernels_per_forward_small
+    launches = int(sum((kl if (ks == 0 or (int(sizes[q]) >= 128 and kl != ks)) else ks)
+                       for k in range(K) for q in window(k)))
+    # DRAM traffic per launch from the committed ncu --set full capture
+    # (profiles/sls_traffic.json: dram read+write bytes / items of that launch),
+    # scaled to this run's mean items per roofline launch like `achieved`
+    n_roof = len(window(0))
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "sls_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("bytes_per_item")
+            tj = json.load(f).get(args.workload)
+        if tj:
+            traffic = tj["dram_bytes_per_item"] * sls_bytes / sls_bytes_per_item(spec) / n_roof
+            traffic_src = tj.get("source")
     if rank == 0:
         line = {
             "metric": METRIC, "value": agg["value"], "unit": "queries/s", "n_gpus": world,
@@ -410,21 +434,25 @@ def run_ours(args, rank, world, local):
                     "p95_ms": r_host.p95 * 1e3, "saturated_qps": agg_e2e["saturated_qps"],
                     "h2d_gbs": h2d_step * K / max(t_host, 1e-9) / 1e9},
             "roofline": {"bound": "hbm",
-                         "kernel": {"Sum": "sls_sum_kernel", "Concat": "gather_concat_kernel",
+                         "kernel": {"Sum": "sls_pipe_kernel", "Concat": "gather_concat_kernel",
                                     "AttentionFC": "din_pool_kernel",
                                     "AttentionRNN": "gru_kernel (FFMA-bound; bytes shown)"}[
                                         e.pooling],
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
-                         "traffic": traffic,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": sls_bytes / n_roof,
                          "algorithmic_bytes_per_item": sls_bytes_per_item(spec),
                          "kernel_share_of_step": (sls_ms * 1e-3) / max(t_dev / K, 1e-12)},
-            "gpu_launches": acc.info.kernels_per_forward * K * Q,
+            "gpu_launches": launches,
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(spec, sizes, os.cpu_count() or 1)
+            _, cpu_sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
+                math.log(300), 0.5), 8192)
+            line["cpu_baseline"] = cpu_baseline(spec, np.minimum(cpu_sizes, args.max_query),
+                                                os.cpu_count() or 1)
         print(json.dumps(line), flush=True)
     acc.close()
     if world > 1:
@@ -435,14 +463,14 @@ def run_ours(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg3-rmc2",
                     help="cfg3-rmc2 (default) | cfg3-rmc3 | cfg1-rmc1 | cfg5-dien | cfg5-din | "
                          "ncf | wnd | mt-wnd | rmc1 | rmc2 | rmc3 | din | dien")
     ap.add_argument("--sla", type=float, default=0.0, help="override SLA seconds")
-    ap.add_argument("--queries-per-step", type=int, default=128)
+    ap.add_argument("--queries-per-step", type=int, default=256)
     ap.add_argument("--max-query", type=int, default=1000)
     ap.add_argument("--fc", choices=["fp32", "tf32", "auto"], default="auto")
     ap.add_argument("--no-cpu", action="store_true")

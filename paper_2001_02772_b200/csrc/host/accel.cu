@@ -13,8 +13,15 @@
 //  * a call = async H2D of the query's dense features and indices (pinned
 //    host memory) + 16-byte descriptor update + cudaGraphLaunch + async D2H
 //    of the logits and the error word, all on the caller's stream.
+//  * the descriptor update is two 64-bit stream memory writes whose VALUES
+//    are taken at enqueue time (cuStreamBatchMemOp), so the host may run any
+//    number of queries ahead of the GPU without a host-side ring to recycle.
+#include <cuda.h>
+
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -40,6 +47,20 @@ namespace {
 
 constexpr int kDescRing = 256;
 
+using BatchMemOpFn = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+
+BatchMemOpFn batch_memop_fn() {
+  static BatchMemOpFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<BatchMemOpFn>(p);
+  }();
+  return fn;
+}
+
 struct FcLayer {
   int64_t in = 0, out = 0, ldk = 0;
   int relu = 0;
@@ -51,8 +72,6 @@ struct FcLayer {
 struct Slot {
   cudaStream_t cap = nullptr;  // capture stream
   QDesc* d_q = nullptr;
-  QDesc* h_q = nullptr;        // pinned ring [kDescRing]
-  int ring = 0;
   int* d_err = nullptr;
   int* h_err = nullptr;        // pinned ring [kDescRing]
   float* dense_stage = nullptr;
@@ -110,6 +129,7 @@ struct rs_accel {
   std::mutex many_mu;
   std::vector<cudaEvent_t> evpool, evstart;
   std::map<int64_t, double> service_memo;
+  rs::BatchMemOpFn memops = nullptr;  // null: pageable-copy descriptor writes
 };
 
 namespace rs {
@@ -419,8 +439,6 @@ std::unique_ptr<Slot> make_slot(rs_accel* a) {
   const int64_t maxS = a->init.max_query_size;
   RS_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
   s->d_q = static_cast<QDesc*>(dmalloc(a, s->allocs, sizeof(QDesc)));
-  RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_q), sizeof(QDesc) * kDescRing,
-                        cudaHostAllocPortable));
   RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_err), sizeof(int) * kDescRing,
                         cudaHostAllocPortable));
   std::memset(s->h_err, 0, sizeof(int) * kDescRing);
@@ -484,7 +502,6 @@ void free_slot(Slot* s) {
   if (s->ready) cudaEventDestroy(s->ready);
   if (s->free) cudaEventDestroy(s->free);
   for (void* p : s->allocs) cudaFree(p);
-  if (s->h_q) cudaFreeHost(s->h_q);
   if (s->h_err) cudaFreeHost(s->h_err);
   if (s->cap) cudaStreamDestroy(s->cap);
   if (s->cap2) cudaStreamDestroy(s->cap2);
@@ -511,6 +528,55 @@ void check_query(rs_accel* a, const rs_query* q) {
 // bottom-MLP staging buffer (or straight into X[:, 0:dense_in] when there is
 // no dense stack), indices into the slot's staging buffer (host) or by
 // pointer (device), then the 16-byte device descriptor.
+// Descriptor update by value: two 64-bit stream writes (front-end ops, no copy
+// engine); the fallback, a copy from a pageable stack object, also consumes
+// the source before returning.
+void write_desc(rs_accel* a, Slot* s, int64_t S, const int64_t* idx, cudaStream_t st) {
+  if (a->memops) {
+    CUstreamBatchMemOpParams ops[2];
+    std::memset(ops, 0, sizeof(ops));
+    for (int k = 0; k < 2; ++k) {
+      ops[k].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+      ops[k].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    }
+    ops[0].writeValue.address = reinterpret_cast<CUdeviceptr>(&s->d_q->S);
+    ops[0].writeValue.value64 = (cuuint64_t)S;
+    ops[1].writeValue.address = reinterpret_cast<CUdeviceptr>(&s->d_q->idx);
+    ops[1].writeValue.value64 = (cuuint64_t)reinterpret_cast<uintptr_t>(idx);
+    if (a->memops(reinterpret_cast<CUstream>(st), 2, ops, 0) != CUDA_SUCCESS)
+      raise(RS_E_CUDA, "cuStreamBatchMemOp failed");
+    return;
+  }
+  QDesc v;
+  v.S = S;
+  v.idx = idx;
+  RS_CUDA(cudaMemcpyAsync(s->d_q, &v, sizeof(QDesc), cudaMemcpyHostToDevice, st));
+}
+
+// Stream memory writes are used only if a test write lands (RS_DESC_COPY=1
+// forces the copy path).
+BatchMemOpFn probe_memops(rs_accel* a) {
+  BatchMemOpFn fn = batch_memop_fn();
+  const char* force = getenv("RS_DESC_COPY");
+  if (!fn || (force && atoi(force))) return nullptr;
+  uint64_t* d = nullptr;
+  if (cudaMalloc(&d, 8) != cudaSuccess) return nullptr;
+  CUstreamBatchMemOpParams op;
+  std::memset(&op, 0, sizeof(op));
+  op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+  op.writeValue.address = reinterpret_cast<CUdeviceptr>(d);
+  op.writeValue.value64 = 0x5eed5eed12345678ull;
+  op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+  uint64_t h = 0;
+  const bool ok = cudaMemsetAsync(d, 0, 8, a->own) == cudaSuccess &&
+                  fn(reinterpret_cast<CUstream>(a->own), 1, &op, 0) == CUDA_SUCCESS &&
+                  cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, a->own) == cudaSuccess &&
+                  cudaStreamSynchronize(a->own) == cudaSuccess && h == 0x5eed5eed12345678ull;
+  cudaFree(d);
+  (void)cudaGetLastError();
+  return ok ? fn : nullptr;
+}
+
 void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream_t st) {
   const int64_t S = q->size;
   const bool host = q->location == RS_MEM_HOST;
@@ -546,11 +612,7 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
       idx = q->indices;
     }
   }
-  const int r = s->ring;
-  s->ring = (s->ring + 1) % kDescRing;
-  s->h_q[r].S = S;
-  s->h_q[r].idx = idx;
-  RS_CUDA(cudaMemcpyAsync(s->d_q, &s->h_q[r], sizeof(QDesc), cudaMemcpyHostToDevice, st));
+  write_desc(a, s, S, idx, st);
 }
 
 cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full) {
@@ -631,21 +693,32 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->own;
     std::lock_guard<std::mutex> many_lock(a->many_mu);
     if (latency_ms && !service_ms) raise(RS_E_INVALID, "latency_ms needs service_ms");
+    // Per-query completion (and staging-start) events live in a fixed ring:
+    // when the ring wraps, the host harvests the oldest query's timestamps
+    // (it completed long ago unless the GPU is kEvRing queries behind), so no
+    // event is created inside a serving call after the first one.
+    constexpr int64_t kEvRing = 4096;
+    std::vector<double> t_done, t_start;
     if (service_ms) {
-      // event pools grow in 4096-event chunks so a timed call after a
-      // warm-up call does not pay event creation
-      auto grow = [](std::vector<cudaEvent_t>& pool, int64_t need) {
-        const int64_t target = (need + 4095) / 4096 * 4096;
-        while ((int64_t)pool.size() < target) {
+      auto fill = [](std::vector<cudaEvent_t>& pool, int64_t need) {
+        while ((int64_t)pool.size() < need) {
           cudaEvent_t e;
           RS_CUDA(cudaEventCreate(&e));
           pool.push_back(e);
         }
       };
-      grow(a->evpool, n + 1);
-      if (latency_ms) grow(a->evstart, n);
+      fill(a->evpool, kEvRing + 1);
+      if (latency_ms) fill(a->evstart, kEvRing);
+      t_done.resize(n);
+      if (latency_ms) t_start.resize(n);
       RS_CUDA(cudaEventRecord(a->evpool[0], st));
     }
+    auto harvest = [&](int64_t j) {
+      cudaEvent_t e = a->evpool[1 + j % kEvRing];
+      RS_CUDA(cudaEventSynchronize(e));
+      t_done[j] = elapsed(a->evpool[0], e);
+      if (latency_ms) t_start[j] = elapsed(a->evpool[0], a->evstart[j % kEvRing]);
+    };
     // Queries are dispatched in FIFO order round-robin over `depth` lanes
     // (compute stream + scratch slot each), so query i+1's embedding gather
     // overlaps query i's latency-bound FC tail. Host inputs are staged by one
@@ -657,39 +730,52 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     RS_CUDA(cudaEventRecord(a->copy_gate, st));
     for (int d = 0; d < depth; ++d) RS_CUDA(cudaStreamWaitEvent(a->lane[d], a->copy_gate, 0));
     if (loc == RS_MEM_HOST) RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
+    const auto host_t0 = std::chrono::steady_clock::now();
     for (int64_t i = 0; i < n; ++i) {
       const int d = (int)(i % depth);
       Slot* s = p[d];
       cudaStream_t ls = a->lane[d];
+      if (service_ms && i >= kEvRing) harvest(i - kEvRing);
+      cudaEvent_t ev_start = latency_ms ? a->evstart[i % kEvRing] : nullptr;
       if (loc == RS_MEM_HOST) {
         RS_CUDA(cudaStreamWaitEvent(a->copy, s->free, 0));
-        if (latency_ms) RS_CUDA(cudaEventRecord(a->evstart[i], a->copy));
+        if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, a->copy));
         stage_inputs(a, s, &qs[i], true, a->copy);
         RS_CUDA(cudaEventRecord(s->ready, a->copy));
         RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
       } else {
-        if (latency_ms) RS_CUDA(cudaEventRecord(a->evstart[i], ls));
+        if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, ls));
         stage_inputs(a, s, &qs[i], true, ls);
       }
       launch_stage(a, s, &qs[i], outs[i], true, ls);
       RS_CUDA(cudaEventRecord(s->free, ls));
-      if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[i + 1], ls));
+      if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[1 + i % kEvRing], ls));
     }
     for (int d = 0; d < depth; ++d) {
       RS_CUDA(cudaEventRecord(a->lane_join[d], a->lane[d]));
       RS_CUDA(cudaStreamWaitEvent(st, a->lane_join[d], 0));
     }
+    if (const char* tr = getenv("RS_TRACE_ENQUEUE")) {
+      if (atoi(tr))
+        fprintf(stderr, "rs_forward_many: n=%lld enqueue %.3f ms (%.2f us/query)\n",
+                (long long)n,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                          host_t0).count(),
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() -
+                                                          host_t0).count() / (double)n);
+    }
     if (service_ms) {
       RS_CUDA(cudaStreamSynchronize(st));
+      for (int64_t j = std::max<int64_t>(0, n - kEvRing); j < n; ++j) harvest(j);
       // Deliveries are in FIFO order: query i is delivered when it and every
       // earlier query completed; service = gap between deliveries.
       double prev = 0;
       for (int64_t i = 0; i < n; ++i) {
-        const double done = std::max(prev, (double)elapsed(a->evpool[0], a->evpool[i + 1]));
+        const double done = std::max(prev, t_done[i]);
         service_ms[i] = done - prev;
         prev = done;
         // residence in the accelerator: input staging start -> completion
-        if (latency_ms) latency_ms[i] = elapsed(a->evstart[i], a->evpool[i + 1]);
+        if (latency_ms) latency_ms[i] = t_done[i] - t_start[i];
       }
       for (int d = 0; d < depth; ++d) collect_errors(p[d], st);
     }
@@ -762,6 +848,7 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     RS_CUDA(cudaStreamCreateWithFlags(&a->own, cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&a->copy_gate, cudaEventDisableTiming));
     build_model(a);
+    a->memops = probe_memops(a);
     *out = a;
   });
   if (rc != RS_OK && a) {

@@ -335,6 +335,122 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
   }
 }
 
+// Variant 3 (RS_SLS_VARIANT=3): warp-per-bag with whole bags staged in shared
+// memory by cp.async. A warp issues 16-byte cp.async copies for EVERY row of
+// its next bag (nbuf-1 bags ahead) before it sums the current one, so a bag's
+// rows are all in flight at once and memory-level parallelism costs shared
+// memory instead of registers. That shortens the kernel's ramp and tail: the
+// last bags of a launch complete in about one memory latency instead of
+// L/(rows in flight) latencies. Rows with an out-of-range index are zero-filled
+// (acc + 0.0f is exact: the accumulator starts at +0 and can never become -0),
+// and are flagged in the error word. Summation order per lane is the one of
+// sls_sum_kernel (rows g, g+R, g+2R, ...; then the xor tree): bit-identical.
+template <int LPR, int VPL, int IPL>
+__global__ void __launch_bounds__(512)
+sls_stage_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
+                 int T, int L, int nbuf, float* __restrict__ out, int64_t ld_out,
+                 int* __restrict__ err) {
+  pdl_trigger();
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  constexpr int C4 = D / 4;  // 16-byte chunks per row
+  extern __shared__ __align__(16) float4 sbuf[];  // [warps][nbuf][L][C4]
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t bags = qd->S * T;
+  const int64_t* __restrict__ idx = qd->idx;
+  const int64_t stride = (int64_t)gridDim.x * nw;
+  const int64_t first = (int64_t)blockIdx.x * nw + warp;
+  float4* wbuf = sbuf + (size_t)warp * nbuf * L * C4;
+  int64_t nidx[IPL];
+  auto fetch_idx = [&](int64_t bag) {
+#pragma unroll
+    for (int q = 0; q < IPL; ++q) {
+      const int l = q * 32 + lane;
+      nidx[q] = (bag < bags && l < L) ? __ldg(idx + bag * L + l) : 0;
+    }
+  };
+  // copy bag `bag`'s rows into stage st (indices in nidx)
+  auto issue = [&](int64_t bag, int st) {
+    const int t = (int)(bag % T);
+    const float4* __restrict__ tab = reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
+    float4* dst = wbuf + (size_t)st * L * C4;
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < IPL; ++q) {
+#pragma unroll
+      for (int i = 0; i < 32 / R; ++i) {
+        const int src = i * R + g;
+        const int64_t r = __shfl_sync(0xffffffffu, nidx[q], src);
+        const int l = q * 32 + src;
+        if (l < L) {
+          float4* d = dst + (size_t)l * C4 + c;
+          if ((uint64_t)r < (uint64_t)rows) {
+            const float4* p = tab + r * C4 + c;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(d + k * LPR)),
+                           "l"(p + k * LPR)
+                           : "memory");
+          } else {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) d[k * LPR] = make_float4(0.f, 0.f, 0.f, 0.f);
+            bad = true;
+          }
+        }
+      }
+    }
+    if (bad) atomicOr(err, kErrIndex);
+  };
+  int64_t bag = first;
+  fetch_idx(bag);
+  for (int s = 0; s < nbuf - 1; ++s) {
+    const int64_t b = first + s * stride;
+    if (b < bags) {
+      issue(b, s);
+      fetch_idx(b + stride);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int64_t k = 0; bag < bags; ++k, bag += stride) {
+    const int64_t ahead = bag + (int64_t)(nbuf - 1) * stride;
+    if (ahead < bags) {
+      issue(ahead, (int)((k + nbuf - 1) % nbuf));
+      fetch_idx(ahead + stride);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // groups complete in order: all but the newest nbuf-1 are done -> bag k landed
+    switch (nbuf) {
+      case 2: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+      case 3: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+      default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    }
+    __syncwarp();
+    const float4* src = wbuf + (size_t)(k % nbuf) * L * C4;
+    float4 acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int l = g; l < L; l += R) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) add4(acc[q], src[(size_t)l * C4 + c + q * LPR]);
+    }
+#pragma unroll
+    for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], off));
+    if (g == 0) {
+      const int t = (int)(bag % T);
+      float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) o[q * LPR] = acc[q];
+    }
+    __syncwarp();  // stage k % nbuf is refilled by the next iteration's issue
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Any D (not a power of two in [8,256]): lane-per-column, sequential in l.
 __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_scalar_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
@@ -686,6 +802,53 @@ bool try_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int
   return true;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// Variant 3 geometry: one CTA per SM, each warp owning nbuf bag stages
+// (RS_SLS_NBUF, 2..4, default 2) of L*D*4 bytes; as many warps as fit in
+// RS_SLS_SMEM_KB (default 200) of shared memory, at most 16 (RS_SLS_WARPS caps).
+template <int LPR, int VPL, int IPL>
+bool launch_sls_stage(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                      float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                      cudaStream_t s) {
+  constexpr int D = LPR * 4 * VPL;
+  const int nbuf = std::min(4, std::max(2, env_int("RS_SLS_NBUF", 2)));
+  const size_t per_warp = (size_t)nbuf * L * D * 4;
+  const size_t budget = (size_t)env_int("RS_SLS_SMEM_KB", 200) * 1024;
+  int nw = (int)std::min<size_t>(16, budget / std::max<size_t>(per_warp, 1));
+  nw = std::min(nw, env_int("RS_SLS_WARPS", 16));
+  if (nw < 1) return false;
+  const size_t smem = per_warp * nw;
+  static bool attr = [] {
+    return cudaFuncSetAttribute(sls_stage_kernel<LPR, VPL, IPL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
+           cudaSuccess;
+  }();
+  if (!attr) return false;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sls_stage_kernel<LPR, VPL, IPL>, nw * 32,
+                                                smem);
+  if (per_sm < 1) return false;
+  const int grid = grid_for(max_items * T, nw, sm_count, per_sm);
+  sls_stage_kernel<LPR, VPL, IPL><<<grid, nw * 32, smem, s>>>(qd, tables, rows, T, L, nbuf, out,
+                                                              ld_out, err);
+  return true;
+}
+
+template <int LPR, int VPL>
+bool try_sls_stage(const QDesc* qd, const float* tables, int64_t rows, int T, int L, float* out,
+                   int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s) {
+  if (L > 96) return false;
+  if (L <= 32)
+    return launch_sls_stage<LPR, VPL, 1>(qd, tables, rows, T, L, out, ld_out, err, max_items,
+                                         sm_count, s);
+  return launch_sls_stage<LPR, VPL, 3>(qd, tables, rows, T, L, out, ld_out, err, max_items,
+                                       sm_count, s);
+}
+
 template <int LPR, int VPL, int U>
 void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                     float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
@@ -732,6 +895,9 @@ void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, i
       break;                                                                                \
     if (sls_variant() == 2 && try_sls_pipe<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,   \
                                                      err, max_items, sm_count, s))          \
+      break;                                                                                \
+    if (sls_variant() == 3 && try_sls_stage<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,  \
+                                                      err, max_items, sm_count, s))         \
       break;                                                                                \
     launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
                                                  max_items, sm_count, s);                   \

@@ -229,3 +229,52 @@ def test_dien_tensor_core_recurrence(augru, L):
     for S in (5, 200):
         check_forward(spec, rows=50000, S=S, fc_mode=rs.FC_TF32, augru=augru, tol=TF32_TOL,
                       max_q=256)
+
+
+@pytest.mark.parametrize("desc_copy", ["0", "1"])
+def test_forward_many_long_batch_host_runs_ahead(desc_copy, monkeypatch):
+    """2000 small queries over 2 lanes: the host enqueues far ahead of the GPU,
+    so every query must carry its own descriptor (item count, index pointer)
+    by value — stream memory writes, or the pageable-copy fallback."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("RS_DESC_COPY", desc_copy)
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 5000
+    acc = rs.Accelerator(spec, rows, seed=4, max_query_size=64, fc_mode=rs.FC_FP32,
+                         queue_depth=2)
+    rng = np.random.default_rng(0)
+    sizes = [int(s) for s in rng.integers(1, 65, size=2000)]
+    pool = [rs.fill_query(spec, rows, 9, q, 64) for q in range(16)]
+    dd = [torch.from_numpy(d).cuda() for d, _ in pool]
+    di = [torch.from_numpy(i).cuda() for _, i in pool]
+    outs = torch.zeros((len(sizes), 64, acc.output_dim), device="cuda")
+    acc.forward_many(sizes, [dd[k % 16].data_ptr() for k in range(len(sizes))],
+                     [di[k % 16].data_ptr() for k in range(len(sizes))],
+                     [outs[k].data_ptr() for k in range(len(sizes))], rs.MEM_DEVICE)
+    got = outs.cpu().numpy()
+    singles = {}
+    for k, S in enumerate(sizes):
+        key = (k % 16, S)
+        if key not in singles:
+            d, i = pool[k % 16]
+            singles[key] = acc.forward(np.ascontiguousarray(d[:S]), np.ascontiguousarray(i[:S]))
+        assert np.array_equal(got[k, :S], singles[key]), k
+        assert not got[k, S:].any(), k  # nothing written past the query's own rows
+    acc.close()
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("D,L", [(32, 80), (64, 80), (64, 20), (128, 33), (256, 7)])
+def test_sls_kernel_variants_bit_exact(variant, D, L, monkeypatch):
+    """Every SLS kernel variant (RS_SLS_VARIANT) reproduces the oracle's
+    canonical fp32 order bit for bit."""
+    monkeypatch.setenv("RS_SLS_VARIANT", variant)
+    spec = rs.ModelSpec(f"sls-v{variant}-D{D}", dense_fc=None, predict_fc=rs.LayerStack([4]),
+                        embeddings=rs.EmbeddingConfig(5, L, D, "Sum"), dense_input_dim=0)
+    rows = 20011
+    acc = rs.Accelerator(spec, rows, seed=2, max_query_size=300)
+    orc = Oracle(spec, rows, seed=2)
+    for S in (1, 37, 300):
+        _, idx = rs.fill_query(spec, rows, 6, S, S)
+        assert np.array_equal(acc.pooled(idx), orc.sls_canonical(idx)), (variant, D, L, S)
+    acc.close()

@@ -1,6 +1,7 @@
 """SLS microbenchmark: achieved HBM GB/s of the embedding stage (rs_pooled graph,
 CUDA-event timed on its stream) for the cfg3 RMC2 shape at several query sizes,
-for each SLS kernel variant (RS_SLS_VARIANT / RS_SLS_HINT / RS_SLS_UB knobs).
+for each SLS kernel variant (RS_SLS_VARIANT / RS_SLS_HINT / RS_SLS_UB knobs;
+variant 3 also takes RS_SLS_NBUF / RS_SLS_WARPS: "var:hint:ub:nbuf:warps").
 
   python tools/sls_micro.py [--rows 10000000] [--variants "0:1:16,1:1:16,2:1:8"]
 """
@@ -38,8 +39,10 @@ def main():
     out = torch.empty((max(sizes), args.T * args.D), device="cuda")
     results = {}
     for v in args.variants.split(","):
-        var, hint, ub = v.split(":")
+        parts = v.split(":") + ["2", "16"]
+        var, hint, ub, nbuf, warps = parts[:5]
         os.environ["RS_SLS_VARIANT"], os.environ["RS_SLS_HINT"], os.environ["RS_SLS_UB"] = var, hint, ub
+        os.environ["RS_SLS_NBUF"], os.environ["RS_SLS_WARPS"] = nbuf, warps
         acc = rs.Accelerator(spec, args.rows, seed=1, max_query_size=max(sizes))
         row = {}
         same = True
