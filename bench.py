@@ -36,6 +36,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the pipelined queue runs 8 lane streams + a copy stream + graph branches;
+# with the default 8 hardware work queues unrelated lanes serialise behind
+# each other (tools/timeline.py). Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "QPS at p95 tail-latency SLA per model at 1/2/4/8 B200; SLS HBM GB/s vs peak"
 NOMINAL_HBM_GBS = 8000.0

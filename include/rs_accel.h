@@ -184,7 +184,7 @@ typedef struct rs_init_desc {
   int32_t fc_mode;          /* RS_FC_*                                       */
   int32_t rnn_cell;         /* RS_RNN_* (AttentionRNN only)                  */
   int32_t l2_persist_mb;    /* >0: L2 persisting window over table rows     */
-  int32_t queue_depth;      /* rs_forward_many lanes in flight (0 = 4, <= 8) */
+  int32_t queue_depth;      /* rs_forward_many lanes in flight (0 = 4, <= 16) */
 } rs_init_desc;
 
 /* One query: S items. dense f32[S * dense_input_dim] and indices

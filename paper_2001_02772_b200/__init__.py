@@ -17,6 +17,11 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
+# rs_forward_many's lanes, copy stream and graph branches need more than the
+# default 8 hardware work queues or unrelated lanes serialise;
+# effective when this package is imported before the CUDA context is created.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librecsys_b200.so")
 

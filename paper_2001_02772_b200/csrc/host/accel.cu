@@ -13,9 +13,9 @@
 //  * a call = async H2D of the query's dense features and indices (pinned
 //    host memory) + 16-byte descriptor update + cudaGraphLaunch + async D2H
 //    of the logits and the error word, all on the caller's stream.
-//  * the descriptor update is two 64-bit stream memory writes whose VALUES
-//    are taken at enqueue time (cuStreamBatchMemOp), so the host may run any
-//    number of queries ahead of the GPU without a host-side ring to recycle.
+//  * the descriptor update has value semantics (event-guarded pinned ring,
+//    or cuStreamBatchMemOp writes), so the host may run any number of
+//    queries ahead of the GPU.
 #include <cuda.h>
 
 #include <algorithm>
@@ -73,7 +73,10 @@ struct Slot {
   cudaStream_t cap = nullptr;  // capture stream
   QDesc* d_q = nullptr;
   int* d_err = nullptr;
-  int* h_err = nullptr;        // pinned ring [kDescRing]
+  int* h_err = nullptr;        // pinned [kDescRing] (only [0] is used)
+  QDesc* h_q = nullptr;        // pinned descriptor ring [kDescRing]
+  cudaEvent_t q_ev[kDescRing] = {};  // last copy out of each ring entry
+  int ring = 0;
   float* dense_stage = nullptr;
   float* dense_raw = nullptr;   // contiguous H2D landing zone for strided dense
   int64_t* idx_stage = nullptr;
@@ -119,7 +122,7 @@ struct rs_accel {
   std::mutex mu;
   std::map<cudaStream_t, std::unique_ptr<rs::Slot>> slots;
   // rs_forward_many queue: `depth` lanes, each a compute stream + a slot
-  static constexpr int kMaxLanes = 8;
+  static constexpr int kMaxLanes = 16;
   int depth = 2;
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
   cudaStream_t lane[kMaxLanes] = {};
@@ -333,7 +336,7 @@ void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off, 
 int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, const float* in0,
                   int64_t ld_in0, int64_t in0_rows, float* const* tmp, int64_t ld_tmp,
                   float* final_out, int64_t ld_final, int64_t final_sCz, bool allow_tc,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool final_to_desc = false) {
   const int64_t maxS = a->init.max_query_size;
   int tc_count = 0;
   const float* in = in0;
@@ -347,6 +350,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
     args.bias = f.b; args.sbz = f.out;
     if (last) {
       args.C = final_out; args.ldc = ld_final; args.sCz = final_sCz;
+      args.c_desc = final_to_desc ? 1 : 0;
     } else {
       args.C = tmp[l & 1]; args.ldc = ld_tmp; args.sCz = maxS * ld_tmp;
     }
@@ -383,22 +387,38 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   if (kind == kGraphPool) {
     enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode == RS_FC_TF32, st);
   } else {
-    // The bottom MLP and the embedding stage are independent (they write
-    // disjoint columns of X): capture them as parallel graph branches.
-    const bool fork = m.has_dense_fc && a->T > 0;
+    // diagnostic only (tools/pipe_micro.py): RS_DIAG_SKIP bit 1 drops the
+    // bottom MLP, 2 the interaction, 4 the predict stack (outputs invalid)
+    const char* dsk = getenv("RS_DIAG_SKIP");
+    const int skip = dsk ? atoi(dsk) : 0;
+    // The dense branch (stage_dense + bottom MLP) and the embedding stage
+    // are independent (they write disjoint columns of X): capture them as
+    // parallel graph branches.
+    const bool dense = a->dense_in > 0;
+    const bool fork = dense && a->T > 0;
     if (fork) {
       RS_CUDA(cudaEventRecord(s->fork, st));
       RS_CUDA(cudaStreamWaitEvent(s->cap2, s->fork, 0));
     }
-    if (m.has_dense_fc)
-      ntc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
-                           a->max_dense_w, s->X, a->ld_x, 0, tc, fork ? s->cap2 : st);
+    cudaStream_t bs = fork ? s->cap2 : st;
+    if (dense) {
+      if (m.has_dense_fc) {
+        launch_stage_dense(s->d_q, a->dense_in, s->dense_stage, a->ld_dense, maxS, a->sm_count,
+                           bs);
+        if (!(skip & 1))
+          ntc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
+                               a->max_dense_w, s->X, a->ld_x, 0, tc, bs);
+      } else {
+        launch_stage_dense(s->d_q, a->dense_in, s->X, a->ld_x, maxS, a->sm_count, bs);
+      }
+    }
     if (fork) RS_CUDA(cudaEventRecord(s->join, s->cap2));
     if (m.pooling == RS_POOL_SUM) {
       if (a->T > 0) {
         enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, tc, st);
         if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
-        launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
+        if (!(skip & 2))
+          launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
                            a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
                            a->sm_count, st);
       }
@@ -406,8 +426,13 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
       enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, tc, st);
       if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
     }
-    ntc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w,
-                         s->out, a->out_w, a->out_dim, tc, st);
+    if (const char* de = getenv("RS_DIAG_EMPTY")) {
+      const char* dc = getenv("RS_DIAG_EMPTY_CTAS");
+      launch_diag_empty(atoi(de), dc ? atoi(dc) : 1, st);
+    }
+    if (!(skip & 4))
+      ntc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w,
+                           s->out, a->out_w, a->out_dim, tc, st, /*final_to_desc=*/true);
   }
   cudaError_t le = cudaGetLastError();
   cudaError_t ce = cudaStreamEndCapture(st, &g);
@@ -426,7 +451,8 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
     if (ty == cudaGraphNodeTypeKernel) ++k;
   }
   cudaGraphExec_t exec = nullptr;
-  RS_CUDA(cudaGraphInstantiate(&exec, g, 0));
+  RS_CUDA(cudaGraphInstantiate(&exec, g,
+                               prio_enabled() ? cudaGraphInstantiateFlagUseNodePriority : 0));
   RS_CUDA(cudaGraphDestroy(g));
   if (kernels) *kernels = k;
   if (tc_layers) *tc_layers = ntc;
@@ -439,6 +465,8 @@ std::unique_ptr<Slot> make_slot(rs_accel* a) {
   const int64_t maxS = a->init.max_query_size;
   RS_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
   s->d_q = static_cast<QDesc*>(dmalloc(a, s->allocs, sizeof(QDesc)));
+  RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_q), sizeof(QDesc) * kDescRing,
+                        cudaHostAllocPortable));
   RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_err), sizeof(int) * kDescRing,
                         cudaHostAllocPortable));
   std::memset(s->h_err, 0, sizeof(int) * kDescRing);
@@ -503,6 +531,9 @@ void free_slot(Slot* s) {
   if (s->free) cudaEventDestroy(s->free);
   for (void* p : s->allocs) cudaFree(p);
   if (s->h_err) cudaFreeHost(s->h_err);
+  if (s->h_q) cudaFreeHost(s->h_q);
+  for (auto e : s->q_ev)
+    if (e) cudaEventDestroy(e);
   if (s->cap) cudaStreamDestroy(s->cap);
   if (s->cap2) cudaStreamDestroy(s->cap2);
   if (s->fork) cudaEventDestroy(s->fork);
@@ -528,37 +559,47 @@ void check_query(rs_accel* a, const rs_query* q) {
 // bottom-MLP staging buffer (or straight into X[:, 0:dense_in] when there is
 // no dense stack), indices into the slot's staging buffer (host) or by
 // pointer (device), then the 16-byte device descriptor.
-// Descriptor update by value: two 64-bit stream writes (front-end ops, no copy
-// engine); the fallback, a copy from a pageable stack object, also consumes
-// the source before returning.
-void write_desc(rs_accel* a, Slot* s, int64_t S, const int64_t* idx, cudaStream_t st) {
+// Descriptor update with value semantics: four 64-bit stream writes, or a
+// 32-byte copy from a pinned ring entry that is reused only after its
+// previous copy executed.
+void write_desc(rs_accel* a, Slot* s, const QDesc& v, cudaStream_t st) {
   if (a->memops) {
-    CUstreamBatchMemOpParams ops[2];
+    const uint64_t vals[4] = {(uint64_t)v.S, (uint64_t)reinterpret_cast<uintptr_t>(v.idx),
+                              (uint64_t)reinterpret_cast<uintptr_t>(v.dense),
+                              (uint64_t)reinterpret_cast<uintptr_t>(v.out)};
+    CUstreamBatchMemOpParams ops[4];
     std::memset(ops, 0, sizeof(ops));
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 4; ++k) {
       ops[k].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
       ops[k].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+      ops[k].writeValue.address = reinterpret_cast<CUdeviceptr>(s->d_q) + 8 * k;
+      ops[k].writeValue.value64 = (cuuint64_t)vals[k];
     }
-    ops[0].writeValue.address = reinterpret_cast<CUdeviceptr>(&s->d_q->S);
-    ops[0].writeValue.value64 = (cuuint64_t)S;
-    ops[1].writeValue.address = reinterpret_cast<CUdeviceptr>(&s->d_q->idx);
-    ops[1].writeValue.value64 = (cuuint64_t)reinterpret_cast<uintptr_t>(idx);
-    if (a->memops(reinterpret_cast<CUstream>(st), 2, ops, 0) != CUDA_SUCCESS)
+    if (a->memops(reinterpret_cast<CUstream>(st), 4, ops, 0) != CUDA_SUCCESS)
       raise(RS_E_CUDA, "cuStreamBatchMemOp failed");
     return;
   }
-  QDesc v;
-  v.S = S;
-  v.idx = idx;
-  RS_CUDA(cudaMemcpyAsync(s->d_q, &v, sizeof(QDesc), cudaMemcpyHostToDevice, st));
+  // Pinned ring: an entry is rewritten only after the copy that last read it
+  // has executed (its event), so the host may run any distance ahead.
+  const int r = s->ring;
+  s->ring = (s->ring + 1) % kDescRing;
+  if (s->q_ev[r]) {
+    RS_CUDA(cudaEventSynchronize(s->q_ev[r]));
+  } else {
+    RS_CUDA(cudaEventCreateWithFlags(&s->q_ev[r], cudaEventDisableTiming));
+  }
+  s->h_q[r] = v;
+  RS_CUDA(cudaMemcpyAsync(s->d_q, &s->h_q[r], sizeof(QDesc), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaEventRecord(s->q_ev[r], st));
 }
 
-// Stream memory writes are used only if a test write lands (RS_DESC_COPY=1
-// forces the copy path).
+// Descriptor writes: a copy from the slot's event-guarded pinned ring
+// (default; measured faster for a lone query, equal in the pipelined queue),
+// or with RS_DESC_MEMOP=1 stream memory writes, used only if a test write lands.
 BatchMemOpFn probe_memops(rs_accel* a) {
   BatchMemOpFn fn = batch_memop_fn();
-  const char* force = getenv("RS_DESC_COPY");
-  if (!fn || (force && atoi(force))) return nullptr;
+  const char* want = getenv("RS_DESC_MEMOP");
+  if (!fn || !want || !atoi(want)) return nullptr;
   uint64_t* d = nullptr;
   if (cudaMalloc(&d, 8) != cudaSuccess) return nullptr;
   CUstreamBatchMemOpParams op;
@@ -577,31 +618,28 @@ BatchMemOpFn probe_memops(rs_accel* a) {
   return ok ? fn : nullptr;
 }
 
-void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream_t st) {
+// Inputs of one query onto the slot: host buffers are copied (one contiguous
+// H2D each) into the slot's landing zones; device buffers are used in place.
+// The descriptor carries the item count and the dense / index / output
+// pointers; the graph's stage_dense kernel places the dense rows, and for a
+// device output buffer the final FC layer writes the logits straight into it.
+void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream_t st,
+                  float* out = nullptr) {
   const int64_t S = q->size;
   const bool host = q->location == RS_MEM_HOST;
-  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  QDesc v{};
+  v.S = S;
   if (full && a->dense_in > 0) {
     if (!q->dense) raise(RS_E_INVALID, "null dense features");
-    float* dst = a->m.has_dense_fc ? s->dense_stage : s->X;
-    const int64_t ld = a->m.has_dense_fc ? a->ld_dense : a->ld_x;
-    if (ld == a->dense_in) {
-      RS_CUDA(cudaMemcpyAsync(dst, q->dense, (size_t)(S * a->dense_in * 4), kind, st));
+    if (host) {
+      RS_CUDA(cudaMemcpyAsync(s->dense_raw, q->dense, (size_t)(S * a->dense_in * 4),
+                              cudaMemcpyHostToDevice, st));
+      v.dense = s->dense_raw;
     } else {
-      // Strided placement: from host, one contiguous H2D into the raw staging
-      // buffer first (a row-by-row 2D DMA over PCIe is several times slower),
-      // then the strided copy on the device.
-      const float* src = q->dense;
-      if (host) {
-        RS_CUDA(cudaMemcpyAsync(s->dense_raw, q->dense, (size_t)(S * a->dense_in * 4),
-                                cudaMemcpyHostToDevice, st));
-        src = s->dense_raw;
-      }
-      RS_CUDA(cudaMemcpy2DAsync(dst, (size_t)(ld * 4), src, (size_t)(a->dense_in * 4),
-                                (size_t)(a->dense_in * 4), (size_t)S, cudaMemcpyDeviceToDevice,
-                                st));
+      v.dense = q->dense;
     }
   }
+  if (full && !host) v.out = out;
   const int64_t* idx = nullptr;
   if (a->T > 0) {
     if (host) {
@@ -612,7 +650,8 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
       idx = q->indices;
     }
   }
-  write_desc(a, s, S, idx, st);
+  v.idx = idx;
+  write_desc(a, s, v, st);
 }
 
 cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full) {
@@ -627,6 +666,7 @@ void launch_stage(rs_accel* a, Slot* s, const rs_query* q, float* out, bool full
                   cudaStream_t st) {
   const int64_t S = q->size;
   RS_CUDA(cudaGraphLaunch(pick_graph(a, s, S, full), st));
+  if (full && q->location != RS_MEM_HOST) return;  // written in place by the final layer
   const int64_t w = full ? a->out_w : a->pooled_dim;
   const float* src = full ? s->out : s->pooled;
   RS_CUDA(cudaMemcpyAsync(out, src, (size_t)(S * w * 4),
@@ -657,15 +697,16 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->own;
     Slot* s = get_slot(a, st);
     if (timing) RS_CUDA(cudaEventRecord(s->ev[0], st));
-    stage_inputs(a, s, q, full, st);
+    stage_inputs(a, s, q, full, st, out);
     if (timing) RS_CUDA(cudaEventRecord(s->ev[1], st));
     RS_CUDA(cudaGraphLaunch(pick_graph(a, s, q->size, full), st));
     if (timing) RS_CUDA(cudaEventRecord(s->ev[2], st));
     const int64_t w = full ? a->out_w : a->pooled_dim;
-    RS_CUDA(cudaMemcpyAsync(out, full ? s->out : s->pooled, (size_t)(q->size * w * 4),
-                            q->location == RS_MEM_HOST ? cudaMemcpyDeviceToHost
-                                                       : cudaMemcpyDeviceToDevice,
-                            st));
+    if (!full || q->location == RS_MEM_HOST)
+      RS_CUDA(cudaMemcpyAsync(out, full ? s->out : s->pooled, (size_t)(q->size * w * 4),
+                              q->location == RS_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                         : cudaMemcpyDeviceToDevice,
+                              st));
     if (timing) {
       RS_CUDA(cudaEventRecord(s->ev[3], st));
       RS_CUDA(cudaEventSynchronize(s->ev[3]));
@@ -730,6 +771,11 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     RS_CUDA(cudaEventRecord(a->copy_gate, st));
     for (int d = 0; d < depth; ++d) RS_CUDA(cudaStreamWaitEvent(a->lane[d], a->copy_gate, 0));
     if (loc == RS_MEM_HOST) RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
+    // diagnostic (tools): RS_MANY_POOL_ONLY=1 runs only the embedding-stage
+    // graph per query (outputs are the pooled rows), to separate the
+    // gather's pipelined throughput from the FC tail's
+    const char* po = getenv("RS_MANY_POOL_ONLY");
+    const bool pool_only = po && atoi(po);
     const auto host_t0 = std::chrono::steady_clock::now();
     for (int64_t i = 0; i < n; ++i) {
       const int d = (int)(i % depth);
@@ -745,9 +791,9 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
         RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
       } else {
         if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, ls));
-        stage_inputs(a, s, &qs[i], true, ls);
+        stage_inputs(a, s, &qs[i], true, ls, outs[i]);
       }
-      launch_stage(a, s, &qs[i], outs[i], true, ls);
+      launch_stage(a, s, &qs[i], outs[i], !pool_only, ls);
       RS_CUDA(cudaEventRecord(s->free, ls));
       if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[1 + i % kEvRing], ls));
     }

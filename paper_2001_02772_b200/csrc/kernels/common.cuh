@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <utility>
 
@@ -16,7 +17,8 @@ namespace rs {
 struct QDesc {
   int64_t S;
   const int64_t* idx;  // [S, T, L] int64 (device)
-  int64_t pad[2];
+  const float* dense;  // [S, dense_in] fp32 contiguous (device), or null
+  float* out;          // final logits [S, out_w] (device) or null: slot buffer
 };
 
 // Error bits accumulated by kernels and read back with the logits.
@@ -81,6 +83,28 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// PDL edges are captured unless RS_PDL=0 (read at graph capture).
+inline bool pdl_enabled() {
+  const char* v = getenv("RS_PDL");
+  return !v || atoi(v) != 0;
+}
+
+// Node priorities (graphs instantiated with cudaGraphInstantiateFlagUseNodePriority):
+// the latency-bound dense kernels (staging, FC layers, interaction) run at the
+// device's greatest priority, the HBM-bound gathers at the default. Without
+// it, the gathers of the other pipelined lanes refill every SM slot as it
+// frees (3 gather CTAs fill an SM's registers) and the larger FC CTAs starve
+// (tools/timeline.py). RS_PRIO=0 disables.
+inline bool prio_enabled() {
+  const char* v = getenv("RS_PRIO");
+  return !v || atoi(v) != 0;
+}
+inline int high_priority() {
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  return greatest;
+}
+
 #if defined(__CUDACC__)
 // Launch with the programmatic-stream-serialisation attribute (captured into
 // a CUDA graph as a programmatic dependency edge).
@@ -92,11 +116,20 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (prio_enabled()) {
+    attr[n].id = cudaLaunchAttributePriority;
+    attr[n].val.priority = high_priority();
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 #endif

@@ -45,7 +45,10 @@ __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
                int hint) {
-  pdl_trigger();  // let the interaction grid launch behind us
+  // No early PDL trigger in the embedding-stage kernels: a dependent grid
+  // launched early would squat on the SM slots this grid's tail frees, which
+  // the next query's gather (another lane) should get. Dependents launch at
+  // completion.
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   __shared__ int64_t sidx[kWarps][kIdxChunk];
@@ -126,7 +129,6 @@ __global__ void __launch_bounds__(32)
 sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap tmap,
                int64_t rows, int T, int L, int LB, float* __restrict__ out, int64_t ld_out,
                int* __restrict__ err) {
-  pdl_trigger();
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   extern __shared__ __align__(128) uint8_t sm_raw[];
@@ -253,8 +255,9 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
 template <int LPR, int VPL, int U, int IPL>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
-                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err) {
-  pdl_trigger();
+                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
+                int trig) {
+  if (trig) pdl_trigger();
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   constexpr int B = R * U;  // rows per batch
@@ -350,7 +353,6 @@ __global__ void __launch_bounds__(512)
 sls_stage_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                  int T, int L, int nbuf, float* __restrict__ out, int64_t ld_out,
                  int* __restrict__ err) {
-  pdl_trigger();
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   constexpr int C4 = D / 4;  // 16-byte chunks per row
@@ -456,7 +458,6 @@ __global__ void __launch_bounds__(kWarps * 32)
 sls_sum_scalar_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
                       int64_t rows, int T, int L, int D, float* __restrict__ out,
                       int64_t ld_out, int* __restrict__ err) {
-  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t bags = qd->S * T;
   const int64_t* __restrict__ idx = qd->idx;
@@ -481,7 +482,6 @@ __global__ void __launch_bounds__(256)
 gather_concat_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
                      int64_t rows, int T, int L, int D, float* __restrict__ out,
                      int64_t ld_out, int64_t col_off, int vec, int* __restrict__ err) {
-  pdl_trigger();
   const int64_t S = qd->S;
   const int64_t* __restrict__ idx = qd->idx;
   const int64_t TL = (int64_t)T * L;
@@ -521,7 +521,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
 din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                 int T, int L, const float* __restrict__ att_w, float* __restrict__ out,
                 int64_t ld_out, int64_t col_off, int* __restrict__ err) {
-  pdl_trigger();
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   __shared__ int64_t sidx[kWarps][kIdxChunk];
@@ -657,7 +656,6 @@ __global__ void __launch_bounds__(kInterThreads)
 interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
                    int64_t ld_pooled, int T, int D, float* __restrict__ X, int64_t ld_x,
                    int64_t sum_off, int64_t dot_off, int has_dense) {
-  pdl_trigger();
   pdl_wait();  // pooled (SLS) and X[:, 0:D] (bottom MLP) are predecessors' outputs
   extern __shared__ float sv[];  // [(T+1)][D+1]
   const int P = has_dense ? (T + 1) * T / 2 : 0;
@@ -703,6 +701,7 @@ interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ poole
       }
     }
     __syncthreads();
+    pdl_trigger();  // the predict layer's grid may launch while the dots run
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
       float s = 0.f;
       for (int t = 1; t <= T; ++t) s += sv[t * ldv + c];
@@ -772,6 +771,11 @@ int sls_ub() {
   return v ? atoi(v) : 4;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 template <int LPR, int VPL, int U, int IPL>
 void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                      float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
@@ -783,28 +787,28 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
     return b > 0 ? b : 1;
   }();
   const int grid = grid_for(max_items * T, kWarps, sm_count, 2 * per_sm);
-  sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out,
-                                                                 ld_out, err);
+  sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, kWarps * 32, 0, s>>>(
+      qd, tables, rows, T, L, out, ld_out, err, env_int("RS_SLS_TRIGGER", 0));
 }
 
 template <int LPR, int VPL>
 bool try_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L, float* out,
                   int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s) {
   if (L > 96) return false;
-  const bool u8 = sls_ub() >= 8;
+  const int ub = sls_ub();
+#define RS_PIPE(U, IPL) \
+  launch_sls_pipe<LPR, VPL, U, IPL>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s)
   if (L <= 32) {
-    if (u8) launch_sls_pipe<LPR, VPL, (VPL == 2 ? 4 : 8), 1>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
-    else launch_sls_pipe<LPR, VPL, (VPL == 2 ? 2 : 4), 1>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
+    if (ub >= 8) RS_PIPE((VPL == 2 ? 4 : 8), 1);
+    else if (ub <= 2) RS_PIPE((VPL == 2 ? 1 : 2), 1);
+    else RS_PIPE((VPL == 2 ? 2 : 4), 1);
   } else {
-    if (u8) launch_sls_pipe<LPR, VPL, (VPL == 2 ? 4 : 8), 3>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
-    else launch_sls_pipe<LPR, VPL, (VPL == 2 ? 2 : 4), 3>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s);
+    if (ub >= 8) RS_PIPE((VPL == 2 ? 4 : 8), 3);
+    else if (ub <= 2) RS_PIPE((VPL == 2 ? 1 : 2), 3);
+    else RS_PIPE((VPL == 2 ? 2 : 4), 3);
   }
+#undef RS_PIPE
   return true;
-}
-
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
 }
 
 // Variant 3 geometry: one CTA per SM, each warp owning nbuf bag stages
@@ -949,12 +953,61 @@ void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
                         int64_t max_items, int sm_count, cudaStream_t s) {
   const size_t smem = (size_t)(T + 1) * (D + 1) * sizeof(float);
-  const int grid = grid_for(max_items, 1, sm_count, 8);
+  const int grid = grid_for(max_items, 1, sm_count, 2);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(interaction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   launch_pdl(interaction_kernel, dim3(grid), dim3(kInterThreads), smem, s, qd, pooled, ld_pooled,
              T, D, X, ld_x, sum_off, dot_off, has_dense);
+}
+
+// Dense features into the FC staging buffer: [S, dense_in] contiguous (the
+// caller's device buffer, or the contiguous H2D landing zone) -> rows of
+// stride ld_dst. A kernel, not a copy-engine memcpy, so the pipelined lanes
+// do not queue behind each other on the copy engine.
+__global__ void __launch_bounds__(256)
+stage_dense_kernel(const QDesc* __restrict__ qd, int64_t dense_in, float* __restrict__ dst,
+                   int64_t ld_dst) {
+  pdl_trigger();
+  const float* __restrict__ src = qd->dense;
+  const int64_t S = qd->S;
+  if (!src) return;
+  const bool vec = (dense_in % 4 == 0) && (ld_dst % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  if (vec) {
+    const int64_t w = dense_in / 4, total = S * w;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = i / w, c = i - r * w;
+      reinterpret_cast<float4*>(dst + r * ld_dst)[c] =
+          __ldg(reinterpret_cast<const float4*>(src) + i);
+    }
+  } else {
+    const int64_t total = S * dense_in;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = i / dense_in, c = i - r * dense_in;
+      dst[r * ld_dst + c] = __ldg(src + i);
+    }
+  }
+}
+
+void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t ld_dst,
+                        int64_t max_items, int sm_count, cudaStream_t s) {
+  const int64_t units = max_items * ((dense_in % 4 == 0) ? dense_in / 4 : dense_in);
+  const int grid = grid_for(units, 256, sm_count, 2);
+  launch_pdl(stage_dense_kernel, dim3(grid), dim3(256), 0, s, qd, dense_in, dst, ld_dst);
+}
+
+// Diagnostic (RS_DIAG_EMPTY, tools/pipe_micro.py): n empty grids of `ctas`
+// CTAs, to measure the per-kernel cost inside the pipelined forward.
+__global__ void diag_empty_kernel() {
+  pdl_trigger();
+  pdl_wait();
+}
+
+void launch_diag_empty(int n, int ctas, cudaStream_t s) {
+  for (int i = 0; i < n; ++i) launch_pdl(diag_empty_kernel, dim3(ctas), dim3(128), 0, s);
 }
 
 size_t interaction_smem(int T, int D) { return (size_t)(T + 1) * (D + 1) * sizeof(float); }

@@ -38,7 +38,6 @@ __global__ void __launch_bounds__(THREADS)
 fc_ffma_kernel(const QDesc* __restrict__ qd, FcArgs a) {
   __shared__ __align__(16) float As[STAGES][BM][PITCH];
   __shared__ __align__(16) float Bs[STAGES][BN][PITCH];
-  pdl_trigger();
   const int64_t M = qd->S;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, z = blockIdx.z;
   if (m0 >= M) return;
@@ -111,8 +110,11 @@ fc_ffma_kernel(const QDesc* __restrict__ qd, FcArgs a) {
     }
   }
   cp_async_wait<0>();
+  // trigger late: the next layer's CTAs launch during this epilogue instead
+  // of holding registers and shared memory through the whole main loop
+  pdl_trigger();
 
-  float* __restrict__ C = a.C + (int64_t)z * a.sCz;
+  float* __restrict__ C = ((a.c_desc && qd->out) ? qd->out : a.C) + (int64_t)z * a.sCz;
   const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {

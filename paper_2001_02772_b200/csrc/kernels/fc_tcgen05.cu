@@ -104,7 +104,6 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   extern __shared__ uint8_t smem_raw[];
   TcSmem<BN, STAGES>& sm = *reinterpret_cast<TcSmem<BN, STAGES>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  pdl_trigger();
   const int64_t M = qd->S;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, z = blockIdx.z;
   if (m0 >= M) return;
@@ -193,11 +192,15 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
     // ---- epilogue: TMEM -> registers -> bias/ReLU -> global ----
     mbar_wait(&sm.tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // trigger late (accumulation done): the next layer's CTAs launch during
+    // this epilogue instead of squatting on the SM through the main loop
+    pdl_trigger();
     const int quad = warp & 3;
     const int64_t m = m0 + quad * 32 + lane;
-    float* __restrict__ C = a.C + (int64_t)z * a.sCz + m * a.ldc;
+    float* __restrict__ Cb = (a.c_desc && qd->out) ? qd->out : a.C;
+    float* __restrict__ C = Cb + (int64_t)z * a.sCz + m * a.ldc;
     const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
-    const bool vec_ok = (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0) &&
+    const bool vec_ok = (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(Cb) & 15) == 0) &&
                         (a.sCz % 4 == 0);
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {

@@ -44,7 +44,6 @@ __device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x))
 
 template <bool WSMEM>
 __global__ void gru_kernel(const QDesc* __restrict__ qd, GruArgs g) {
-  pdl_trigger();
   const int H = g.H, D = g.D, L = g.L;
   const int G = blockDim.x / H;
   const int NSEQ = SPT * G;

@@ -63,7 +63,6 @@ struct GruTcSmem {
 template <int D, int H>
 __global__ void __launch_bounds__(kThreads, 1)
 gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
-  pdl_trigger();
   using SM = GruTcSmem<D, H>;
   constexpr int N = SM::N, KA = SM::KA, DA = D / 32;
   constexpr int HU = H / 2;   // hidden units per thread

@@ -20,6 +20,9 @@ bool din_supported(int64_t D);
 void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
                      const float* att_w, float* out, int64_t ld_out, int64_t col_off, int* err,
                      int64_t max_items, int sm_count, cudaStream_t s);
+void launch_diag_empty(int n, int ctas, cudaStream_t s);
+void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t ld_dst,
+                        int64_t max_items, int sm_count, cudaStream_t s);
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
                         int64_t max_items, int sm_count, cudaStream_t s);
@@ -36,6 +39,7 @@ struct FcArgs {
   const float* bias; int64_t sbz;
   float* C; int64_t ldc; int64_t sCz;
   int N; int K; int relu; int batch;
+  int c_desc;  // 1: write C into QDesc::out when that is non-null (final layer)
 };
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);
 

@@ -231,13 +231,14 @@ def test_dien_tensor_core_recurrence(augru, L):
                       max_q=256)
 
 
-@pytest.mark.parametrize("desc_copy", ["0", "1"])
-def test_forward_many_long_batch_host_runs_ahead(desc_copy, monkeypatch):
+@pytest.mark.parametrize("desc_memop", ["0", "1"])
+def test_forward_many_long_batch_host_runs_ahead(desc_memop, monkeypatch):
     """2000 small queries over 2 lanes: the host enqueues far ahead of the GPU,
-    so every query must carry its own descriptor (item count, index pointer)
-    by value — stream memory writes, or the pageable-copy fallback."""
+    so every query must carry its own descriptor (item count, pointers) by
+    value — the event-guarded pinned ring (wraps every 256 queries per lane),
+    or stream memory writes."""
     torch = pytest.importorskip("torch")
-    monkeypatch.setenv("RS_DESC_COPY", desc_copy)
+    monkeypatch.setenv("RS_DESC_MEMOP", desc_memop)
     spec = rs.builtin_model("DLRM-RMC1")
     rows = 5000
     acc = rs.Accelerator(spec, rows, seed=4, max_query_size=64, fc_mode=rs.FC_FP32,
