@@ -8,14 +8,15 @@
 // tensor core rounds operands to tf32 and accumulates in fp32 in TMEM.
 // Tolerance for this path is stated in tests/test_gpu_parity.py.
 //
-// One 128 x BN output tile per CTA, 8 warps with fixed roles:
-//   warp 0  TMA producer: K slabs of 32 fp32 (=128 B, one SWIZZLE_128B atom
-//           row) for A (128 rows) and W (BN rows) into a STAGES-deep ring
-//   warp 1  MMA issuer: one elected lane issues 4 x tcgen05.mma (K = 8 each)
-//           per slab, tcgen05.commit frees the slab / signals the epilogue
-//   warp 2  TMEM allocator (BN fp32 columns x 128 lanes)
-//   warps 4-7  epilogue: tcgen05.ld 32x32b.x32 (warp w%4 owns TMEM lanes
-//           32(w%4)..+31 = tile rows), + bias, ReLU, 128-bit stores
+// One 128 x BN output tile per CTA, 4 warps (a small CTA: inside the
+// pipelined queue these grids share SMs with the gathers of other queries):
+//   warp 0  TMEM allocator (BN fp32 columns x 128 lanes); lane 0 is the TMA
+//           producer: K slabs of 32 fp32 (=128 B, one SWIZZLE_128B atom row)
+//           for A (128 rows) and W (BN rows) into a STAGES-deep ring
+//   warp 1  lane 0 issues 4 x tcgen05.mma (K = 8 each) per slab;
+//           tcgen05.commit frees the slab / signals the epilogue
+//   all 4   epilogue: tcgen05.ld 32x32b.x32 (warp w owns TMEM lanes
+//           32w..32w+31 = tile rows), + bias, ReLU, 128-bit stores
 // Rows >= S (device query descriptor) are masked at the store; the tile's
 // K tail is zero-filled by TMA.
 #include <algorithm>
@@ -97,8 +98,10 @@ struct TcSmem {
   uint32_t tmem_base;
 };
 
+constexpr int kTcThreads = 128;
+
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kTcThreads, 1)
 fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap map_a,
              const __grid_constant__ CUtensorMap map_w, FcArgs a, int a_batched) {
   extern __shared__ uint8_t smem_raw[];
@@ -124,7 +127,7 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm.tmem_base)),
                  "r"(BN)
@@ -146,9 +149,9 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   }
   pdl_wait();  // the activations A are the previous layer's output
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer ----
-    for (int kb = 0; kb < nk; ++kb) {
+  if (warp == 0) {
+    // ---- TMA producer (lane 0) ----
+    for (int kb = 0; lane == 0 && kb < nk; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
       if (kb >= pre) {
@@ -159,10 +162,11 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
       if (a_batched) tma_load_3d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0, z);
       else tma_load_2d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0);
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer (single thread) ----
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---- MMA issuer (lane 0) ----
     const uint32_t idesc = idesc_tf32<BN>();
-    for (int kb = 0; kb < nk; ++kb) {
+    for (int kb = 0; lane == 0 && kb < nk; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
       mbar_wait(&sm.full[s], ph);
@@ -184,18 +188,21 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
               smem_u32(&sm.empty[s]))
           : "memory");
     }
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(&sm.tmem_full))
-        : "memory");
-  } else if (warp >= 4) {
-    // ---- epilogue: TMEM -> registers -> bias/ReLU -> global ----
+    if (lane == 0)
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              smem_u32(&sm.tmem_full))
+          : "memory");
+    __syncwarp();
+  }
+  {
+    // ---- epilogue (all warps): TMEM -> registers -> bias/ReLU -> global ----
     mbar_wait(&sm.tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // trigger late (accumulation done): the next layer's CTAs launch during
     // this epilogue instead of squatting on the SM through the main loop
     pdl_trigger();
-    const int quad = warp & 3;
+    const int quad = warp;
     const int64_t m = m0 + quad * 32 + lane;
     float* __restrict__ Cb = (a.c_desc && qd->out) ? qd->out : a.C;
     float* __restrict__ C = Cb + (int64_t)z * a.sCz + m * a.ldc;
@@ -242,7 +249,7 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN)
                  : "memory");
@@ -314,8 +321,11 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.W) & 15))
     return false;
   // tile/pipeline configuration: 0 <BN128,3 stages> 1 <64,4> 2 <128,6> 3 <64,8>
-  // (RS_TC_CFG overrides, for tools/fc_micro.py)
-  p->cfg = a.N >= 128 ? 0 : 1;
+  // (RS_TC_CFG overrides, for tools/fc_micro.py). Default: the deep pipelines.
+  // A layer CTA is latency-bound (few k-blocks per round trip), and inside the
+  // pipelined queue its lifetime is what it costs the concurrent gathers
+  // (tools/pipe_micro.py: 44.0 -> 41.4 us/query on cfg3 RMC2 vs <128,3>).
+  p->cfg = a.N >= 128 ? 2 : 3;
   if (const char* e = getenv("RS_TC_CFG")) p->cfg = atoi(e) & 3;
   if (a.N < 128 && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
   p->block_n = (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
@@ -353,7 +363,7 @@ void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_
   const dim3 grid(p.n_tiles, p.m_tiles, a.batch);
   const int a_batched = a.sAz != 0 ? 1 : 0;
 #define RS_TC(BN, ST)                                                                   \
-  launch_pdl(fc_tc_kernel<BN, ST>, grid, dim3(256), tc_smem_bytes<BN, ST>(), s, qd, p.map_a, \
+  launch_pdl(fc_tc_kernel<BN, ST>, grid, dim3(kTcThreads), tc_smem_bytes<BN, ST>(), s, qd, p.map_a, \
              p.map_w, a, a_batched)
   switch (p.cfg) {
     case 0: RS_TC(128, 3); break;
