@@ -325,7 +325,12 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   // A layer CTA is latency-bound (few k-blocks per round trip), and inside the
   // pipelined queue its lifetime is what it costs the concurrent gathers
   // (tools/pipe_micro.py: 44.0 -> 41.4 us/query on cfg3 RMC2 vs <128,3>).
-  p->cfg = a.N >= 128 ? 2 : 3;
+  // Long-K or wide layers (MT-WND's 1640 -> 1024 x 4 stacks) are bound by
+  // feeding the tensor cores from L2, not by latency: there two shallower
+  // CTAs per SM win (MT-WND 27.0 -> 21.5 us/query), so they keep <128,3>/<64,4>.
+  const int64_t ctas = (int64_t)((a.N + 127) / 128) * ((m_cap + BM - 1) / BM) * a.batch;
+  const bool wide = a.K >= 1024 || ctas > 148;
+  p->cfg = a.N >= 128 ? (wide ? 0 : 2) : (wide ? 1 : 3);
   if (const char* e = getenv("RS_TC_CFG")) p->cfg = atoi(e) & 3;
   if (a.N < 128 && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
   p->block_n = (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
