@@ -333,6 +333,12 @@ void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off, 
 
 // One FC stack: layer l reads `in` and writes the next buffer; the last layer
 // writes `final_out`.
+// RS_FUSE_LAST=0 keeps the narrow final layer as its own kernel.
+bool fuse_enabled() {
+  const char* v = getenv("RS_FUSE_LAST");
+  return !v || atoi(v) != 0;
+}
+
 int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, const float* in0,
                   int64_t ld_in0, int64_t in0_rows, float* const* tmp, int64_t ld_tmp,
                   float* final_out, int64_t ld_final, int64_t final_sCz, bool allow_tc,
@@ -357,11 +363,37 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
     args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
     bool used_tc = false;
     if (allow_tc) {
+      // A narrow final layer (<= 4 outputs: the DLRM / DIN / DIEN logits)
+      // after a single-N-tile layer is fused into that layer's epilogue: one
+      // kernel fewer per query and no round trip of the hidden activations.
+      const bool fuse = l + 2 == layers.size() && layers[l + 1].out <= kFuseMaxN2 &&
+                        f.out <= 128 && fuse_enabled();
+      if (fuse) {
+        const FcLayer& g = layers[l + 1];
+        args.single_n_tile = 1;
+        args.W2 = g.W; args.ldw2 = g.ldk; args.sW2z = g.out * g.ldk;
+        args.b2 = g.b; args.sb2z = g.out;
+        args.C2 = final_out; args.ldc2 = ld_final; args.sC2z = final_sCz;
+        args.N2 = (int)g.out; args.relu2 = g.relu; args.c2_desc = final_to_desc ? 1 : 0;
+        args.skip_c = 1;
+      }
       TcPlan p;
-      if (tc_plan(&p, args, maxS, a_rows)) {
+      if (tc_plan(&p, args, maxS, a_rows) && (!fuse || p.n_tiles == 1)) {
         launch_fc_tc(s->d_q, p, args, st);
         used_tc = true;
         ++tc_count;
+        if (fuse) {
+          ++tc_count;
+          break;  // the final layer ran in this epilogue
+        }
+      } else if (fuse) {
+        args.single_n_tile = 0; args.N2 = 0; args.skip_c = 0; args.W2 = nullptr;
+        args.b2 = nullptr; args.C2 = nullptr;
+        if (tc_plan(&p, args, maxS, a_rows)) {
+          launch_fc_tc(s->d_q, p, args, st);
+          used_tc = true;
+          ++tc_count;
+        }
       }
     }
     if (!used_tc) launch_fc_ffma(s->d_q, args, maxS, st);

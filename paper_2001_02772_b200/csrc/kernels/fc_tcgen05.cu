@@ -209,6 +209,8 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
     const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
     const bool vec_ok = (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(Cb) & 15) == 0) &&
                         (a.sCz % 4 == 0);
+    const float* __restrict__ W2 = a.W2 + (int64_t)z * a.sW2z;
+    float part[kFuseMaxN2] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
@@ -234,7 +236,21 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
           float val = __uint_as_float(v[i]) + (n < a.N ? __ldg(bias + n) : 0.f);
           y[i] = a.relu ? fmaxf(val, 0.f) : val;
         }
-        if (vec_ok && nb + 32 <= a.N) {
+        if (a.N2 > 0) {
+          // fused narrow next layer: this thread owns row m; columns in order
+#pragma unroll
+          for (int o = 0; o < kFuseMaxN2; ++o) {
+            if (o >= a.N2) break;
+            const float* __restrict__ w = W2 + (int64_t)o * a.ldw2 + nb;
+            float acc2 = part[o];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (nb + i < a.N) acc2 = fmaf(y[i], __ldg(w + i), acc2);
+            part[o] = acc2;
+          }
+        }
+        if (a.skip_c) {
+        } else if (vec_ok && nb + 32 <= a.N) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             reinterpret_cast<float4*>(C + nb)[i] =
@@ -244,6 +260,17 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
           for (int i = 0; i < 32; ++i)
             if (nb + i < a.N) C[nb + i] = y[i];
         }
+      }
+    }
+    if (a.N2 > 0 && m < M) {
+      float* __restrict__ C2b = (a.c2_desc && qd->out) ? qd->out : a.C2;
+      float* __restrict__ C2 = C2b + (int64_t)z * a.sC2z + m * a.ldc2;
+      const float* __restrict__ b2 = a.b2 + (int64_t)z * a.sb2z;
+#pragma unroll
+      for (int o = 0; o < kFuseMaxN2; ++o) {
+        if (o >= a.N2) break;
+        const float val = part[o] + __ldg(b2 + o);
+        C2[o] = a.relu2 ? fmaxf(val, 0.f) : val;
       }
     }
   }
@@ -332,7 +359,8 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   const bool wide = a.K >= 1024 || ctas > 148;
   p->cfg = a.N >= 128 ? (wide ? 0 : 2) : (wide ? 1 : 3);
   if (const char* e = getenv("RS_TC_CFG")) p->cfg = atoi(e) & 3;
-  if (a.N < 128 && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
+  if (a.single_n_tile && a.N <= 128 && (p->cfg == 1 || p->cfg == 3)) p->cfg -= 1;
+  if (a.N < 128 && !a.single_n_tile && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
   p->block_n = (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
   p->m_tiles = (int)((m_cap + BM - 1) / BM);
   p->n_tiles = (a.N + p->block_n - 1) / p->block_n;

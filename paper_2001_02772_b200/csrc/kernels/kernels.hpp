@@ -40,7 +40,17 @@ struct FcArgs {
   float* C; int64_t ldc; int64_t sCz;
   int N; int K; int relu; int batch;
   int c_desc;  // 1: write C into QDesc::out when that is non-null (final layer)
+  // Optional narrow next layer fused into the tcgen05 epilogue (the CTA owns
+  // whole rows of C when the layer is a single N tile):
+  //   C2[z][m][o] = act2( sum_n C[z][m][n] * W2[z][o][n] + b2[z][o] ), o < N2 <= 4
+  const float* W2; int64_t ldw2; int64_t sW2z;
+  const float* b2; int64_t sb2z;
+  float* C2; int64_t ldc2; int64_t sC2z;
+  int N2; int relu2; int c2_desc;
+  int skip_c;          // 1: C itself is not needed (only C2)
+  int single_n_tile;   // planning hint: prefer one N tile (BN = 128) when N <= 128
 };
+constexpr int kFuseMaxN2 = 4;
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);
 
 // ---- fc_tcgen05.cu ----
