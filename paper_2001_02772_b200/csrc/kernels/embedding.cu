@@ -719,6 +719,79 @@ interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ poole
   }
 }
 
+// Warp-per-item interaction (the default when 8 items' operands fit in shared
+// memory): 8 warps = 8 items per CTA, so a 300-item query is ~40 CTAs instead
+// of 300 — inside the pipelined queue every CTA slot these take is a slot
+// the concurrent gathers lose. Same per-output summation order as
+// interaction_kernel: sum over t = 1..T in order; each dot sequential in c.
+constexpr int kInterWarps = 8;
+
+__global__ void __launch_bounds__(kInterWarps * 32)
+interaction_warp_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
+                        int64_t ld_pooled, int T, int D, float* __restrict__ X, int64_t ld_x,
+                        int64_t sum_off, int64_t dot_off, int has_dense) {
+  pdl_wait();  // pooled (SLS) and X[:, 0:D] (bottom MLP) are predecessors' outputs
+  extern __shared__ float smem_int[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ldv = D + 1;
+  float* sv = smem_int + (size_t)warp * (T + 1) * ldv;  // [(T+1)][D+1]
+  const int P = has_dense ? (T + 1) * T / 2 : 0;
+  const int D4 = D / 4;
+  const int units = (T + 1) * D4;
+  const int64_t S = qd->S;
+  for (int64_t item = (int64_t)blockIdx.x * kInterWarps + warp; item < S;
+       item += (int64_t)gridDim.x * kInterWarps) {
+    __syncwarp();
+    // all of the item's 128-bit loads in flight before any shared store
+    constexpr int kPer = 9;  // float4 per lane per round (T+1 <= 33, D <= 64: two rounds)
+    for (int base = 0; base < units; base += kPer * 32) {
+      float4 r[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int u = base + k * 32 + lane;
+        r[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u < units) {
+          const int v = u / D4, c4 = u - v * D4;
+          if (v == 0) {
+            if (has_dense) r[k] = *reinterpret_cast<const float4*>(X + item * ld_x + c4 * 4);
+          } else {
+            r[k] = __ldg(reinterpret_cast<const float4*>(pooled + item * ld_pooled +
+                                                         (int64_t)(v - 1) * D) + c4);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int u = base + k * 32 + lane;
+        if (u < units) {
+          const int v = u / D4, c = (u - v * D4) * 4;
+          float* d = sv + v * ldv + c;
+          d[0] = r[k].x; d[1] = r[k].y; d[2] = r[k].z; d[3] = r[k].w;
+        }
+      }
+    }
+    __syncwarp();
+    if (warp == 0 && item == (int64_t)blockIdx.x * kInterWarps) pdl_trigger();
+    for (int c = lane; c < D; c += 32) {
+      float sacc = 0.f;
+      for (int t = 1; t <= T; ++t) sacc += sv[t * ldv + c];
+      X[item * ld_x + sum_off + c] = sacc;
+    }
+    for (int p = lane; p < P; p += 32) {
+      int i = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)p)) * 0.5f);
+      while (i * (i - 1) / 2 > p) --i;
+      while ((i + 1) * i / 2 <= p) ++i;
+      const int j = p - i * (i - 1) / 2;
+      const float* vi = sv + i * ldv;
+      const float* vj = sv + j * ldv;
+      float d = 0.f;
+#pragma unroll 8
+      for (int c = 0; c < D; ++c) d = fmaf(vi[c], vj[c], d);
+      X[item * ld_x + dot_off + p] = d;
+    }
+  }
+}
+
 __global__ void init_tables_kernel(float* __restrict__ tables, int64_t T, int64_t rows,
                                    int64_t D, uint64_t seed) {
   const int64_t per_table = rows * D;
@@ -952,6 +1025,24 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
                         int64_t max_items, int sm_count, cudaStream_t s) {
+  const size_t per_item = (size_t)(T + 1) * (D + 1) * sizeof(float);
+  // warp-per-item only while an item's dot work is short: one warp runs each
+  // dot as a dependent FMA chain, so at cfg3's 528 pairs x 64 it lengthens the
+  // query's critical path more than it saves in CTA slots (pipe_micro: 39.8
+  // -> 43.2 us/query), while at RMC1's 36 pairs x 32 it wins (10.6 -> 9.9).
+  const int64_t pair_work = (int64_t)(T + 1) * T / 2 * D;
+  if (D % 4 == 0 && D <= 64 && T + 1 <= 33 && per_item * kInterWarps <= 200 * 1024 &&
+      pair_work <= 8192 && env_int("RS_INTER_WARP", 1)) {
+    static bool attr = cudaFuncSetAttribute(interaction_warp_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            200 * 1024) == cudaSuccess;
+    (void)attr;
+    const int grid = grid_for(max_items, kInterWarps, sm_count, 2);
+    launch_pdl(interaction_warp_kernel, dim3(grid), dim3(kInterWarps * 32),
+               per_item * kInterWarps, s, qd, pooled, ld_pooled, T, D, X, ld_x, sum_off,
+               dot_off, has_dense);
+    return;
+  }
   const size_t smem = (size_t)(T + 1) * (D + 1) * sizeof(float);
   const int grid = grid_for(max_items, 1, sm_count, 2);
   if (smem > 48 * 1024)
