@@ -91,6 +91,10 @@ struct Slot {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ready = nullptr, free = nullptr;  // pipelined queue hand-off
   cudaStream_t cap2 = nullptr;                  // capture: parallel graph branch
+  // SM-partitioned slots (rs_forward_many lanes when the device is split):
+  // capture streams on the dense and the gather green contexts
+  cudaStream_t gcap_d = nullptr, gcap_e = nullptr;
+  int emb_sms = 0, dense_sms = 0;  // SMs the gather / dense grids are sized for
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<void*> allocs;
 };
@@ -133,6 +137,10 @@ struct rs_accel {
   std::vector<cudaEvent_t> evpool, evstart;
   std::map<int64_t, double> service_memo;
   rs::BatchMemOpFn memops = nullptr;  // null: pageable-copy descriptor writes
+  // SM partition for the pipelined queue (green contexts): the gathers run
+  // on emb_sms SMs, the latency-bound dense kernels on part_dense_sms.
+  CUgreenCtx g_dense = nullptr, g_emb = nullptr;
+  int part_dense_sms = 0, part_emb_sms = 0;
 };
 
 namespace rs {
@@ -312,20 +320,20 @@ void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off, 
   switch (m.pooling) {
     case RS_POOL_SUM:
       launch_sls_sum(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out + off, ld,
-                     s->d_err, maxS, a->sm_count, st);
+                     s->d_err, maxS, s->emb_sms, st);
       break;
     case RS_POOL_CONCAT:
       launch_gather_concat(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out, ld,
-                           off, s->d_err, maxS, a->sm_count, st);
+                           off, s->d_err, maxS, s->emb_sms, st);
       break;
     case RS_POOL_ATTENTION_FC:
       launch_din_pool(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, a->att_w, out,
-                      ld, off, s->d_err, maxS, a->sm_count, st);
+                      ld, off, s->d_err, maxS, s->emb_sms, st);
       break;
     case RS_POOL_ATTENTION_RNN: {
       GruArgs g = gru_args(a, s, out, ld, off);
       // tensor-core recurrence in the tcgen05 graph, FFMA recurrence otherwise
-      if (!(tc && launch_gru_tc(s->d_q, g, maxS, st))) launch_gru(s->d_q, g, maxS, a->sm_count, st);
+      if (!(tc && launch_gru_tc(s->d_q, g, maxS, st))) launch_gru(s->d_q, g, maxS, s->emb_sms, st);
       break;
     }
   }
@@ -409,7 +417,11 @@ enum GraphKind { kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kNumGraphs = 
 constexpr int64_t kAutoTcMinItems = 128;  // one full UMMA M tile
 
 cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_layers) {
-  cudaStream_t st = s->cap;
+  // A partitioned slot captures the gathers on the gather partition's stream
+  // and everything else on the dense partition's; each kernel node keeps the
+  // green context of the stream it was captured on, so one graph spans both.
+  const bool part = s->gcap_d != nullptr;
+  cudaStream_t st = part ? s->gcap_d : s->cap;
   cudaGraph_t g = nullptr;
   RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   const rs_model_desc& m = a->m;
@@ -417,7 +429,16 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   const bool tc = kind == kGraphLarge;
   int ntc = 0;
   if (kind == kGraphPool) {
-    enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode == RS_FC_TF32, st);
+    if (part && a->T > 0) {
+      RS_CUDA(cudaEventRecord(s->fork, st));
+      RS_CUDA(cudaStreamWaitEvent(s->gcap_e, s->fork, 0));
+      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode == RS_FC_TF32,
+                      s->gcap_e);
+      RS_CUDA(cudaEventRecord(s->join, s->gcap_e));
+      RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
+    } else {
+      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode == RS_FC_TF32, st);
+    }
   } else {
     // diagnostic only (tools/pipe_micro.py): RS_DIAG_SKIP bit 1 drops the
     // bottom MLP, 2 the interaction, 4 the predict stack (outputs invalid)
@@ -425,39 +446,42 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
     const int skip = dsk ? atoi(dsk) : 0;
     // The dense branch (stage_dense + bottom MLP) and the embedding stage
     // are independent (they write disjoint columns of X): capture them as
-    // parallel graph branches.
+    // parallel graph branches. Unpartitioned: the gather on the main stream,
+    // the dense branch forked; partitioned: the gather forked onto the
+    // gather partition, the dense branch on the main (dense) stream.
     const bool dense = a->dense_in > 0;
-    const bool fork = dense && a->T > 0;
+    const bool fork = part ? a->T > 0 : (dense && a->T > 0);
+    cudaStream_t bs = st, es = st;
     if (fork) {
       RS_CUDA(cudaEventRecord(s->fork, st));
-      RS_CUDA(cudaStreamWaitEvent(s->cap2, s->fork, 0));
+      cudaStream_t other = part ? s->gcap_e : s->cap2;
+      RS_CUDA(cudaStreamWaitEvent(other, s->fork, 0));
+      if (part) es = other;
+      else bs = other;
     }
-    cudaStream_t bs = fork ? s->cap2 : st;
     if (dense) {
       if (m.has_dense_fc) {
-        launch_stage_dense(s->d_q, a->dense_in, s->dense_stage, a->ld_dense, maxS, a->sm_count,
+        launch_stage_dense(s->d_q, a->dense_in, s->dense_stage, a->ld_dense, maxS, s->dense_sms,
                            bs);
         if (!(skip & 1))
           ntc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
                                a->max_dense_w, s->X, a->ld_x, 0, tc, bs);
       } else {
-        launch_stage_dense(s->d_q, a->dense_in, s->X, a->ld_x, maxS, a->sm_count, bs);
+        launch_stage_dense(s->d_q, a->dense_in, s->X, a->ld_x, maxS, s->dense_sms, bs);
       }
     }
-    if (fork) RS_CUDA(cudaEventRecord(s->join, s->cap2));
+    if (fork && !part) RS_CUDA(cudaEventRecord(s->join, bs));
     if (m.pooling == RS_POOL_SUM) {
-      if (a->T > 0) {
-        enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, tc, st);
-        if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
-        if (!(skip & 2))
-          launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
-                           a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
-                           a->sm_count, st);
-      }
+      if (a->T > 0) enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, tc, es);
     } else {
-      enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, tc, st);
-      if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
+      enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, tc, es);
     }
+    if (fork && part) RS_CUDA(cudaEventRecord(s->join, es));
+    if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
+    if (m.pooling == RS_POOL_SUM && a->T > 0 && !(skip & 2))
+      launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
+                         a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
+                         s->dense_sms, st);
     if (const char* de = getenv("RS_DIAG_EMPTY")) {
       const char* dc = getenv("RS_DIAG_EMPTY_CTAS");
       launch_diag_empty(atoi(de), dc ? atoi(dc) : 1, st);
@@ -491,11 +515,86 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   return exec;
 }
 
-std::unique_ptr<Slot> make_slot(rs_accel* a) {
+// Green-context entry points (driver API, fetched at run time: no -lcuda).
+struct GreenApi {
+  CUresult (*get_res)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned,
+                    unsigned) = nullptr;
+  CUresult (*gen_desc)(CUdevResourceDesc*, CUdevResource*, unsigned) = nullptr;
+  CUresult (*create)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+  CUresult (*destroy)(CUgreenCtx) = nullptr;
+  CUresult (*stream)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+  bool ok = false;
+};
+
+const GreenApi& green_api() {
+  static GreenApi g = [] {
+    GreenApi r;
+    auto get = [](const char* name) -> void* {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        return nullptr;
+      return p;
+    };
+    r.get_res = reinterpret_cast<decltype(r.get_res)>(get("cuDeviceGetDevResource"));
+    r.split = reinterpret_cast<decltype(r.split)>(get("cuDevSmResourceSplitByCount"));
+    r.gen_desc = reinterpret_cast<decltype(r.gen_desc)>(get("cuDevResourceGenerateDesc"));
+    r.create = reinterpret_cast<decltype(r.create)>(get("cuGreenCtxCreate"));
+    r.destroy = reinterpret_cast<decltype(r.destroy)>(get("cuGreenCtxDestroy"));
+    r.stream = reinterpret_cast<decltype(r.stream)>(get("cuGreenCtxStreamCreate"));
+    r.ok = r.get_res && r.split && r.gen_desc && r.create && r.destroy && r.stream;
+    return r;
+  }();
+  return g;
+}
+
+// Split the device for the pipelined queue: `dense_sms` SMs (a multiple of 8
+// on sm_90+) for the latency-bound dense kernels, the rest for the gathers.
+// Returns false (queue stays unpartitioned) if green contexts are unavailable.
+bool make_partition(rs_accel* a, int dense_sms) {
+  const GreenApi& ga = green_api();
+  if (!ga.ok || dense_sms <= 0) return false;
+  CUdevResource all, grp, rest;
+  unsigned n = 1;
+  if (ga.get_res((CUdevice)a->device, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return false;
+  if (ga.split(&grp, &n, &all, &rest, 0, (unsigned)dense_sms) != CUDA_SUCCESS || n != 1)
+    return false;
+  CUdevResourceDesc dd, de;
+  if (ga.gen_desc(&dd, &grp, 1) != CUDA_SUCCESS || ga.gen_desc(&de, &rest, 1) != CUDA_SUCCESS)
+    return false;
+  if (ga.create(&a->g_dense, dd, (CUdevice)a->device, CU_GREEN_CTX_DEFAULT_STREAM) !=
+      CUDA_SUCCESS)
+    return false;
+  if (ga.create(&a->g_emb, de, (CUdevice)a->device, CU_GREEN_CTX_DEFAULT_STREAM) !=
+      CUDA_SUCCESS) {
+    ga.destroy(a->g_dense);
+    a->g_dense = nullptr;
+    return false;
+  }
+  a->part_dense_sms = (int)grp.sm.smCount;
+  a->part_emb_sms = (int)rest.sm.smCount;
+  return true;
+}
+
+std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   RS_CUDA(cudaSetDevice(a->device));
   auto s = std::make_unique<Slot>();
   const int64_t maxS = a->init.max_query_size;
   RS_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
+  s->emb_sms = s->dense_sms = a->sm_count;
+  if (partitioned && a->g_dense) {
+    const GreenApi& ga = green_api();
+    CUstream sd = nullptr, se = nullptr;
+    if (ga.stream(&sd, a->g_dense, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+        ga.stream(&se, a->g_emb, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+      raise(RS_E_CUDA, "cuGreenCtxStreamCreate failed");
+    s->gcap_d = reinterpret_cast<cudaStream_t>(sd);
+    s->gcap_e = reinterpret_cast<cudaStream_t>(se);
+    s->emb_sms = a->part_emb_sms;
+    s->dense_sms = a->part_dense_sms;
+  }
   s->d_q = static_cast<QDesc*>(dmalloc(a, s->allocs, sizeof(QDesc)));
   RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_q), sizeof(QDesc) * kDescRing,
                         cudaHostAllocPortable));
@@ -547,7 +646,7 @@ Slot* get_slot(rs_accel* a, cudaStream_t st) {
 // The two slots of the pipelined host-input queue (rs_forward_many).
 Slot* get_pipe_slot(rs_accel* a, int i) {
   std::lock_guard<std::mutex> lock(a->mu);
-  if (!a->pipe[i]) a->pipe[i] = make_slot(a);
+  if (!a->pipe[i]) a->pipe[i] = make_slot(a, /*partitioned=*/true);
   if (!a->copy) RS_CUDA(cudaStreamCreateWithFlags(&a->copy, cudaStreamNonBlocking));
   if (!a->lane[i]) {
     RS_CUDA(cudaStreamCreateWithFlags(&a->lane[i], cudaStreamNonBlocking));
@@ -570,6 +669,8 @@ void free_slot(Slot* s) {
   if (s->cap2) cudaStreamDestroy(s->cap2);
   if (s->fork) cudaEventDestroy(s->fork);
   if (s->join) cudaEventDestroy(s->join);
+  if (s->gcap_d) cudaStreamDestroy(s->gcap_d);
+  if (s->gcap_e) cudaStreamDestroy(s->gcap_e);
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -927,6 +1028,7 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     RS_CUDA(cudaEventCreateWithFlags(&a->copy_gate, cudaEventDisableTiming));
     build_model(a);
     a->memops = probe_memops(a);
+    if (const char* ds = getenv("RS_DENSE_SMS")) make_partition(a, atoi(ds));
     *out = a;
   });
   if (rc != RS_OK && a) {
@@ -956,6 +1058,8 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
     }
     for (void* p : a->allocs) cudaFree(p);
     if (a->own) cudaStreamDestroy(a->own);
+    if (a->g_dense) green_api().destroy(a->g_dense);
+    if (a->g_emb) green_api().destroy(a->g_emb);
     delete a;
   });
 }

@@ -860,6 +860,7 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
     return b > 0 ? b : 1;
   }();
   const int grid = grid_for(max_items * T, kWarps, sm_count, 2 * per_sm);
+  max_carveout(reinterpret_cast<const void*>(sls_pipe_kernel<LPR, VPL, U, IPL>));
   sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, kWarps * 32, 0, s>>>(
       qd, tables, rows, T, L, out, ld_out, err, env_int("RS_SLS_TRIGGER", 0));
 }
@@ -910,6 +911,7 @@ bool launch_sls_stage(const QDesc* qd, const float* tables, int64_t rows, int T,
                                                 smem);
   if (per_sm < 1) return false;
   const int grid = grid_for(max_items * T, nw, sm_count, per_sm);
+  max_carveout(reinterpret_cast<const void*>(sls_stage_kernel<LPR, VPL, IPL>));
   sls_stage_kernel<LPR, VPL, IPL><<<grid, nw * 32, smem, s>>>(qd, tables, rows, T, L, nbuf, out,
                                                               ld_out, err);
   return true;
@@ -936,6 +938,7 @@ void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, i
     return b > 0 ? b : 1;
   }();
   const int grid = grid_for(max_items * T, kWarps, sm_count, 2 * per_sm);
+  max_carveout(reinterpret_cast<const void*>(sls_sum_kernel<LPR, VPL, U>));
   sls_sum_kernel<LPR, VPL, U><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out,
                                                            err, 0);
 }
@@ -956,6 +959,7 @@ bool launch_sls_tma(const QDesc* qd, const float* tables, int64_t rows, int T, i
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sls_tma_kernel<LPR, VPL, NBUF>, 32, smem);
   if (per_sm < 1) return false;
   const int grid = grid_for(max_items * T, 1, sm_count, per_sm);
+  max_carveout(reinterpret_cast<const void*>(sls_tma_kernel<LPR, VPL, NBUF>));
   sls_tma_kernel<LPR, VPL, NBUF><<<grid, 32, smem, s>>>(qd, map, rows, T, L, LB, out, ld_out,
                                                         err);
   return true;
@@ -988,6 +992,7 @@ void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, i
     case 256: RS_SLS(32, 2); break;
     default: {
       const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
+      max_carveout(reinterpret_cast<const void*>(sls_sum_scalar_kernel));
       sls_sum_scalar_kernel<<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, D, out, ld_out,
                                                          err);
     }
@@ -1001,6 +1006,7 @@ void launch_gather_concat(const QDesc* qd, const float* tables, int64_t rows, in
   const int vec = (D % 4 == 0 && col_off % 4 == 0 && ld_out % 4 == 0) ? 1 : 0;
   const int64_t units = max_items * T * L * (vec ? D / 4 : D);
   const int grid = grid_for(units, 256, sm_count, 8);
+  max_carveout(reinterpret_cast<const void*>(gather_concat_kernel));
   gather_concat_kernel<<<grid, 256, 0, s>>>(qd, tables, rows, T, L, D, out, ld_out, col_off,
                                             vec, err);
 }
@@ -1013,12 +1019,12 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
   const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
   const dim3 blk(kWarps * 32);
   switch (D) {
-    case 8: din_pool_kernel<2, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 16: din_pool_kernel<4, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 32: din_pool_kernel<8, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 64: din_pool_kernel<16, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 128: din_pool_kernel<32, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
-    case 256: din_pool_kernel<32, 2, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 8: max_carveout(reinterpret_cast<const void*>(din_pool_kernel<2, 1, 4>)); din_pool_kernel<2, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 16: max_carveout(reinterpret_cast<const void*>(din_pool_kernel<4, 1, 4>)); din_pool_kernel<4, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 32: max_carveout(reinterpret_cast<const void*>(din_pool_kernel<8, 1, 4>)); din_pool_kernel<8, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 64: max_carveout(reinterpret_cast<const void*>(din_pool_kernel<16, 1, 4>)); din_pool_kernel<16, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 128: max_carveout(reinterpret_cast<const void*>(din_pool_kernel<32, 1, 4>)); din_pool_kernel<32, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
+    case 256: max_carveout(reinterpret_cast<const void*>(din_pool_kernel<32, 2, 4>)); din_pool_kernel<32, 2, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
   }
 }
 

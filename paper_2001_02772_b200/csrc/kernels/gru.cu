@@ -242,6 +242,8 @@ void launch_gru(const QDesc* qd, const GruArgs& g, int64_t max_items, int sm_cou
   const dim3 grid((unsigned)((max_items + nseq - 1) / nseq), g.T);
   const bool ws = use_wsmem(g);
   const size_t smem = gru_smem(g.D, g.H, ws);
+  max_carveout(reinterpret_cast<const void*>(gru_kernel<true>));
+  max_carveout(reinterpret_cast<const void*>(gru_kernel<false>));
   if (ws) gru_kernel<true><<<grid, gru_threads(g.H), smem, s>>>(qd, g);
   else gru_kernel<false><<<grid, gru_threads(g.H), smem, s>>>(qd, g);
 }

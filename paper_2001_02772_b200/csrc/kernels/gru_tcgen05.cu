@@ -288,6 +288,7 @@ void launch_typed(const QDesc* qd, const GruArgs& g, int64_t max_items, cudaStre
                          (int)smem);
   });
   const dim3 grid((unsigned)((max_items + kSeq - 1) / kSeq), g.T);
+  max_carveout(reinterpret_cast<const void*>(gru_tc_kernel<D, H>));
   gru_tc_kernel<D, H><<<grid, kThreads, smem, s>>>(qd, g);
 }
 
