@@ -338,6 +338,120 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
   }
 }
 
+// Variant 4 (RS_SLS_VARIANT=4): variant 2 without the bubble between bags.
+// A warp's bags are one continuous stream of row batches: batch t+1 is issued
+// before batch t is summed even when t+1 is the first batch of the warp's
+// next bag, so the rows in flight per warp never drop to zero at a bag
+// boundary (variant 2 pays one dependent round trip per bag there, and at
+// the end of a launch every warp's last bags are exactly that chain).
+// Index lists are double-buffered in shared memory; bag k's list is staged
+// when its first batch is issued, from registers fetched one bag earlier.
+// Same per-lane accumulation order as sls_sum_kernel: bit-identical.
+template <int LPR, int VPL, int U, int IPL>
+__global__ void __launch_bounds__(kWarps * 32)
+sls_stream_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
+                  int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err) {
+  constexpr int R = 32 / LPR;
+  constexpr int D = LPR * 4 * VPL;
+  constexpr int B = R * U;  // rows per batch
+  __shared__ int64_t sidx[kWarps][2][32 * IPL];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPR, c = lane % LPR;
+  const int64_t bags = qd->S * T;
+  const int64_t* __restrict__ idx = qd->idx;
+  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  const int64_t bag0 = (int64_t)blockIdx.x * kWarps + warp;
+  if (bag0 >= bags) return;
+  const int64_t nbags = (bags - bag0 + stride - 1) / stride;
+  const int nb = (L + B - 1) / B;  // batches per bag
+  const int64_t total = nbags * nb;
+  int64_t nidx[IPL];
+  auto fetch_idx = [&](int64_t bag) {
+#pragma unroll
+    for (int q = 0; q < IPL; ++q) {
+      const int l = q * 32 + lane;
+      nidx[q] = (bag < bags && l < L) ? __ldg(idx + bag * L + l) : 0;
+    }
+  };
+  fetch_idx(bag0);
+  // issue batch t into v (t = k*nb + jb: rows jb*B.. of the warp's k-th bag)
+  auto load = [&](int64_t t, float4 (&v)[U][VPL], bool (&ok)[U]) {
+    const int64_t k = t / nb;
+    const int jb = (int)(t - k * nb);
+    const int64_t bag = bag0 + k * stride;
+    int64_t* si = sidx[warp][k & 1];
+    if (jb == 0) {
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < IPL; ++q) si[q * 32 + lane] = nidx[q];
+      __syncwarp();
+      fetch_idx(bag + stride);  // flies while this bag's rows stream
+    }
+    const int t_ = (int)(bag % T);
+    const float4* __restrict__ tab =
+        reinterpret_cast<const float4*>(tables + (int64_t)t_ * rows * D);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int l = jb * B + u * R + g;
+      ok[u] = false;
+      if (l < L) {
+        const int64_t r = si[l];
+        if ((uint64_t)r < (uint64_t)rows) {
+          ok[u] = true;
+          const float4* p = tab + r * (D / 4) + c;
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) v[u][q] = ldg_stream(p + q * LPR);
+        } else {
+          atomicOr(err, kErrIndex);
+        }
+      }
+    }
+  };
+  float4 acc[VPL];
+  // sum batch t; at a bag's last batch reduce across lane groups and store
+  auto consume = [&](int64_t t, const float4 (&v)[U][VPL], const bool (&ok)[U]) {
+    const int64_t k = t / nb;
+    const int jb = (int)(t - k * nb);
+    if (jb == 0) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) add4(acc[q], v[u][q]);
+      }
+    if (jb == nb - 1) {
+      float4 r[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) r[q] = acc[q];
+#pragma unroll
+      for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) add4(r[q], shfl_xor4(r[q], off));
+      if (g == 0) {
+        const int64_t bag = bag0 + k * stride;
+        const int t_ = (int)(bag % T);
+        float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t_ * D) + c;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) o[q * LPR] = r[q];
+      }
+    }
+  };
+  float4 va[U][VPL], vb[U][VPL];
+  bool oa[U], ob[U];
+  load(0, va, oa);
+  for (int64_t t = 0; t < total; t += 2) {
+    if (t + 1 < total) load(t + 1, vb, ob);
+    consume(t, va, oa);
+    if (t + 1 < total) {
+      if (t + 2 < total) load(t + 2, va, oa);
+      consume(t + 1, vb, ob);
+    }
+  }
+}
+
 // Variant 3 (RS_SLS_VARIANT=3): warp-per-bag with whole bags staged in shared
 // memory by cp.async. A warp issues 16-byte cp.async copies for EVERY row of
 // its next bag (nbuf-1 bags ahead) before it sums the current one, so a bag's
@@ -865,6 +979,41 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
       qd, tables, rows, T, L, out, ld_out, err, env_int("RS_SLS_TRIGGER", 0));
 }
 
+template <int LPR, int VPL, int U, int IPL>
+void launch_sls_stream(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                       float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                       cudaStream_t s) {
+  static const int per_sm = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_stream_kernel<LPR, VPL, U, IPL>,
+                                                  kWarps * 32, 0);
+    return b > 0 ? b : 1;
+  }();
+  const int grid = grid_for(max_items * T, kWarps, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
+  max_carveout(reinterpret_cast<const void*>(sls_stream_kernel<LPR, VPL, U, IPL>));
+  sls_stream_kernel<LPR, VPL, U, IPL><<<grid, kWarps * 32, 0, s>>>(qd, tables, rows, T, L, out,
+                                                                   ld_out, err);
+}
+
+template <int LPR, int VPL>
+bool try_sls_stream(const QDesc* qd, const float* tables, int64_t rows, int T, int L, float* out,
+                    int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s) {
+  if (L > 96) return false;
+  const int ub = sls_ub();
+#define RS_STREAM(U, IPL)                                                                \
+  launch_sls_stream<LPR, VPL, U, IPL>(qd, tables, rows, T, L, out, ld_out, err, max_items, \
+                                      sm_count, s)
+  if (L <= 32) {
+    if (ub >= 8) RS_STREAM((VPL == 2 ? 4 : 8), 1);
+    else RS_STREAM((VPL == 2 ? 2 : 4), 1);
+  } else {
+    if (ub >= 8) RS_STREAM((VPL == 2 ? 4 : 8), 3);
+    else RS_STREAM((VPL == 2 ? 2 : 4), 3);
+  }
+#undef RS_STREAM
+  return true;
+}
+
 template <int LPR, int VPL>
 bool try_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L, float* out,
                   int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s) {
@@ -979,6 +1128,9 @@ void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, i
       break;                                                                                \
     if (sls_variant() == 3 && try_sls_stage<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,  \
                                                       err, max_items, sm_count, s))         \
+      break;                                                                                \
+    if (sls_variant() == 4 && try_sls_stream<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, \
+                                                       err, max_items, sm_count, s))        \
       break;                                                                                \
     launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
                                                  max_items, sm_count, s);                   \

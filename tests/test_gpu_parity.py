@@ -264,7 +264,7 @@ def test_forward_many_long_batch_host_runs_ahead(desc_memop, monkeypatch):
     acc.close()
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
 @pytest.mark.parametrize("D,L", [(32, 80), (64, 80), (64, 20), (128, 33), (256, 7)])
 def test_sls_kernel_variants_bit_exact(variant, D, L, monkeypatch):
     """Every SLS kernel variant (RS_SLS_VARIANT) reproduces the oracle's
