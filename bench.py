@@ -296,12 +296,16 @@ def run_ours(args, rank, world, local):
     # pool of 2Q distinct queries: pinned host copies (e2e) and device copies (value)
     P = 2 * Q
     d_dense, d_idx, h_dense, h_idx = [], [], [], []
+    i32 = args.index_bits == 32
+    ity = rs.INDEX_I32 if i32 else rs.INDEX_I64
     for q in range(P):
         dn, ix = rs.fill_query(spec, rows, seed, q, int(sizes[q]))
+        if i32:
+            ix = ix.astype(np.int32)
         hb_d = rs.PinnedBuffer(max(dn.nbytes, 16))
         hb_i = rs.PinnedBuffer(max(ix.nbytes, 16))
         hb_d.view(np.float32, dn.shape)[...] = dn
-        hb_i.view(np.int64, ix.shape)[...] = ix
+        hb_i.view(ix.dtype, ix.shape)[...] = ix
         h_dense.append(hb_d)
         h_idx.append(hb_i)
         d_dense.append(torch.from_numpy(dn).to(device))
@@ -328,7 +332,7 @@ def run_ours(args, rank, world, local):
             ip = [d_idx[q].data_ptr() for q in qs]
             op = [out_dev.data_ptr()] * len(qs)
             loc = rs.MEM_DEVICE
-        return acc.batch([int(sizes[q]) for q in qs], dp, ip, op, loc)
+        return acc.batch([int(sizes[q]) for q in qs], dp, ip, op, loc, index_type=ity)
 
     def serve(batch):
         return acc.forward_many(None, stream=sp, timed=True, residence=True, prepared=batch)
@@ -381,7 +385,7 @@ def run_ours(args, rank, world, local):
     for q in window(0):
         S = int(sizes[q])
         t = acc.pooled_ptr(S, d_idx[q].data_ptr(), pooled_dev.data_ptr(), rs.MEM_DEVICE,
-                           stream=sp, timed=True)
+                           stream=sp, timed=True, index_type=ity)
         sls_ms += t.compute_ms
         sls_bytes += S * sls_bytes_per_item(spec)
     peak, peak_src = measured_peaks()
@@ -389,7 +393,8 @@ def run_ours(args, rank, world, local):
 
     items_step = float(np.mean([sum(int(sizes[q]) for q in window(k)) for k in range(K)]))
     h2d_step = float(np.mean([sum(int(sizes[q]) * (spec.dense_input_dim * 4 +
-                                                   e.num_tables * e.lookups_per_table * 8)
+                                                   e.num_tables * e.lookups_per_table *
+                                                   (4 if i32 else 8))
                                   for q in window(k)) for k in range(K)]))
     d2h_step = float(np.mean([sum(int(sizes[q]) * acc.output_dim * 4 + 4 for q in window(k))
                               for k in range(K)]))
@@ -421,6 +426,9 @@ def run_ours(args, rank, world, local):
                        "dim": e.embedding_dim, "queries_per_step": Q,
                        "items_per_step": items_step, "sla_s": sla,
                        "fc_path": args.fc, "parallelism": f"replicas{world}",
+                       "input_format": ("int32 indices: LABELLED variant (SURVEY 8f-2), not "
+                                        "the reference byte model" if i32 else
+                                        "reference byte model (int64 indices + fp32 dense)"),
                        "l2": "inputs >> L2 (tables %.1f GB, ~%.0f MB of indices per step)" % (
                            acc.info.table_bytes / 1e9, h2d_step / 1e6),
                        "qps_method": "open-loop Poisson replay (n=50,000, sim.hpp:79) of the "
@@ -475,6 +483,8 @@ def main():
                          "ncf | wnd | mt-wnd | rmc1 | rmc2 | rmc3 | din | dien")
     ap.add_argument("--sla", type=float, default=0.0, help="override SLA seconds")
     ap.add_argument("--queries-per-step", type=int, default=256)
+    ap.add_argument("--index-bits", type=int, choices=[64, 32], default=64,
+                    help="32 = labelled int32-index input variant (SURVEY 8f-2)")
     ap.add_argument("--max-query", type=int, default=1000)
     ap.add_argument("--fc", choices=["fp32", "tf32", "auto"], default="auto")
     ap.add_argument("--no-cpu", action="store_true")

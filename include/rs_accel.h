@@ -191,14 +191,19 @@ typedef struct rs_init_desc {
  * i64[S * num_tables * lookups_per_table] (item-major, then table, then
  * lookup) — the byte model of accel_input_bytes (platform.cpp:105-111).
  * location RS_MEM_HOST: pointers are host memory (pinned for async copy);
- * RS_MEM_DEVICE: pointers are device memory on the handle's GPU.           */
+ * RS_MEM_DEVICE: pointers are device memory on the handle's GPU.
+ * index_type RS_INDEX_I32 is a LABELLED input-format variant (SURVEY
+ * §8f-2): `indices` then points at int32 values (half the host-link bytes);
+ * they are widened on the device and the forward is bit-identical to the
+ * int64 query with the same values. Default RS_INDEX_I64 = the reference.  */
 enum { RS_MEM_HOST = 0, RS_MEM_DEVICE = 1 };
+enum { RS_INDEX_I64 = 0, RS_INDEX_I32 = 1 };
 typedef struct rs_query {
   int64_t size;
   const float* dense;
-  const int64_t* indices;
+  const int64_t* indices;   /* int32_t* when index_type == RS_INDEX_I32 */
   int32_t location;
-  int32_t reserved;
+  int32_t index_type;       /* RS_INDEX_* (0 = int64, the reference)    */
 } rs_query;
 
 /* Per-call timing (CUDA events on the call's stream), milliseconds.        */

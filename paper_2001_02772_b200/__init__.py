@@ -100,6 +100,7 @@ OP_CATEGORIES = ["DenseFC", "PredictFC", "EmbeddingLookup", "Pooling", "Attentio
 FC_FP32, FC_TF32, FC_AUTO = 0, 1, 2
 RNN_GRU, RNN_AUGRU = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
+INDEX_I64, INDEX_I32 = 0, 1  # rs_query.index_type (I32: labelled input variant)
 
 
 class CLayerStack(C.Structure):
@@ -139,7 +140,7 @@ class CInitDesc(C.Structure):
 
 class CQuery(C.Structure):
     _fields_ = [("size", C.c_int64), ("dense", C.c_void_p), ("indices", C.c_void_p),
-                ("location", C.c_int32), ("reserved", C.c_int32)]
+                ("location", C.c_int32), ("index_type", C.c_int32)]
 
 
 class CTiming(C.Structure):
@@ -487,34 +488,38 @@ class Accelerator:
         except Exception:
             pass
 
-    def _query(self, size, dense_ptr, idx_ptr, location) -> CQuery:
-        return CQuery(size, dense_ptr, idx_ptr, location, 0)
+    def _query(self, size, dense_ptr, idx_ptr, location, index_type=INDEX_I64) -> CQuery:
+        return CQuery(size, dense_ptr, idx_ptr, location, index_type)
 
     def forward_ptr(self, size: int, dense_ptr: int, idx_ptr: int, out_ptr: int,
-                    location: int, stream: int = 0, timed: bool = False):
-        """Raw-pointer call (host pinned or device memory), the C-ABI as is."""
-        q = self._query(size, dense_ptr, idx_ptr, location)
+                    location: int, stream: int = 0, timed: bool = False,
+                    index_type: int = 0):
+        """Raw-pointer call (host pinned or device memory), the C-ABI as is.
+        index_type INDEX_I32: `idx_ptr` holds int32 (labelled input variant)."""
+        q = self._query(size, dense_ptr, idx_ptr, location, index_type)
         t = CTiming()
         _check(_lib.rs_forward(self._h, C.byref(q), out_ptr, stream or None,
                                C.byref(t) if timed else None))
         return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms) if timed else None
 
     def pooled_ptr(self, size: int, idx_ptr: int, out_ptr: int, location: int,
-                   stream: int = 0, timed: bool = False, dense_ptr: int = 0):
-        q = self._query(size, dense_ptr, idx_ptr, location)
+                   stream: int = 0, timed: bool = False, dense_ptr: int = 0,
+                   index_type: int = 0):
+        q = self._query(size, dense_ptr, idx_ptr, location, index_type)
         t = CTiming()
         _check(_lib.rs_pooled(self._h, C.byref(q), out_ptr, stream or None,
                               C.byref(t) if timed else None))
         return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms) if timed else None
 
     @staticmethod
-    def batch(sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int):
+    def batch(sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int, index_type: int = 0):
         """Pre-built argument arrays for forward_many (keeps Python work out of
         timed regions)."""
         n = len(sizes)
         qs = (CQuery * n)()
         for i in range(n):
-            qs[i] = CQuery(int(sizes[i]), dense_ptrs[i] or None, idx_ptrs[i] or None, location, 0)
+            qs[i] = CQuery(int(sizes[i]), dense_ptrs[i] or None, idx_ptrs[i] or None, location,
+                           index_type)
         outs = (C.c_void_p * n)(*[C.c_void_p(p) for p in out_ptrs])
         return n, qs, outs
 
@@ -538,20 +543,24 @@ class Accelerator:
         _check(_lib.rs_sync(self._h, stream or None))
 
     def forward(self, dense: np.ndarray, idx: np.ndarray) -> np.ndarray:
-        """Host numpy in, host numpy out (synchronous): logits [S, stacks*out]."""
+        """Host numpy in, host numpy out (synchronous): logits [S, stacks*out].
+        int32 `idx` selects the labelled INDEX_I32 input variant."""
         S = int(idx.shape[0]) if idx.size else int(dense.shape[0])
         dense = np.ascontiguousarray(dense, dtype=np.float32)
-        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        i32 = idx.dtype == np.int32
+        idx = np.ascontiguousarray(idx, dtype=np.int32 if i32 else np.int64)
         out = np.empty((S, self.output_dim), dtype=np.float32)
         self.forward_ptr(S, dense.ctypes.data, idx.ctypes.data, out.ctypes.data, MEM_HOST,
-                         timed=True)
+                         timed=True, index_type=INDEX_I32 if i32 else INDEX_I64)
         return out
 
     def pooled(self, idx: np.ndarray, dense: Optional[np.ndarray] = None) -> np.ndarray:
         S = int(idx.shape[0])
-        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        i32 = idx.dtype == np.int32
+        idx = np.ascontiguousarray(idx, dtype=np.int32 if i32 else np.int64)
         out = np.empty((S, self.pooled_dim), dtype=np.float32)
-        self.pooled_ptr(S, idx.ctypes.data, out.ctypes.data, MEM_HOST, timed=True)
+        self.pooled_ptr(S, idx.ctypes.data, out.ctypes.data, MEM_HOST, timed=True,
+                        index_type=INDEX_I32 if i32 else INDEX_I64)
         return out
 
     def service_time(self, query_size: int) -> float:

@@ -80,6 +80,7 @@ struct Slot {
   float* dense_stage = nullptr;
   float* dense_raw = nullptr;   // contiguous H2D landing zone for strided dense
   int64_t* idx_stage = nullptr;
+  int32_t* idx32_stage = nullptr;  // H2D landing zone of RS_INDEX_I32 queries
   float* act[2] = {nullptr, nullptr};
   float* pooled = nullptr;
   float* X = nullptr;
@@ -132,6 +133,7 @@ struct rs_accel {
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t lane_join[kMaxLanes] = {};
   cudaStream_t copy = nullptr;
+  cudaStream_t copy_more[3] = {};  // further copy streams: queries rotate (RS_COPY_STREAMS)
   cudaEvent_t copy_gate = nullptr;
   std::mutex many_mu;
   std::vector<cudaEvent_t> evpool, evstart;
@@ -607,6 +609,8 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
       dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->dense_in, 1) * 4), false));
   s->idx_stage = static_cast<int64_t*>(
       dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->T * a->L, 1) * 8)));
+  s->idx32_stage = static_cast<int32_t*>(
+      dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->T * a->L, 1) * 4), false));
   for (int i = 0; i < 2; ++i) {
     s->act[i] = static_cast<float*>(
         dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->max_dense_w, 4) * 4)));
@@ -648,6 +652,8 @@ Slot* get_pipe_slot(rs_accel* a, int i) {
   std::lock_guard<std::mutex> lock(a->mu);
   if (!a->pipe[i]) a->pipe[i] = make_slot(a, /*partitioned=*/true);
   if (!a->copy) RS_CUDA(cudaStreamCreateWithFlags(&a->copy, cudaStreamNonBlocking));
+  for (auto& c : a->copy_more)
+    if (!c) RS_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
   if (!a->lane[i]) {
     RS_CUDA(cudaStreamCreateWithFlags(&a->lane[i], cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&a->lane_join[i], cudaEventDisableTiming));
@@ -686,6 +692,8 @@ void check_query(rs_accel* a, const rs_query* q) {
   if (q->location != RS_MEM_HOST && q->location != RS_MEM_DEVICE)
     raise(RS_E_INVALID, "bad memory location");
   if (a->T > 0 && !q->indices) raise(RS_E_INVALID, "null indices");
+  if (q->index_type != RS_INDEX_I64 && q->index_type != RS_INDEX_I32)
+    raise(RS_E_INVALID, "bad index_type");
 }
 
 // Stage one query's inputs for slot s on stream st: dense features into the
@@ -756,8 +764,21 @@ BatchMemOpFn probe_memops(rs_accel* a) {
 // The descriptor carries the item count and the dense / index / output
 // pointers; the graph's stage_dense kernel places the dense rows, and for a
 // device output buffer the final FC layer writes the logits straight into it.
+// RS_INDEX_I32: widen the slot's int32 indices (landing zone, or the caller's
+// device buffer) into the int64 staging buffer on stream st.
+void widen_indices(rs_accel* a, Slot* s, const rs_query* q, cudaStream_t st) {
+  if (a->T == 0 || q->index_type != RS_INDEX_I32) return;
+  const int64_t n = q->size * a->T * a->L;
+  const int32_t* src = q->location == RS_MEM_HOST ? s->idx32_stage
+                                                  : reinterpret_cast<const int32_t*>(q->indices);
+  launch_widen_idx(src, s->idx_stage, n, a->sm_count, st);
+}
+
+// `widen_later`: the caller launches widen_indices itself on its compute
+// stream (the pipelined queue keeps kernels off the copy stream, where one
+// would wait for SM slots and stall the next query's transfer).
 void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream_t st,
-                  float* out = nullptr) {
+                  float* out = nullptr, bool widen_later = false) {
   const int64_t S = q->size;
   const bool host = q->location == RS_MEM_HOST;
   QDesc v{};
@@ -775,9 +796,17 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
   if (full && !host) v.out = out;
   const int64_t* idx = nullptr;
   if (a->T > 0) {
-    if (host) {
-      RS_CUDA(cudaMemcpyAsync(s->idx_stage, q->indices, (size_t)(S * a->T * a->L * 8),
-                              cudaMemcpyHostToDevice, st));
+    const int64_t n = S * a->T * a->L;
+    if (q->index_type == RS_INDEX_I32) {
+      // labelled variant: int32 over the link (or in place), widened on device
+      if (host)
+        RS_CUDA(cudaMemcpyAsync(s->idx32_stage, q->indices, (size_t)(n * 4),
+                                cudaMemcpyHostToDevice, st));
+      if (!widen_later) widen_indices(a, s, q, st);
+      idx = s->idx_stage;
+    } else if (host) {
+      RS_CUDA(cudaMemcpyAsync(s->idx_stage, q->indices, (size_t)(n * 8), cudaMemcpyHostToDevice,
+                              st));
       idx = s->idx_stage;
     } else {
       idx = q->indices;
@@ -903,7 +932,13 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     for (int d = 0; d < depth; ++d) p[d] = get_pipe_slot(a, d);
     RS_CUDA(cudaEventRecord(a->copy_gate, st));
     for (int d = 0; d < depth; ++d) RS_CUDA(cudaStreamWaitEvent(a->lane[d], a->copy_gate, 0));
-    if (loc == RS_MEM_HOST) RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
+    // host inputs: one copy stream, or two alternating so one query's
+    // per-transfer fixed costs overlap the other's transfer
+    const char* cs = getenv("RS_COPY_STREAMS");
+    const int ncopy = cs ? std::min(4, std::max(1, atoi(cs))) : 2;
+    cudaStream_t copies[4] = {a->copy, a->copy_more[0], a->copy_more[1], a->copy_more[2]};
+    if (loc == RS_MEM_HOST)
+      for (int c = 0; c < ncopy; ++c) RS_CUDA(cudaStreamWaitEvent(copies[c], a->copy_gate, 0));
     // diagnostic (tools): RS_MANY_POOL_ONLY=1 runs only the embedding-stage
     // graph per query (outputs are the pooled rows), to separate the
     // gather's pipelined throughput from the FC tail's
@@ -917,11 +952,13 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
       if (service_ms && i >= kEvRing) harvest(i - kEvRing);
       cudaEvent_t ev_start = latency_ms ? a->evstart[i % kEvRing] : nullptr;
       if (loc == RS_MEM_HOST) {
-        RS_CUDA(cudaStreamWaitEvent(a->copy, s->free, 0));
-        if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, a->copy));
-        stage_inputs(a, s, &qs[i], true, a->copy);
-        RS_CUDA(cudaEventRecord(s->ready, a->copy));
+        cudaStream_t cp = copies[i % ncopy];
+        RS_CUDA(cudaStreamWaitEvent(cp, s->free, 0));
+        if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, cp));
+        stage_inputs(a, s, &qs[i], true, cp, nullptr, /*widen_later=*/true);
+        RS_CUDA(cudaEventRecord(s->ready, cp));
         RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
+        widen_indices(a, s, &qs[i], ls);
       } else {
         if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, ls));
         stage_inputs(a, s, &qs[i], true, ls, outs[i]);
@@ -1052,6 +1089,8 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
     for (auto e : a->evstart) cudaEventDestroy(e);
     if (a->copy_gate) cudaEventDestroy(a->copy_gate);
     if (a->copy) cudaStreamDestroy(a->copy);
+    for (auto c : a->copy_more)
+      if (c) cudaStreamDestroy(c);
     for (int d = 0; d < rs_accel::kMaxLanes; ++d) {
       if (a->lane[d]) cudaStreamDestroy(a->lane[d]);
       if (a->lane_join[d]) cudaEventDestroy(a->lane_join[d]);

@@ -1248,6 +1248,28 @@ void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t l
   launch_pdl(stage_dense_kernel, dim3(grid), dim3(256), 0, s, qd, dense_in, dst, ld_dst);
 }
 
+// int32 -> int64 index widening for the RS_INDEX_I32 input variant
+// (sign-extending: an out-of-range index stays out of range and is reported).
+__global__ void __launch_bounds__(256)
+widen_idx_kernel(const int32_t* __restrict__ src, int64_t* __restrict__ dst, int64_t n) {
+  const int64_t n4 = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) ? n / 4 : 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v = __ldg(reinterpret_cast<const int4*>(src) + i);
+    reinterpret_cast<longlong2*>(dst)[2 * i] = make_longlong2(v.x, v.y);
+    reinterpret_cast<longlong2*>(dst)[2 * i + 1] = make_longlong2(v.z, v.w);
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (int64_t)__ldg(src + i);
+}
+
+void launch_widen_idx(const int32_t* src, int64_t* dst, int64_t n, int sm_count,
+                      cudaStream_t s) {
+  const int grid = grid_for((n + 3) / 4, 256, sm_count, 4);
+  widen_idx_kernel<<<grid, 256, 0, s>>>(src, dst, n);
+}
+
 // Diagnostic (RS_DIAG_EMPTY, tools/pipe_micro.py): n empty grids of `ctas`
 // CTAs, to measure the per-kernel cost inside the pipelined forward.
 __global__ void diag_empty_kernel() {

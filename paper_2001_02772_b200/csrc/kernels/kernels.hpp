@@ -21,6 +21,7 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
                      const float* att_w, float* out, int64_t ld_out, int64_t col_off, int* err,
                      int64_t max_items, int sm_count, cudaStream_t s);
 void launch_diag_empty(int n, int ctas, cudaStream_t s);
+void launch_widen_idx(const int32_t* src, int64_t* dst, int64_t n, int sm_count, cudaStream_t s);
 void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t ld_dst,
                         int64_t max_items, int sm_count, cudaStream_t s);
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,

@@ -279,3 +279,37 @@ def test_sls_kernel_variants_bit_exact(variant, D, L, monkeypatch):
         _, idx = rs.fill_query(spec, rows, 6, S, S)
         assert np.array_equal(acc.pooled(idx), orc.sls_canonical(idx)), (variant, D, L, S)
     acc.close()
+
+
+@pytest.mark.parametrize("name", ["DLRM-RMC2", "DIN", "WND"])
+def test_int32_index_variant_is_bit_identical(name):
+    """RS_INDEX_I32 (labelled input-format variant): int32
+    indices over the link, widened on the device — the same logits and pooled
+    rows as the int64 query, host and device paths, and bad indices still
+    reported."""
+    torch = pytest.importorskip("torch")
+    spec = rs.builtin_model(name)
+    rows = 7000
+    acc = rs.Accelerator(spec, rows, seed=5, max_query_size=300, fc_mode=rs.FC_AUTO)
+    for S in (3, 150, 300):
+        dense, idx = rs.fill_query(spec, rows, 8, S, S)
+        ref = acc.forward(dense, idx)
+        assert np.array_equal(acc.forward(dense, idx.astype(np.int32)), ref)
+        assert np.array_equal(acc.pooled(idx.astype(np.int32)), acc.pooled(idx))
+        d_dense = torch.from_numpy(dense).cuda()
+        d_idx32 = torch.from_numpy(idx.astype(np.int32)).cuda()
+        out = torch.empty((S, acc.output_dim), device="cuda")
+        acc.forward_ptr(S, d_dense.data_ptr(), d_idx32.data_ptr(), out.data_ptr(), rs.MEM_DEVICE,
+                        index_type=rs.INDEX_I32)
+        acc.sync()
+        assert np.array_equal(out.cpu().numpy(), ref)
+        b = acc.batch([S, S], [d_dense.data_ptr()] * 2, [d_idx32.data_ptr()] * 2,
+                      [out.data_ptr()] * 2, rs.MEM_DEVICE, index_type=rs.INDEX_I32)
+        acc.forward_many(None, prepared=b)
+        assert np.array_equal(out.cpu().numpy(), ref)
+    dense, idx = rs.fill_query(spec, rows, 8, 1, 4)
+    bad = idx.astype(np.int32)
+    bad[1, 0, 0] = -1
+    with pytest.raises(rs.IndexOutOfRange):
+        acc.forward(dense, bad)
+    acc.close()

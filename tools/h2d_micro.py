@@ -43,6 +43,26 @@ def main():
             gbs = reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
             out[f"{'wc' if wc else 'pinned'}_{mb}MB"] = round(gbs, 1)
             out["src_is_pinned"] = bool(srcs[0].is_pinned())
+    # two copy streams alternating 7 MB copies (two DMA engines on the link)
+    nbytes = 7 << 20
+    bufs = [rs.PinnedBuffer(nbytes) for _ in range(4)]
+    srcs = [torch.frombuffer((ctypes.c_char * nbytes).from_address(b.ptr), dtype=torch.uint8)
+            for b in bufs]
+    dsts = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    reps = 256
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(streams[0])
+    streams[1].wait_event(e0)
+    for i in range(reps):
+        with torch.cuda.stream(streams[i % 2]):
+            dsts[i % 2].copy_(srcs[i % 4], non_blocking=True)
+    streams[0].wait_stream(streams[1])
+    e1.record(streams[0])
+    torch.cuda.synchronize()
+    out["pinned_7MB_two_streams"] = round(reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
     print(json.dumps(out))
 
 
