@@ -227,7 +227,7 @@ class CpuArm:
         nq = int(min(len(self.sizes), max(self.threads, budget_s / self.per_query)))
         secs = self.orc.bench_queries(self.sizes[:nq], self.threads, seed=5)
         return {"value": nq / secs, "unit": "queries/s", "cores": self.threads, "kind": "port",
-                "sample": f"{nq} queries of the same LogNormal(ln300,0.5) stream (mean "
+                "sample": f"{nq} queries of the same LogNormal stream (mean "
                           f"{float(np.mean(self.sizes[:nq])):.0f} items), fp32 oracle forward, "
                           f"one query per thread, {self.threads} threads, tables materialised "
                           f"at {self.rows:,} rows/table, {secs:.1f} s wall"}
@@ -244,7 +244,7 @@ def run_reference(args, rank, world):
         return
     import paper_2001_02772_b200 as rs
     spec, rows, zoo_name = workload_spec(rs, args.workload)
-    _, sizes = rs.gen_trace(rank_seed(0), 1000.0, rs.SizeDistribution.log_normal(math.log(300), 0.5),
+    _, sizes = rs.gen_trace(rank_seed(0), 1000.0, rs.SizeDistribution.log_normal(math.log(args.size_median), 0.5),
                             4096)
     threads = os.cpu_count() or 1
     arm = CpuArm(spec, sizes, threads)
@@ -286,12 +286,14 @@ def run_ours(args, rank, world, local):
         0.100 if args.workload.startswith("cfg5") else rs.sla_target(zoo_name, "medium"))
     Q, K, W = args.queries_per_step, args.steps, args.warmup
     seed = rank_seed(rank)
-    _, sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(math.log(300), 0.5),
+    _, sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(math.log(args.size_median), 0.5),
                             2 * Q)
     sizes = np.minimum(sizes, args.max_query)
     acc = rs.Accelerator(spec, rows, seed=1, device=local, max_query_size=args.max_query,
                          fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc],
                          queue_depth=args.depth)
+    if args.merge > 1:
+        acc.set_option(rs.OPT_MERGE_QUERIES, args.merge)
     e = spec.embeddings
     # pool of 2Q distinct queries: pinned host copies (e2e) and device copies (value)
     P = 2 * Q
@@ -420,7 +422,7 @@ def run_ours(args, rank, world, local):
             "metric": METRIC, "value": agg["value"], "unit": "queries/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": agg["time_s"] * 1e3 / K,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded random-init tables/weights, LogNormal(ln300,0.5) sizes)",
+            "data": f"synthetic (seeded random-init tables/weights, LogNormal(ln{args.size_median:g},0.5) sizes)",
             "config": {"workload": args.workload, "model": spec.name, "rows_per_table": rows,
                        "tables": e.num_tables, "lookups": e.lookups_per_table,
                        "dim": e.embedding_dim, "queries_per_step": Q,
@@ -429,6 +431,10 @@ def run_ours(args, rank, world, local):
                        "input_format": ("int32 indices: LABELLED variant (SURVEY 8f-2), not "
                                         "the reference byte model" if i32 else
                                         "reference byte model (int64 indices + fp32 dense)"),
+                       "query_merging": (f"up to {args.merge} consecutive queries per launch: "
+                                         "LABELLED scheduler extension (SURVEY 8f-3)"
+                                         if args.merge > 1 else "off (one query per launch, "
+                                         "as the reference's accelerator server)"),
                        "l2": "inputs >> L2 (tables %.1f GB, ~%.0f MB of indices per step)" % (
                            acc.info.table_bytes / 1e9, h2d_step / 1e6),
                        "qps_method": "open-loop Poisson replay (n=50,000, sim.hpp:79) of the "
@@ -462,7 +468,7 @@ def run_ours(args, rank, world, local):
         }
         if world == 1 and not args.no_cpu:
             _, cpu_sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
-                math.log(300), 0.5), 8192)
+                math.log(args.size_median), 0.5), 8192)
             line["cpu_baseline"] = cpu_baseline(spec, np.minimum(cpu_sizes, args.max_query),
                                                 os.cpu_count() or 1)
         print(json.dumps(line), flush=True)
@@ -483,6 +489,10 @@ def main():
                          "ncf | wnd | mt-wnd | rmc1 | rmc2 | rmc3 | din | dien")
     ap.add_argument("--sla", type=float, default=0.0, help="override SLA seconds")
     ap.add_argument("--queries-per-step", type=int, default=256)
+    ap.add_argument("--size-median", type=float, default=300.0,
+                    help="LogNormal(ln m, 0.5) query sizes (SURVEY 8d: 300; 30 = small-query regime)")
+    ap.add_argument("--merge", type=int, default=1,
+                    help=">1 = labelled query-merging variant (SURVEY 8f-3)")
     ap.add_argument("--index-bits", type=int, choices=[64, 32], default=64,
                     help="32 = labelled int32-index input variant (SURVEY 8f-2)")
     ap.add_argument("--max-query", type=int, default=1000)

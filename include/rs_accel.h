@@ -266,6 +266,16 @@ int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
                     float* const* outs, void* stream, double* service_ms,
                     double* latency_ms);
 
+/* Runtime options of a handle.
+ * RS_OPT_MERGE_QUERIES (default 1 = off): rs_forward_many stages up to
+ *   `value` (1..64) consecutive queries of one index type whose items fit
+ *   max_query_size back to back in one slot and serves them with ONE graph
+ *   launch; every merged query completes with the group. A LABELLED
+ *   scheduler extension: the reference never merges distinct
+ *   queries.                                                  */
+enum { RS_OPT_MERGE_QUERIES = 1 };
+int rs_accel_set_option(rs_accel* a, int32_t option, int64_t value);
+
 /* Wait for `stream` and report (then clear) errors that asynchronous calls
  * left in the handle's sticky error words (e.g. RS_E_INDEX).               */
 int rs_sync(rs_accel* a, void* stream);

@@ -101,6 +101,7 @@ FC_FP32, FC_TF32, FC_AUTO = 0, 1, 2
 RNN_GRU, RNN_AUGRU = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 INDEX_I64, INDEX_I32 = 0, 1  # rs_query.index_type (I32: labelled input variant)
+OPT_MERGE_QUERIES = 1        # rs_accel_set_option (labelled scheduler extension)
 
 
 class CLayerStack(C.Structure):
@@ -189,6 +190,7 @@ _sig("rs_pooled", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_void_p, P(CTim
 _sig("rs_forward_many", C.c_int, C.c_void_p, C.c_int64, P(CQuery), P(C.c_void_p), C.c_void_p,
      P(C.c_double), P(C.c_double))
 _sig("rs_sync", C.c_int, C.c_void_p, C.c_void_p)
+_sig("rs_accel_set_option", C.c_int, C.c_void_p, C.c_int32, C.c_int64)
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
@@ -204,7 +206,7 @@ EXPORTED_SYMBOLS = [
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
     "rs_pooled", "rs_service_time",
     "rs_fill_query", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
-    "rs_device_count"]
+    "rs_device_count", "rs_accel_set_option"]
 
 
 # ---- operator API (model_zoo.hpp mirror) ------------------------------------
@@ -537,6 +539,11 @@ class Accelerator:
                                     lat.ctypes.data_as(P(C.c_double)) if lat is not None
                                     else None))
         return (svc, lat) if residence else svc
+
+    def set_option(self, option: int, value: int) -> None:
+        """rs_accel_set_option, e.g. (OPT_MERGE_QUERIES, 2): up to 2 consecutive
+        queries per launch in forward_many (labelled)."""
+        _check(_lib.rs_accel_set_option(self._h, option, value))
 
     def sync(self, stream: int = 0) -> None:
         """rs_sync: wait for `stream`, raise any sticky error (e.g. bad index)."""

@@ -129,6 +129,7 @@ struct rs_accel {
   // rs_forward_many queue: `depth` lanes, each a compute stream + a slot
   static constexpr int kMaxLanes = 16;
   int depth = 2;
+  int64_t merge_queries = 1;  // RS_OPT_MERGE_QUERIES (1 = one query per launch)
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t lane_join[kMaxLanes] = {};
@@ -881,6 +882,63 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
   });
 }
 
+// RS_OPT_MERGE_QUERIES (labelled scheduler extension): stage m
+// consecutive queries back to back in one slot (item offsets in arrival
+// order) so one graph launch serves all of them; returns the total items.
+int64_t stage_group(rs_accel* a, Slot* s, const rs_query* qs, int64_t m, cudaStream_t st) {
+  const bool host = qs[0].location == RS_MEM_HOST;
+  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const bool i32 = qs[0].index_type == RS_INDEX_I32;
+  const int64_t TL = a->T * a->L;
+  int64_t off = 0;
+  if (!host) {
+    // device-resident: one gather kernel for the whole group (no copy-engine
+    // work queued behind the other lanes); int32 indices widened on the way
+    GroupGather g{};
+    g.m = (int)m;
+    g.idx32 = i32 ? 1 : 0;
+    for (int64_t k = 0; k < m; ++k) {
+      if (a->dense_in > 0 && !qs[k].dense) raise(RS_E_INVALID, "null dense features");
+      g.dense[k] = qs[k].dense;
+      g.idx[k] = qs[k].indices;
+      g.size[k] = qs[k].size;
+      g.off[k] = off;
+      off += qs[k].size;
+    }
+    launch_group_gather(g, a->dense_in, TL, s->dense_raw, s->idx_stage, a->sm_count, st);
+    QDesc v{};
+    v.S = off;
+    v.dense = a->dense_in > 0 ? s->dense_raw : nullptr;
+    v.idx = a->T > 0 ? s->idx_stage : nullptr;
+    write_desc(a, s, v, st);
+    return off;
+  }
+  for (int64_t k = 0; k < m; ++k) {
+    const int64_t S = qs[k].size;
+    if (a->dense_in > 0) {
+      if (!qs[k].dense) raise(RS_E_INVALID, "null dense features");
+      RS_CUDA(cudaMemcpyAsync(s->dense_raw + off * a->dense_in, qs[k].dense,
+                              (size_t)(S * a->dense_in * 4), kind, st));
+    }
+    if (a->T > 0) {
+      if (i32)
+        RS_CUDA(cudaMemcpyAsync(s->idx32_stage + off * TL, qs[k].indices, (size_t)(S * TL * 4),
+                                kind, st));
+      else
+        RS_CUDA(cudaMemcpyAsync(s->idx_stage + off * TL, qs[k].indices, (size_t)(S * TL * 8),
+                                kind, st));
+    }
+    off += S;
+  }
+  QDesc v{};
+  v.S = off;
+  v.dense = a->dense_in > 0 ? s->dense_raw : nullptr;
+  v.idx = a->T > 0 ? s->idx_stage : nullptr;
+  v.out = nullptr;  // logits land in the slot and are split per query
+  write_desc(a, s, v, st);
+  return off;
+}
+
 int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, void* stream,
              double* service_ms, double* latency_ms) {
   return guarded([&] {
@@ -945,27 +1003,61 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     const char* po = getenv("RS_MANY_POOL_ONLY");
     const bool pool_only = po && atoi(po);
     const auto host_t0 = std::chrono::steady_clock::now();
-    for (int64_t i = 0; i < n; ++i) {
-      const int d = (int)(i % depth);
+    const int64_t maxS = a->init.max_query_size;
+    int64_t group = 0;
+    for (int64_t i = 0; i < n;) {
+      // group [i, j): one query, or up to merge_queries consecutive ones of
+      // the same index type whose items fit one slot
+      int64_t j = i + 1, items = qs[i].size;
+      while (!pool_only && j < n && j - i < a->merge_queries &&
+             items + qs[j].size <= maxS && qs[j].index_type == qs[i].index_type)
+        items += qs[j++].size;
+      const int d = (int)(group % depth);
       Slot* s = p[d];
       cudaStream_t ls = a->lane[d];
-      if (service_ms && i >= kEvRing) harvest(i - kEvRing);
-      cudaEvent_t ev_start = latency_ms ? a->evstart[i % kEvRing] : nullptr;
+      for (int64_t k = i; k < j; ++k)
+        if (service_ms && k >= kEvRing) harvest(k - kEvRing);
+      cudaStream_t sst = ls;  // staging stream
       if (loc == RS_MEM_HOST) {
-        cudaStream_t cp = copies[i % ncopy];
-        RS_CUDA(cudaStreamWaitEvent(cp, s->free, 0));
-        if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, cp));
-        stage_inputs(a, s, &qs[i], true, cp, nullptr, /*widen_later=*/true);
-        RS_CUDA(cudaEventRecord(s->ready, cp));
-        RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
-        widen_indices(a, s, &qs[i], ls);
-      } else {
-        if (latency_ms) RS_CUDA(cudaEventRecord(ev_start, ls));
-        stage_inputs(a, s, &qs[i], true, ls, outs[i]);
+        sst = copies[group % ncopy];
+        RS_CUDA(cudaStreamWaitEvent(sst, s->free, 0));
       }
-      launch_stage(a, s, &qs[i], outs[i], !pool_only, ls);
+      if (latency_ms)
+        for (int64_t k = i; k < j; ++k) RS_CUDA(cudaEventRecord(a->evstart[k % kEvRing], sst));
+      if (j - i == 1) {
+        if (loc == RS_MEM_HOST) {
+          stage_inputs(a, s, &qs[i], true, sst, nullptr, /*widen_later=*/true);
+          RS_CUDA(cudaEventRecord(s->ready, sst));
+          RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
+          widen_indices(a, s, &qs[i], ls);
+        } else {
+          stage_inputs(a, s, &qs[i], true, ls, outs[i]);
+        }
+        launch_stage(a, s, &qs[i], outs[i], !pool_only, ls);
+      } else {
+        const int64_t S = stage_group(a, s, qs + i, j - i, sst);
+        if (loc == RS_MEM_HOST) {
+          RS_CUDA(cudaEventRecord(s->ready, sst));
+          RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
+        }
+        if (loc == RS_MEM_HOST && a->T > 0 && qs[i].index_type == RS_INDEX_I32)
+          launch_widen_idx(s->idx32_stage, s->idx_stage, S * a->T * a->L, a->sm_count, ls);
+        RS_CUDA(cudaGraphLaunch(pick_graph(a, s, S, true), ls));
+        int64_t off = 0;
+        for (int64_t k = i; k < j; ++k) {
+          RS_CUDA(cudaMemcpyAsync(outs[k], s->out + off * a->out_w,
+                                  (size_t)(qs[k].size * a->out_w * 4),
+                                  loc == RS_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                     : cudaMemcpyDeviceToDevice,
+                                  ls));
+          off += qs[k].size;
+        }
+      }
       RS_CUDA(cudaEventRecord(s->free, ls));
-      if (service_ms) RS_CUDA(cudaEventRecord(a->evpool[1 + i % kEvRing], ls));
+      if (service_ms)
+        for (int64_t k = i; k < j; ++k) RS_CUDA(cudaEventRecord(a->evpool[1 + k % kEvRing], ls));
+      ++group;
+      i = j;
     }
     for (int d = 0; d < depth; ++d) {
       RS_CUDA(cudaEventRecord(a->lane_join[d], a->lane[d]));
@@ -1002,6 +1094,21 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
 }  // namespace rs
 
 using namespace rs;
+
+extern "C" int rs_accel_set_option(rs_accel* a, int32_t option, int64_t value) {
+  return guarded([&] {
+    if (!a) raise(RS_E_INVALID, "null handle");
+    switch (option) {
+      case RS_OPT_MERGE_QUERIES:
+        if (value < 1 || value > kMaxGroup)
+          raise(RS_E_INVALID, "merge_queries must be in [1, 64]");
+        a->merge_queries = value;
+        break;
+      default:
+        raise(RS_E_INVALID, "unknown option");
+    }
+  });
+}
 
 extern "C" int rs_device_count(int* out) {
   return guarded([&] {

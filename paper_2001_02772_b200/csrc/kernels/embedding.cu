@@ -1270,6 +1270,36 @@ void launch_widen_idx(const int32_t* src, int64_t* dst, int64_t n, int sm_count,
   widen_idx_kernel<<<grid, 256, 0, s>>>(src, dst, n);
 }
 
+__global__ void __launch_bounds__(256)
+group_gather_kernel(const __grid_constant__ GroupGather g, int64_t dense_in, int64_t TL,
+                    float* __restrict__ dense_dst, int64_t* __restrict__ idx_dst) {
+  const int k = blockIdx.y;
+  const int64_t S = g.size[k], off = g.off[k];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (dense_in > 0 && g.dense[k]) {
+    const float* __restrict__ src = g.dense[k];
+    float* __restrict__ dst = dense_dst + off * dense_in;
+    for (int64_t i = t0; i < S * dense_in; i += stride) dst[i] = __ldg(src + i);
+  }
+  if (TL > 0) {
+    int64_t* __restrict__ dst = idx_dst + off * TL;
+    if (g.idx32) {
+      const int32_t* __restrict__ src = static_cast<const int32_t*>(g.idx[k]);
+      for (int64_t i = t0; i < S * TL; i += stride) dst[i] = (int64_t)__ldg(src + i);
+    } else {
+      const int64_t* __restrict__ src = static_cast<const int64_t*>(g.idx[k]);
+      for (int64_t i = t0; i < S * TL; i += stride) dst[i] = __ldg(src + i);
+    }
+  }
+}
+
+void launch_group_gather(const GroupGather& g, int64_t dense_in, int64_t TL, float* dense_dst,
+                         int64_t* idx_dst, int sm_count, cudaStream_t s) {
+  const int gx = std::max(1, 2 * sm_count / std::max(1, g.m));
+  group_gather_kernel<<<dim3(gx, g.m), 256, 0, s>>>(g, dense_in, TL, dense_dst, idx_dst);
+}
+
 // Diagnostic (RS_DIAG_EMPTY, tools/pipe_micro.py): n empty grids of `ctas`
 // CTAs, to measure the per-kernel cost inside the pipelined forward.
 __global__ void diag_empty_kernel() {

@@ -22,6 +22,20 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
                      int64_t max_items, int sm_count, cudaStream_t s);
 void launch_diag_empty(int n, int ctas, cudaStream_t s);
 void launch_widen_idx(const int32_t* src, int64_t* dst, int64_t n, int sm_count, cudaStream_t s);
+// Device-resident inputs of m merged queries gathered back to back in one
+// launch (RS_OPT_MERGE_QUERIES): per query k, dense rows -> dense_dst + off_k
+// * dense_in and indices -> idx_dst + off_k * TL (int32 sources widened).
+constexpr int kMaxGroup = 64;
+struct GroupGather {
+  const float* dense[kMaxGroup];
+  const void* idx[kMaxGroup];
+  int64_t size[kMaxGroup];
+  int64_t off[kMaxGroup];
+  int m;
+  int idx32;
+};
+void launch_group_gather(const GroupGather& g, int64_t dense_in, int64_t TL, float* dense_dst,
+                         int64_t* idx_dst, int sm_count, cudaStream_t s);
 void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t ld_dst,
                         int64_t max_items, int sm_count, cudaStream_t s);
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,

@@ -313,3 +313,44 @@ def test_int32_index_variant_is_bit_identical(name):
     with pytest.raises(rs.IndexOutOfRange):
         acc.forward(dense, bad)
     acc.close()
+
+
+@pytest.mark.parametrize("fc_mode", [rs.FC_FP32, rs.FC_TF32])
+@pytest.mark.parametrize("location", [rs.MEM_HOST, rs.MEM_DEVICE])
+def test_merged_queries_match_single_calls(fc_mode, location):
+    """RS_OPT_MERGE_QUERIES (labelled scheduler extension):
+    consecutive queries staged back to back and served by one launch return
+    exactly the rows each query gets alone (per-row arithmetic does not depend
+    on the row's position in the launch; one FC path per handle here)."""
+    torch = pytest.importorskip("torch")
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 4000
+    acc = rs.Accelerator(spec, rows, seed=6, max_query_size=400, fc_mode=fc_mode,
+                         queue_depth=2)
+    acc.set_option(rs.OPT_MERGE_QUERIES, 3)
+    sizes = [5, 40, 100, 7, 300, 2, 399, 1]
+    qs = [rs.fill_query(spec, rows, 2, k, S) for k, S in enumerate(sizes)]
+    singles = [acc.forward(d, i) for d, i in qs]
+    if location == rs.MEM_HOST:
+        bd = [rs.PinnedBuffer(max(d.nbytes, 16)) for d, _ in qs]
+        bi = [rs.PinnedBuffer(i.nbytes) for _, i in qs]
+        bo = [rs.PinnedBuffer(S * acc.output_dim * 4) for S in sizes]
+        for k, (d, i) in enumerate(qs):
+            bd[k].view(np.float32, d.shape)[...] = d
+            bi[k].view(np.int64, i.shape)[...] = i
+        svc = acc.forward_many(sizes, [b.ptr for b in bd], [b.ptr for b in bi],
+                               [b.ptr for b in bo], rs.MEM_HOST)
+        got = [bo[k].view(np.float32, (S, acc.output_dim)).copy() for k, S in enumerate(sizes)]
+    else:
+        dd = [torch.from_numpy(d).cuda() for d, _ in qs]
+        di = [torch.from_numpy(i).cuda() for _, i in qs]
+        do = [torch.empty((S, acc.output_dim), device="cuda") for S in sizes]
+        svc = acc.forward_many(sizes, [t.data_ptr() for t in dd], [t.data_ptr() for t in di],
+                               [t.data_ptr() for t in do], rs.MEM_DEVICE)
+        got = [t.cpu().numpy() for t in do]
+    assert (svc >= 0).all() and svc.sum() > 0
+    for k in range(len(sizes)):
+        assert np.array_equal(got[k], singles[k]), k
+    with pytest.raises(rs.InvalidArgument):
+        acc.set_option(rs.OPT_MERGE_QUERIES, 0)
+    acc.close()
