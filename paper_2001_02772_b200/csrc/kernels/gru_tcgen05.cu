@@ -41,12 +41,25 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
 __device__ __forceinline__ uint32_t sw_off(int row, int c) {
   return (uint32_t)(row * 128 + ((((c >> 2) ^ row) & 7) << 4) + (c & 3) * 4);
 }
-// Cell nonlinearities on the SFU (ex2.approx): ~1e-6 relative, far inside the
-// tf32 operand rounding this path is toleranced for.
+// Cell nonlinearities: one MUFU.TANH each (tanh.approx.f32; sigmoid(x) =
+// 0.5 + 0.5 tanh(x/2)). The epilogue of a 128-sequence step is bound by the
+// SM's SFU (128 x H units x 3 transcendental ops), and ex2 + rcp pairs took
+// twice the SFU issue. tanh.approx's ~2^-11 relative error stays inside the
+// tf32 tolerance this path is checked against (tests/test_gpu_parity.py);
+// RS_GRU_EXACT_SFU=1 at build time restores the ex2/rcp forms.
+#ifndef RS_GRU_EXACT_SFU
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigm(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
+#else
 __device__ __forceinline__ float sigm(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float tanh_fast(float x) {
   return 1.0f - __fdividef(2.0f, __expf(2.0f * x) + 1.0f);
 }
+#endif
 
 template <int D, int H>
 struct GruTcSmem {
@@ -55,7 +68,7 @@ struct GruTcSmem {
   alignas(1024) uint8_t b[KA][N * 128];     // weights, per K atom
   alignas(1024) uint8_t ax[2][D / 32][kSeq * 128];
   alignas(1024) uint8_t ah[H / 32][kSeq * 128];
-  float bias[N];
+  alignas(16) float bias[N];
   uint64_t mma_done;
   uint32_t tmem_base;
 };
@@ -89,19 +102,41 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   {
     const float* Wih = g.w_ih + (int64_t)t * 3 * H * D;
     const float* Whh = g.w_hh + (int64_t)t * 3 * H * H;
-    for (int e = tid; e < N * (D + H); e += kThreads) {
-      const int n = e / (D + H), k = e - n * (D + H);
-      const int gate = n / H, j = n - gate * H;
-      float v = 0.f;
-      if (k < D) {
-        if (gate < 3) v = __ldg(Wih + (int64_t)(gate * H + j) * D + k);
-      } else {
-        const int kh = k - D;
-        if (gate == 0 || gate == 1) v = __ldg(Whh + (int64_t)(gate * H + j) * H + kh);
-        else if (gate == 3) v = __ldg(Whh + (int64_t)(2 * H + j) * H + kh);
+    // 128-bit loads along k (D and H are multiples of 4, so a vector never
+    // straddles the x/h boundary), 4 in flight per thread, one 16-byte store
+    // each into the swizzled K-major layout (the CTA prologue was ~8% of the
+    // kernel with scalar loads)
+    constexpr int K4 = (D + H) / 4;
+    constexpr int kU = 4;
+    for (int e0 = tid; e0 < N * K4; e0 += kThreads * kU) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kThreads;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e < N * K4) {
+          const int n = e / K4, k = (e - n * K4) * 4;
+          const int gate = n / H, j = n - gate * H;
+          if (k < D) {
+            if (gate < 3)
+              v[u] = __ldg(reinterpret_cast<const float4*>(Wih + (int64_t)(gate * H + j) * D + k));
+          } else {
+            const int kh = k - D;
+            const int row = gate < 2 ? gate * H + j : (gate == 3 ? 2 * H + j : -1);
+            if (row >= 0)
+              v[u] = __ldg(reinterpret_cast<const float4*>(Whh + (int64_t)row * H + kh));
+          }
+        }
       }
-      const int atom = k >> 5, c = k & 31;
-      *reinterpret_cast<float*>(sm.b[atom] + n * 128 + ((((c >> 2) ^ n) & 7) << 4) + (c & 3) * 4) = v;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e < N * K4) {
+          const int n = e / K4, k = (e - n * K4) * 4;
+          const int atom = k >> 5, c = k & 31;
+          *reinterpret_cast<float4*>(sm.b[atom] + n * 128 + ((((c >> 2) ^ n) & 7) << 4)) = v[u];
+        }
+      }
     }
     const float* bih = g.b_ih + (int64_t)t * 3 * H;
     const float* bhh = g.b_hh + (int64_t)t * 3 * H;
@@ -130,11 +165,16 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   // a random HBM row per sequence per step is the recurrence's only memory
   // traffic, so its latency must hide behind two MMA + epilogue rounds) ----
   float4 xa[DX / 4], xb2[DX / 4];
-  auto fetch = [&](int l, float4* xn) {
+  // the row index of step l+1 is loaded one step before its row is fetched,
+  // so no step waits a memory latency on an index (ncu: long-scoreboard
+  // stalls were the largest share before this)
+  const int64_t* __restrict__ my_idx = idx + (item * g.T + t) * L;
+  auto load_index = [&](int l) -> int64_t { return (live && l < L) ? __ldg(my_idx + l) : 0; };
+  int64_t next_r = 0;
+  auto fetch = [&](int l, float4* xn, int64_t r) {
 #pragma unroll
     for (int q = 0; q < DX / 4; ++q) xn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!live || l >= L) return;
-    const int64_t r = __ldg(idx + (item * g.T + t) * L + l);
     if ((uint64_t)r >= (uint64_t)g.rows) {
       if (half == 0) atomicOr(g.err, kErrIndex);
       return;
@@ -150,9 +190,10 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
       *reinterpret_cast<float4*>(sm.ax[buf][c >> 5] + sw_off(row, c & 31)) = xn[q];
     }
   };
-  fetch(0, xa);
+  fetch(0, xa, load_index(0));
   stash(0, xa);
-  fetch(1, xa);
+  fetch(1, xa, load_index(1));
+  next_r = load_index(2);
 
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -208,7 +249,8 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
       }
       att = sigm(sc);
     }
-    fetch(l + 2, xb2);  // rows two steps ahead fly during this MMA + epilogue
+    fetch(l + 2, xb2, next_r);  // rows two steps ahead fly during this MMA + epilogue
+    next_r = load_index(l + 3);
     asm volatile(
         "{\n.reg .pred p;\nW_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -238,14 +280,23 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
         uint8_t* hp = sm.ah[j >> 5] + sw_off(row, j & 31);
         const float4 ho = *reinterpret_cast<const float4*>(hp);
         const float hold[4] = {ho.x, ho.y, ho.z, ho.w};
+        // the 4 units' folded biases of each gate: one 128-bit load per gate
+        const float4 b4[4] = {*reinterpret_cast<const float4*>(&sm.bias[j]),
+                              *reinterpret_cast<const float4*>(&sm.bias[H + j]),
+                              *reinterpret_cast<const float4*>(&sm.bias[2 * H + j]),
+                              *reinterpret_cast<const float4*>(&sm.bias[3 * H + j])};
+        const float bb[4][4] = {{b4[0].x, b4[0].y, b4[0].z, b4[0].w},
+                                {b4[1].x, b4[1].y, b4[1].z, b4[1].w},
+                                {b4[2].x, b4[2].y, b4[2].z, b4[2].w},
+                                {b4[3].x, b4[3].y, b4[3].z, b4[3].w}};
         float hn[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int jj = 4 * q + u, jx = j + u;
-          const float r = sigm(__uint_as_float(v[0][jj]) + sm.bias[jx]);
-          const float z = sigm(__uint_as_float(v[1][jj]) + sm.bias[H + jx]);
-          const float n = tanh_fast(__uint_as_float(v[2][jj]) + sm.bias[2 * H + jx] +
-                                    r * (__uint_as_float(v[3][jj]) + sm.bias[3 * H + jx]));
+          const int jj = 4 * q + u;
+          const float r = sigm(__uint_as_float(v[0][jj]) + bb[0][u]);
+          const float z = sigm(__uint_as_float(v[1][jj]) + bb[1][u]);
+          const float n = tanh_fast(__uint_as_float(v[2][jj]) + bb[2][u] +
+                                    r * (__uint_as_float(v[3][jj]) + bb[3][u]));
           if (g.augru) {
             const float uu = att * (1.0f - z);
             hn[u] = (1.0f - uu) * hold[u] + uu * n;
