@@ -153,7 +153,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     s_u32(&sm.tmem_base)), "r"(N) : "memory");
+                     s_u32(&sm.tmem_base)), "r"(2 * N) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
@@ -193,6 +193,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   fetch(0, xa, load_index(0));
   stash(0, xa);
   fetch(1, xa, load_index(1));
+  stash(1, xa);
   next_r = load_index(2);
 
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -216,27 +217,38 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
                          ((uint32_t)(kSeq >> 4) << 24);
 
+  // Two TMEM accumulators: while step l's cell math runs, the tensor core
+  // already computes step l+1's input projection x_{l+1} W_x (it does not
+  // depend on h); after the epilogue only the h-part is on the critical path.
+  auto issue = [&](uint32_t acc_tmem, int a_begin, int a_end, const uint8_t* ax_buf,
+                   bool first_init) {
+#pragma unroll
+    for (int a = a_begin; a < a_end; ++a) {
+      const uint32_t abase = a < DA ? s_u32(ax_buf + a * kSeq * 128) : s_u32(sm.ah[a - DA]);
+      const uint32_t bbase = s_u32(sm.b[a]);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t acc = (first_init && a == a_begin && kk == 0) ? 0u : 1u;
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc_tmem),
+            "l"(sw128(abase + kk * 32)), "l"(sw128(bbase + kk * 32)), "r"(idesc), "r"(acc)
+            : "memory");
+      }
+    }
+  };
+  if (tid == 0) issue(tmem, 0, DA, sm.ax[0][0], true);  // x_0 W_x
+
   for (int l = 0; l < L; ++l) {
     const int xb = l & 1;
+    const uint32_t tcur = tmem + (uint32_t)(xb * N);
     if (tid == 0) {
-#pragma unroll
-      for (int a = 0; a < KA; ++a) {
-        const uint32_t abase = a < DA ? s_u32(sm.ax[xb][a]) : s_u32(sm.ah[a - DA]);
-        const uint32_t bbase = s_u32(sm.b[a]);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint32_t acc = (a | kk) ? 1u : 0u;
-          asm volatile(
-              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-              "l"(sw128(abase + kk * 32)), "l"(sw128(bbase + kk * 32)), "r"(idesc), "r"(acc)
-              : "memory");
-        }
-      }
+      issue(tcur, DA, KA, nullptr, false);  // += h_l W_h
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
               s_u32(&sm.mma_done))
           : "memory");
+      if (l + 1 < L) issue(tmem + (uint32_t)((xb ^ 1) * N), 0, DA, sm.ax[xb ^ 1][0], true);
     }
     float att = 1.f;
     if (g.augru) {  // a_l = sigmoid(<ua, x_l>) from the x row in shared memory
@@ -258,7 +270,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
         "r"((uint32_t)(l & 1))
         : "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const uint32_t lane_base = tcur + ((uint32_t)(quad * 32) << 16);
 #pragma unroll
     for (int j0 = 0; j0 < HU; j0 += 16) {
       uint32_t v[4][16];
@@ -307,9 +319,8 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
         *reinterpret_cast<float4*>(hp) = make_float4(hn[0], hn[1], hn[2], hn[3]);
       }
     }
-    if (l + 1 < L) stash(xb ^ 1, xa);
-#pragma unroll
-    for (int q = 0; q < DX / 4; ++q) xa[q] = xb2[q];
+    // x_{l+2} into the buffer x_l used (its MMA finished before step l's h-part)
+    if (l + 2 < L) stash(xb, xb2);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -326,7 +337,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
     }
   }
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(N)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * N)
                  : "memory");
 }
 
