@@ -973,7 +973,7 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
                                                   kWarps * 32, 0);
     return b > 0 ? b : 1;
   }();
-  const int grid = grid_for(max_items * T, kWarps, sm_count, 2 * per_sm);
+  const int grid = grid_for(max_items * T, kWarps, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
   max_carveout(reinterpret_cast<const void*>(sls_pipe_kernel<LPR, VPL, U, IPL>));
   sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, kWarps * 32, 0, s>>>(
       qd, tables, rows, T, L, out, ld_out, err, env_int("RS_SLS_TRIGGER", 0));
