@@ -266,6 +266,15 @@ int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
                     float* const* outs, void* stream, double* service_ms,
                     double* latency_ms);
 
+/* Real-time serving over K replicas (one handle per GPU, same model): query i
+ * is released at host time t0 + arrival_s[i] (non-decreasing), dispatched to
+ * the replica with the least outstanding items (ties to the lowest index; the
+ * reference's FIFO accelerator generalised to a K-server pool) and served on
+ * its lanes like rs_forward_many. latency_ms[i] = completion (CUDA events)
+ * minus arrival: queueing + service. Synchronous; all queries one location. */
+int rs_serve(rs_accel* const* replicas, int32_t k, int64_t n, const rs_query* queries,
+             const double* arrival_s, float* const* outs, double* latency_ms);
+
 /* Runtime options of a handle.
  * RS_OPT_MERGE_QUERIES (default 1 = off): rs_forward_many stages up to
  *   `value` (1..64) consecutive queries of one index type whose items fit

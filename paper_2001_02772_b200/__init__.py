@@ -191,6 +191,8 @@ _sig("rs_forward_many", C.c_int, C.c_void_p, C.c_int64, P(CQuery), P(C.c_void_p)
      P(C.c_double), P(C.c_double))
 _sig("rs_sync", C.c_int, C.c_void_p, C.c_void_p)
 _sig("rs_accel_set_option", C.c_int, C.c_void_p, C.c_int32, C.c_int64)
+_sig("rs_serve", C.c_int, P(C.c_void_p), C.c_int32, C.c_int64, P(CQuery), P(C.c_double),
+     P(C.c_void_p), P(C.c_double))
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
@@ -206,7 +208,7 @@ EXPORTED_SYMBOLS = [
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
     "rs_pooled", "rs_service_time",
     "rs_fill_query", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
-    "rs_device_count", "rs_accel_set_option"]
+    "rs_device_count", "rs_accel_set_option", "rs_serve"]
 
 
 # ---- operator API (model_zoo.hpp mirror) ------------------------------------
@@ -575,6 +577,21 @@ class Accelerator:
         v = C.c_double()
         _check(_lib.rs_service_time(self._h, query_size, C.byref(v)))
         return v.value
+
+
+def serve(replicas: Sequence["Accelerator"], prepared, arrival_s) -> np.ndarray:
+    """rs_serve: release query i at arrival_s[i] (seconds from the call),
+    least-outstanding-items replica, real execution; returns per-query
+    latency (ms) = completion - arrival. `prepared` = Accelerator.batch(...)."""
+    n, qs, outs = prepared
+    arr = np.ascontiguousarray(arrival_s, dtype=np.float64)
+    if arr.shape[0] != n:
+        raise InvalidArgument("arrival_s must have one entry per query")
+    hs = (C.c_void_p * len(replicas))(*[r._h for r in replicas])
+    lat = np.zeros(n, dtype=np.float64)
+    _check(_lib.rs_serve(hs, len(replicas), n, qs, arr.ctypes.data_as(P(C.c_double)), outs,
+                         lat.ctypes.data_as(P(C.c_double))))
+    return lat
 
 
 class PinnedBuffer:

@@ -23,7 +23,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -1240,6 +1242,127 @@ extern "C" int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
                                float* const* outs, void* stream, double* service_ms,
                                double* latency_ms) {
   return run_many(a, n, queries, outs, stream, service_ms, latency_ms);
+}
+
+// Real-time executor: queries are released at their arrival
+// times (host clock), each to the replica with the least outstanding items
+// (ties to the lowest index — the K-server pool of §8e), and served on that
+// replica's lanes exactly as in rs_forward_many. latency = completion (CUDA
+// event on the replica, relative to a start event recorded at t0) minus the
+// arrival offset: queueing + service as a client would see it.
+extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_query* qs,
+                        const double* arrival_s, float* const* outs, double* latency_ms) {
+  std::vector<std::unique_lock<std::mutex>> locks;
+  return guarded([&] {
+    if (!reps || !qs || !arrival_s || !outs || !latency_ms) raise(RS_E_INVALID, "null argument");
+    if (k < 1 || n < 1) raise(RS_E_INVALID, "k < 1 or n < 1");
+    const int loc = qs[0].location;
+    for (int r = 0; r < k; ++r)
+      if (!reps[r]) raise(RS_E_INVALID, "null replica");
+    for (int64_t i = 0; i < n; ++i) {
+      for (int r = 0; r < k; ++r) check_query(reps[r], &qs[i]);
+      if (qs[i].location != loc) raise(RS_E_INVALID, "mixed memory locations");
+      if (!outs[i]) raise(RS_E_INVALID, "null output");
+      if (!(arrival_s[i] >= 0) || (i && arrival_s[i] < arrival_s[i - 1]))
+        raise(RS_E_INVALID, "arrival times must be non-negative and non-decreasing");
+    }
+    constexpr int64_t kRing = 4096;
+    struct Rep {
+      rs_accel* a;
+      Slot* p[rs_accel::kMaxLanes];
+      int64_t issued = 0, outstanding = 0;
+      std::deque<std::pair<int64_t, int64_t>> inflight;  // (query, replica-local seq)
+      std::vector<int64_t> who;                            // ring slot -> query
+    };
+    std::vector<Rep> R((size_t)k);
+    for (int r = 0; r < k; ++r) {
+      rs_accel* a = reps[r];
+      locks.emplace_back(a->many_mu);
+      RS_CUDA(cudaSetDevice(a->device));
+      R[r].a = a;
+      for (int d = 0; d < a->depth; ++d) R[r].p[d] = get_pipe_slot(a, d);
+      while ((int64_t)a->evpool.size() < kRing + 1) {
+        cudaEvent_t e;
+        RS_CUDA(cudaEventCreate(&e));
+        a->evpool.push_back(e);
+      }
+      R[r].who.assign(kRing, -1);
+    }
+    std::vector<double> done_ms((size_t)n, -1.0);
+    std::vector<int> rep_of((size_t)n, 0);
+    auto retire = [&](Rep& rp, bool block) {
+      while (!rp.inflight.empty()) {
+        const auto [qi, seq] = rp.inflight.front();
+        cudaEvent_t e = rp.a->evpool[1 + seq % kRing];
+        if (block) {
+          RS_CUDA(cudaEventSynchronize(e));
+        } else {
+          const cudaError_t st = cudaEventQuery(e);
+          if (st == cudaErrorNotReady) break;
+          if (st != cudaSuccess) RS_CUDA(st);
+        }
+        done_ms[(size_t)qi] = elapsed(rp.a->evpool[0], e);
+        rp.outstanding -= qs[qi].size;
+        rp.inflight.pop_front();
+      }
+    };
+    // t0: a start event on every replica, then release queries on the clock
+    for (auto& rp : R) {
+      RS_CUDA(cudaSetDevice(rp.a->device));
+      RS_CUDA(cudaEventRecord(rp.a->evpool[0], rp.a->own));
+      RS_CUDA(cudaEventRecord(rp.a->copy_gate, rp.a->own));
+      for (int d = 0; d < rp.a->depth; ++d)
+        RS_CUDA(cudaStreamWaitEvent(rp.a->lane[d], rp.a->copy_gate, 0));
+      RS_CUDA(cudaStreamWaitEvent(rp.a->copy, rp.a->copy_gate, 0));
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < n; ++i) {
+      const auto due = t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                                std::chrono::duration<double>(arrival_s[i]));
+      for (;;) {
+        const auto now = std::chrono::steady_clock::now();
+        if (now >= due) break;
+        if (due - now > std::chrono::microseconds(200))
+          std::this_thread::sleep_for(std::chrono::microseconds(50));
+      }
+      int best = 0;
+      for (int r = 0; r < k; ++r) {
+        retire(R[r], false);
+        if (R[r].outstanding < R[best].outstanding) best = r;
+      }
+      Rep& rp = R[best];
+      rs_accel* a = rp.a;
+      RS_CUDA(cudaSetDevice(a->device));
+      const int64_t seq = rp.issued++;
+      if (seq >= kRing) {  // ring slot reuse: its query must have retired
+        while (!rp.inflight.empty() && rp.inflight.front().second <= seq - kRing) retire(rp, true);
+      }
+      const int d = (int)(seq % a->depth);
+      Slot* sl = rp.p[d];
+      cudaStream_t ls = a->lane[d];
+      if (loc == RS_MEM_HOST) {
+        RS_CUDA(cudaStreamWaitEvent(a->copy, sl->free, 0));
+        stage_inputs(a, sl, &qs[i], true, a->copy, nullptr, /*widen_later=*/true);
+        RS_CUDA(cudaEventRecord(sl->ready, a->copy));
+        RS_CUDA(cudaStreamWaitEvent(ls, sl->ready, 0));
+        widen_indices(a, sl, &qs[i], ls);
+      } else {
+        stage_inputs(a, sl, &qs[i], true, ls, outs[i]);
+      }
+      launch_stage(a, sl, &qs[i], outs[i], true, ls);
+      RS_CUDA(cudaEventRecord(sl->free, ls));
+      RS_CUDA(cudaEventRecord(a->evpool[1 + seq % kRing], ls));
+      rp.inflight.emplace_back(i, seq);
+      rp.outstanding += qs[i].size;
+      rep_of[(size_t)i] = best;
+    }
+    for (auto& rp : R) {
+      RS_CUDA(cudaSetDevice(rp.a->device));
+      retire(rp, true);
+      for (int d = 0; d < rp.a->depth; ++d) collect_errors(rp.p[d], rp.a->lane[d]);
+    }
+    for (int64_t i = 0; i < n; ++i) latency_ms[i] = done_ms[(size_t)i] - arrival_s[i] * 1e3;
+  });
 }
 
 extern "C" int rs_sync(rs_accel* a, void* stream) {

@@ -354,3 +354,33 @@ def test_merged_queries_match_single_calls(fc_mode, location):
     with pytest.raises(rs.InvalidArgument):
         acc.set_option(rs.OPT_MERGE_QUERIES, 0)
     acc.close()
+
+
+def test_realtime_serve_matches_single_calls_and_queues():
+    """rs_serve (real-time executor, K-server pool): released on the clock,
+    routed to the least-loaded replica (two handles on one GPU here), every
+    output equals its single-call result; sparse arrivals see ~service-time
+    latency, a burst at t=0 sees queueing."""
+    torch = pytest.importorskip("torch")
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 3000
+    reps = [rs.Accelerator(spec, rows, seed=7, max_query_size=256, queue_depth=2)
+            for _ in range(2)]
+    sizes = [int(s) for s in np.random.default_rng(1).integers(1, 257, size=40)]
+    qs = [rs.fill_query(spec, rows, 4, k, S) for k, S in enumerate(sizes)]
+    singles = [reps[0].forward(d, i) for d, i in qs]
+    dd = [torch.from_numpy(d).cuda() for d, _ in qs]
+    di = [torch.from_numpy(i).cuda() for _, i in qs]
+    do = [torch.zeros((S, reps[0].output_dim), device="cuda") for S in sizes]
+    b = reps[0].batch(sizes, [t.data_ptr() for t in dd], [t.data_ptr() for t in di],
+                      [t.data_ptr() for t in do], rs.MEM_DEVICE)
+    sparse = rs.serve(reps, b, np.arange(len(sizes)) * 2e-3)  # one query every 2 ms
+    for k in range(len(sizes)):
+        assert np.array_equal(do[k].cpu().numpy(), singles[k]), k
+    assert (sparse > 0).all() and np.median(sparse) < 2.0
+    burst = rs.serve(reps, b, np.zeros(len(sizes)))
+    assert burst.max() > np.median(sparse)  # the last of a burst waits behind the rest
+    with pytest.raises(rs.InvalidArgument):
+        rs.serve(reps, b, np.arange(len(sizes))[::-1] * 1e-3)  # decreasing arrivals
+    for r in reps:
+        r.close()
