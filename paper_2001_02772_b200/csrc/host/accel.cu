@@ -1274,10 +1274,15 @@ extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_qu
       std::deque<std::pair<int64_t, int64_t>> inflight;  // (query, replica-local seq)
       std::vector<int64_t> who;                            // ring slot -> query
     };
+    // queue locks in address order (two concurrent callers can never deadlock)
+    std::vector<rs_accel*> order(reps, reps + k);
+    std::sort(order.begin(), order.end());
+    order.erase(std::unique(order.begin(), order.end()), order.end());
+    if ((int)order.size() != k) raise(RS_E_INVALID, "a replica appears twice");
+    for (rs_accel* a : order) locks.emplace_back(a->many_mu);
     std::vector<Rep> R((size_t)k);
     for (int r = 0; r < k; ++r) {
       rs_accel* a = reps[r];
-      locks.emplace_back(a->many_mu);
       RS_CUDA(cudaSetDevice(a->device));
       R[r].a = a;
       for (int d = 0; d < a->depth; ++d) R[r].p[d] = get_pipe_slot(a, d);

@@ -266,7 +266,8 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
   const int g = lane / LPR, c = lane % LPR;
   const int64_t bags = qd->S * T;
   const int64_t* __restrict__ idx = qd->idx;
-  const int64_t stride = (int64_t)gridDim.x * kWarps;
+  const int nw = blockDim.x >> 5;  // warps per CTA (<= kWarps; RS_SLS_WPC)
+  const int64_t stride = (int64_t)gridDim.x * nw;
   int64_t nidx[IPL];
   auto fetch_idx = [&](int64_t bag) {
 #pragma unroll
@@ -275,7 +276,7 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
       nidx[q] = (bag < bags && l < L) ? __ldg(idx + bag * L + l) : 0;
     }
   };
-  int64_t bag = (int64_t)blockIdx.x * kWarps + warp;
+  int64_t bag = (int64_t)blockIdx.x * nw + warp;
   fetch_idx(bag);
   for (; bag < bags; bag += stride) {
     __syncwarp();
@@ -967,15 +968,14 @@ template <int LPR, int VPL, int U, int IPL>
 void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                      float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
                      cudaStream_t s) {
-  static const int per_sm = [] {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sls_pipe_kernel<LPR, VPL, U, IPL>,
-                                                  kWarps * 32, 0);
-    return b > 0 ? b : 1;
-  }();
-  const int grid = grid_for(max_items * T, kWarps, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
+  const int wpc = std::min(kWarps, std::max(1, env_int("RS_SLS_WPC", kWarps)));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sls_pipe_kernel<LPR, VPL, U, IPL>,
+                                                wpc * 32, 0);
+  per_sm = std::max(per_sm, 1);
+  const int grid = grid_for(max_items * T, wpc, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
   max_carveout(reinterpret_cast<const void*>(sls_pipe_kernel<LPR, VPL, U, IPL>));
-  sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, kWarps * 32, 0, s>>>(
+  sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, wpc * 32, 0, s>>>(
       qd, tables, rows, T, L, out, ld_out, err, env_int("RS_SLS_TRIGGER", 0));
 }
 
