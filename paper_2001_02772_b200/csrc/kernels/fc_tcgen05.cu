@@ -358,10 +358,15 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   const int64_t ctas = (int64_t)((a.N + 127) / 128) * ((m_cap + BM - 1) / BM) * a.batch;
   const bool wide = a.K >= 1024 || ctas > 148;
   p->cfg = a.N >= 128 ? (wide ? 0 : 2) : (wide ? 1 : 3);
-  if (const char* e = getenv("RS_TC_CFG")) p->cfg = atoi(e) & 3;
+  // cfg 4 <256,4>: one CTA covers 256 output columns (half the CTAs of a
+  // 512-wide layer, same k-block round trips per CTA); RS_TC_WIDE=1 selects it
+  // for the latency-bound layers with N >= 256
+  if (!wide && a.N >= 256 && getenv("RS_TC_WIDE") && atoi(getenv("RS_TC_WIDE"))) p->cfg = 4;
+  if (const char* e = getenv("RS_TC_CFG")) p->cfg = std::min(4, std::max(0, atoi(e)));
+  if (p->cfg == 4 && a.N < 256) p->cfg = 2;
   if (a.single_n_tile && a.N <= 128 && (p->cfg == 1 || p->cfg == 3)) p->cfg -= 1;
   if (a.N < 128 && !a.single_n_tile && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
-  p->block_n = (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
+  p->block_n = p->cfg == 4 ? 256 : (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
   p->m_tiles = (int)((m_cap + BM - 1) / BM);
   p->n_tiles = (a.N + p->block_n - 1) / p->block_n;
   // A: [batch][rows][K] (or shared 2D when sAz == 0)
@@ -387,6 +392,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
     case 0: set_attr_once<128, 3>(); break;
     case 1: set_attr_once<64, 4>(); break;
     case 2: set_attr_once<128, 6>(); break;
+    case 4: set_attr_once<256, 4>(); break;
     default: set_attr_once<64, 8>(); break;
   }
   return true;
@@ -400,6 +406,7 @@ void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_
              p.map_w, a, a_batched)
   switch (p.cfg) {
     case 0: RS_TC(128, 3); break;
+    case 4: RS_TC(256, 4); break;
     case 1: RS_TC(64, 4); break;
     case 2: RS_TC(128, 6); break;
     default: RS_TC(64, 8); break;
