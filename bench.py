@@ -304,12 +304,21 @@ def run_ours(args, rank, world, local):
         dn, ix = rs.fill_query(spec, rows, seed, q, int(sizes[q]))
         if i32:
             ix = ix.astype(np.int32)
-        hb_d = rs.PinnedBuffer(max(dn.nbytes, 16))
-        hb_i = rs.PinnedBuffer(max(ix.nbytes, 16))
-        hb_d.view(np.float32, dn.shape)[...] = dn
-        hb_i.view(ix.dtype, ix.shape)[...] = ix
-        h_dense.append(hb_d)
-        h_idx.append(hb_i)
+        if args.pack and not i32 and dn.nbytes:
+            # one pinned buffer per query, [dense | indices]: the library moves
+            # a packed query with one transfer (same bytes)
+            hb = rs.PinnedBuffer(dn.nbytes + ix.nbytes)
+            hb.view(np.uint8, (dn.nbytes + ix.nbytes,))[...] = np.concatenate(
+                [dn.reshape(-1).view(np.uint8), ix.reshape(-1).view(np.uint8)])
+            h_dense.append((hb, hb.ptr))
+            h_idx.append((hb, hb.ptr + dn.nbytes))
+        else:
+            hb_d = rs.PinnedBuffer(max(dn.nbytes, 16))
+            hb_i = rs.PinnedBuffer(max(ix.nbytes, 16))
+            hb_d.view(np.float32, dn.shape)[...] = dn
+            hb_i.view(ix.dtype, ix.shape)[...] = ix
+            h_dense.append((hb_d, hb_d.ptr))
+            h_idx.append((hb_i, hb_i.ptr))
         d_dense.append(torch.from_numpy(dn).to(device))
         d_idx.append(torch.from_numpy(ix).to(device))
     out_dev = torch.empty((args.max_query, acc.output_dim), device=device)
@@ -325,8 +334,8 @@ def run_ours(args, rank, world, local):
         """rs_forward_many arguments for n_steps windows (built before timing)."""
         qs = [q for k in range(n_steps) for q in window(k)]
         if host:
-            dp = [h_dense[q].ptr for q in qs]
-            ip = [h_idx[q].ptr for q in qs]
+            dp = [h_dense[q][1] for q in qs]
+            ip = [h_idx[q][1] for q in qs]
             op = [out_host.ptr] * len(qs)
             loc = rs.MEM_HOST
         else:
@@ -507,6 +516,8 @@ def main():
                          "ncf | wnd | mt-wnd | rmc1 | rmc2 | rmc3 | din | dien")
     ap.add_argument("--sla", type=float, default=0.0, help="override SLA seconds")
     ap.add_argument("--queries-per-step", type=int, default=256)
+    ap.add_argument("--pack", type=int, default=1,
+                    help="1: each host query in one pinned buffer [dense | indices]")
     ap.add_argument("--size-median", type=float, default=300.0,
                     help="LogNormal(ln m, 0.5) query sizes (SURVEY 8d: 300; 30 = small-query regime)")
     ap.add_argument("--merge", type=int, default=1,

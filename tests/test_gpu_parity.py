@@ -384,3 +384,22 @@ def test_realtime_serve_matches_single_calls_and_queues():
         rs.serve(reps, b, np.arange(len(sizes))[::-1] * 1e-3)  # decreasing arrivals
     for r in reps:
         r.close()
+
+
+def test_packed_host_query_one_transfer():
+    """A host query whose indices follow its dense features in one pinned
+    buffer is moved with one transfer — same results as separate buffers."""
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 3000
+    acc = rs.Accelerator(spec, rows, seed=9, max_query_size=200, fc_mode=rs.FC_AUTO)
+    for S in (1, 50, 200):
+        dense, idx = rs.fill_query(spec, rows, 3, S, S)
+        ref = acc.forward(dense, idx)
+        buf = rs.PinnedBuffer(dense.nbytes + idx.nbytes)
+        raw = buf.view(np.uint8, (dense.nbytes + idx.nbytes,))
+        raw[:dense.nbytes] = dense.reshape(-1).view(np.uint8)
+        raw[dense.nbytes:] = idx.reshape(-1).view(np.uint8)
+        out = rs.PinnedBuffer(S * acc.output_dim * 4)
+        acc.forward_ptr(S, buf.ptr, buf.ptr + dense.nbytes, out.ptr, rs.MEM_HOST, timed=True)
+        assert np.array_equal(out.view(np.float32, (S, acc.output_dim)), ref), S
+    acc.close()

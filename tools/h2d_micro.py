@@ -63,6 +63,23 @@ def main():
     e1.record(streams[0])
     torch.cuda.synchronize()
     out["pinned_7MB_two_streams"] = round(reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
+    # many distinct source buffers (a pool of queries, 1.8 GB) vs the 4 above:
+    # host-side translation of a large pinned footprint
+    many = [rs.PinnedBuffer(nbytes) for _ in range(256)]
+    msrc = [torch.frombuffer((ctypes.c_char * nbytes).from_address(b.ptr), dtype=torch.uint8)
+            for b in many]
+    for b in many:
+        b.view(np.uint8, (nbytes,))[...] = 1
+    torch.cuda.synchronize()
+    e0.record(streams[0])
+    streams[1].wait_event(e0)
+    for i in range(reps):
+        with torch.cuda.stream(streams[i % 2]):
+            dsts[i % 2].copy_(msrc[i % 256], non_blocking=True)
+    streams[0].wait_stream(streams[1])
+    e1.record(streams[0])
+    torch.cuda.synchronize()
+    out["pinned_7MB_256_buffers"] = round(reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
     print(json.dumps(out))
 
 
