@@ -304,7 +304,7 @@ def run_ours(args, rank, world, local):
         dn, ix = rs.fill_query(spec, rows, seed, q, int(sizes[q]))
         if i32:
             ix = ix.astype(np.int32)
-        if args.pack and not i32 and dn.nbytes:
+        if args.pack and dn.nbytes:
             # one pinned buffer per query, [dense | indices]: the library moves
             # a packed query with one transfer (same bytes)
             hb = rs.PinnedBuffer(dn.nbytes + ix.nbytes)

@@ -84,6 +84,7 @@ struct Slot {
   int64_t* idx_stage = nullptr;
   int32_t* idx32_stage = nullptr;  // H2D landing zone of RS_INDEX_I32 queries
   uint8_t* landing = nullptr;      // one-DMA landing zone for packed host inputs
+  const int32_t* idx32_src = nullptr;  // where this query's int32 indices landed
   float* act[2] = {nullptr, nullptr};
   float* pooled = nullptr;
   float* X = nullptr;
@@ -777,7 +778,7 @@ BatchMemOpFn probe_memops(rs_accel* a) {
 void widen_indices(rs_accel* a, Slot* s, const rs_query* q, cudaStream_t st) {
   if (a->T == 0 || q->index_type != RS_INDEX_I32) return;
   const int64_t n = q->size * a->T * a->L;
-  const int32_t* src = q->location == RS_MEM_HOST ? s->idx32_stage
+  const int32_t* src = q->location == RS_MEM_HOST ? s->idx32_src
                                                   : reinterpret_cast<const int32_t*>(q->indices);
   launch_widen_idx(src, s->idx_stage, n, a->sm_count, st);
 }
@@ -792,20 +793,27 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
   QDesc v{};
   v.S = S;
   const int64_t dense_bytes = S * a->dense_in * 4;
-  if (host && full && a->dense_in > 0 && a->T > 0 && q->index_type == RS_INDEX_I64 &&
-      q->dense && dense_bytes % 8 == 0 &&
+  const bool i32 = q->index_type == RS_INDEX_I32;
+  s->idx32_src = s->idx32_stage;
+  if (host && full && a->dense_in > 0 && a->T > 0 && q->dense && dense_bytes % 8 == 0 &&
       reinterpret_cast<const uint8_t*>(q->indices) ==
           reinterpret_cast<const uint8_t*>(q->dense) + dense_bytes) {
     // packed host query [dense | indices] in one buffer: ONE transfer (same
     // bytes as the reference byte model, one DMA op's fixed cost instead of
     // two). Two separate pinned allocations that merely touch are rejected by
     // the copy (invalid argument, not sticky): then the two-copy path runs.
-    const cudaError_t e = cudaMemcpyAsync(s->landing, q->dense,
-                                          (size_t)(dense_bytes + S * a->T * a->L * 8),
-                                          cudaMemcpyHostToDevice, st);
+    const cudaError_t e = cudaMemcpyAsync(
+        s->landing, q->dense, (size_t)(dense_bytes + S * a->T * a->L * (i32 ? 4 : 8)),
+        cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
       v.dense = reinterpret_cast<const float*>(s->landing);
-      v.idx = reinterpret_cast<const int64_t*>(s->landing + dense_bytes);
+      if (i32) {
+        s->idx32_src = reinterpret_cast<const int32_t*>(s->landing + dense_bytes);
+        if (!widen_later) widen_indices(a, s, q, st);
+        v.idx = s->idx_stage;
+      } else {
+        v.idx = reinterpret_cast<const int64_t*>(s->landing + dense_bytes);
+      }
       write_desc(a, s, v, st);
       return;
     }
