@@ -28,7 +28,18 @@ namespace rs {
 namespace {
 
 constexpr int kSeq = 128;           // sequences per CTA = UMMA M = TMEM lanes
-constexpr int kThreads = 2 * kSeq;  // two threads per sequence (hidden units split)
+// Threads per sequence: the hidden units of a sequence are split over TPS
+// threads (warps w, w+4, ... share TMEM lanes 32(w%4)..+31). Build knob;
+// TPS=4 (512 threads, 128 registers) measured slower for DIEN cfg5
+// (126 -> 142 us/query: spills and the per-step barrier over 16 warps).
+#ifndef RS_GRU_TPS
+#define RS_GRU_TPS 2
+#endif
+template <int H>
+struct GruThreads {
+  static constexpr int TPS = H >= 64 ? RS_GRU_TPS : 2;  // >= 16 units per thread
+  static constexpr int N = TPS * kSeq;
+};
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -74,12 +85,15 @@ struct GruTcSmem {
 };
 
 template <int D, int H>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(GruThreads<H>::N, 1)
 gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   using SM = GruTcSmem<D, H>;
   constexpr int N = SM::N, KA = SM::KA, DA = D / 32;
-  constexpr int HU = H / 2;   // hidden units per thread
-  constexpr int DX = D / 2;   // x elements fetched per thread
+  constexpr int kTps = GruThreads<H>::TPS, kThreads = GruThreads<H>::N;
+  constexpr int HU = H / kTps;  // hidden units per thread
+  constexpr int DX = D / kTps;  // x elements fetched per thread
+  static_assert(HU % 16 == 0, "hidden units per thread");
+  static_assert(DX % 4 == 0, "x elements per thread");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align by offsetting smem_raw itself (not through an integer round trip) so
   // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
@@ -89,7 +103,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   const int64_t S = qd->S;
   if (item0 >= S) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quad = warp & 3, half = warp >> 2;
+  const int quad = warp & 3, half = warp >> 2;  // half = which slice of the units
   const int row = quad * 32 + lane;          // sequence = TMEM lane
   const int u0 = half * HU;                  // this thread's hidden units
   const int64_t item = item0 + row;
@@ -351,7 +365,7 @@ void launch_typed(const QDesc* qd, const GruArgs& g, int64_t max_items, cudaStre
   });
   const dim3 grid((unsigned)((max_items + kSeq - 1) / kSeq), g.T);
   max_carveout(reinterpret_cast<const void*>(gru_tc_kernel<D, H>));
-  gru_tc_kernel<D, H><<<grid, kThreads, smem, s>>>(qd, g);
+  gru_tc_kernel<D, H><<<grid, GruThreads<H>::N, smem, s>>>(qd, g);
 }
 
 }  // namespace
