@@ -92,7 +92,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
   constexpr int kTps = GruThreads<H>::TPS, kThreads = GruThreads<H>::N;
   constexpr int HU = H / kTps;  // hidden units per thread
   constexpr int DX = D / kTps;  // x elements fetched per thread
-  static_assert(HU % 16 == 0, "hidden units per thread");
+  static_assert(HU % 8 == 0, "hidden units per thread");
   static_assert(DX % 4 == 0, "x elements per thread");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align by offsetting smem_raw itself (not through an integer round trip) so
@@ -286,22 +286,34 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t lane_base = tcur + ((uint32_t)(quad * 32) << 16);
 #pragma unroll
-    for (int j0 = 0; j0 < HU; j0 += 16) {
-      uint32_t v[4][16];
+    // units per TMEM batch: 16 (x16 loads) with 2 threads per sequence, 8 with
+    // 4 (keeps the 512-thread build under its 128-register cap)
+    constexpr int UB = kTps <= 2 ? 16 : 8;
+    for (int j0 = 0; j0 < HU; j0 += UB) {
+      uint32_t v[4][UB];
 #pragma unroll
       for (int gte = 0; gte < 4; ++gte) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[gte][0]), "=r"(v[gte][1]), "=r"(v[gte][2]), "=r"(v[gte][3]),
-              "=r"(v[gte][4]), "=r"(v[gte][5]), "=r"(v[gte][6]), "=r"(v[gte][7]),
-              "=r"(v[gte][8]), "=r"(v[gte][9]), "=r"(v[gte][10]), "=r"(v[gte][11]),
-              "=r"(v[gte][12]), "=r"(v[gte][13]), "=r"(v[gte][14]), "=r"(v[gte][15])
-            : "r"(lane_base + (uint32_t)(gte * H + u0 + j0)));
+        const uint32_t ta = lane_base + (uint32_t)(gte * H + u0 + j0);
+        if constexpr (UB == 16) {
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+              "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[gte][0]), "=r"(v[gte][1]), "=r"(v[gte][2]), "=r"(v[gte][3]),
+                "=r"(v[gte][4]), "=r"(v[gte][5]), "=r"(v[gte][6]), "=r"(v[gte][7]),
+                "=r"(v[gte][8]), "=r"(v[gte][9]), "=r"(v[gte][10]), "=r"(v[gte][11]),
+                "=r"(v[gte][12]), "=r"(v[gte][13]), "=r"(v[gte][14]), "=r"(v[gte][15])
+              : "r"(ta));
+        } else {
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+              : "=r"(v[gte][0]), "=r"(v[gte][1]), "=r"(v[gte][2]), "=r"(v[gte][3]),
+                "=r"(v[gte][4]), "=r"(v[gte][5]), "=r"(v[gte][6]), "=r"(v[gte][7])
+              : "r"(ta));
+        }
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < UB / 4; ++q) {
         const int j = u0 + j0 + 4 * q;
         uint8_t* hp = sm.ah[j >> 5] + sw_off(row, j & 31);
         const float4 ho = *reinterpret_cast<const float4*>(hp);
