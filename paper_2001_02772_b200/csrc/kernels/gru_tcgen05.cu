@@ -285,10 +285,10 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
         : "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t lane_base = tcur + ((uint32_t)(quad * 32) << 16);
-#pragma unroll
     // units per TMEM batch: 16 (x16 loads) with 2 threads per sequence, 8 with
     // 4 (keeps the 512-thread build under its 128-register cap)
     constexpr int UB = kTps <= 2 ? 16 : 8;
+#pragma unroll
     for (int j0 = 0; j0 < HU; j0 += UB) {
       uint32_t v[4][UB];
 #pragma unroll
