@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--loads", default="0.5,0.8,0.9,1.0")
     ap.add_argument("--depth", type=int, default=8)
     ap.add_argument("--host", action="store_true", help="pinned host inputs (end to end)")
+    ap.add_argument("--replicas", type=int, default=1, help="K GPUs (one handle each)")
     args = ap.parse_args()
     import torch
     import bench
@@ -44,6 +45,10 @@ def main():
                             args.pool)
     sizes = np.minimum(sizes, 1000)
     acc = rs.Accelerator(spec, rows, seed=1, max_query_size=1000, queue_depth=args.depth)
+    reps = [acc] + [rs.Accelerator(spec, rows, seed=1, device=k, max_query_size=1000,
+                                   queue_depth=args.depth) for k in range(1, args.replicas)]
+    if args.replicas > 1 and not args.host:
+        raise SystemExit("--replicas > 1 needs --host (device inputs live on one GPU)")
     dp, ip = [], []
     keep = []
     for q in range(args.pool):
@@ -74,16 +79,27 @@ def main():
     acc.forward_many(None, prepared=b)
     svc, res = acc.forward_many(None, prepared=b, residence=True)
     svc_s, extra_s = svc * 1e-3, np.maximum(res - svc, 0.0) * 1e-3
-    cap = 1.0 / float(np.mean(svc_s))
+    cap = args.replicas / float(np.mean(svc_s))
     out = {"workload": args.workload, "inputs": "host pinned" if args.host else "device",
+           "replicas": args.replicas,
            "n": args.n, "capacity_qps": cap, "rows": []}
     rng = np.random.default_rng(11)
     for f in [float(x) for x in args.loads.split(",")]:
         lam = f * cap
         arrival = np.cumsum(rng.exponential(1.0 / lam, size=args.n))
         arrival -= arrival[0]
-        lat_real = rs.serve([acc], b, arrival) * 1e-3
-        lat_rep = replay(arrival, svc_s, extra_s)
+        lat_real = rs.serve(reps, b, arrival) * 1e-3
+        # K-server replay: query i to the earliest-free server (FIFO per server)
+        if args.replicas == 1:
+            lat_rep = replay(arrival, svc_s, extra_s)
+        else:
+            free = np.zeros(args.replicas)
+            lat_rep = np.empty(args.n)
+            for i2 in range(args.n):
+                k = int(np.argmin(free))
+                fin = max(arrival[i2], free[k]) + svc_s[i2]
+                free[k] = fin
+                lat_rep[i2] = fin - arrival[i2] + extra_s[i2]
         w = args.n // 10  # warm-up excluded, as sim.cpp
         row = {"load": f, "lambda_qps": lam,
                "real_p50_ms": float(np.percentile(lat_real[w:], 50) * 1e3),
@@ -94,7 +110,8 @@ def main():
         out["rows"].append(row)
         print(json.dumps(row), flush=True)
     print(json.dumps(out))
-    acc.close()
+    for r in reps:
+        r.close()
 
 
 if __name__ == "__main__":
