@@ -255,9 +255,7 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
 template <int LPR, int VPL, int U, int IPL>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
-                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
-                int trig) {
-  if (trig) pdl_trigger();
+                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err) {
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   constexpr int B = R * U;  // rows per batch
@@ -976,7 +974,7 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
   const int grid = grid_for(max_items * T, wpc, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
   max_carveout(reinterpret_cast<const void*>(sls_pipe_kernel<LPR, VPL, U, IPL>));
   sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, wpc * 32, 0, s>>>(
-      qd, tables, rows, T, L, out, ld_out, err, env_int("RS_SLS_TRIGGER", 0));
+      qd, tables, rows, T, L, out, ld_out, err);
 }
 
 template <int LPR, int VPL, int U, int IPL>
