@@ -299,11 +299,14 @@ def run_ours(args, rank, world, local):
     P = 2 * Q
     d_dense, d_idx, h_dense, h_idx = [], [], [], []
     i32 = args.index_bits == 32
-    ity = rs.INDEX_I32 if i32 else rs.INDEX_I64
+    bf16 = args.dense_bits == 16
+    ity = (rs.INDEX_I32 if i32 else rs.INDEX_I64) | (rs.DENSE_BF16 if bf16 else 0)
     for q in range(P):
         dn, ix = rs.fill_query(spec, rows, seed, q, int(sizes[q]))
         if i32:
             ix = ix.astype(np.int32)
+        if bf16:
+            dn = (dn.view(np.uint32) >> 16).astype(np.uint16)
         if args.pack and dn.nbytes:
             # one pinned buffer per query, [dense | indices]: the library moves
             # a packed query with one transfer (same bytes)
@@ -315,7 +318,7 @@ def run_ours(args, rank, world, local):
         else:
             hb_d = rs.PinnedBuffer(max(dn.nbytes, 16))
             hb_i = rs.PinnedBuffer(max(ix.nbytes, 16))
-            hb_d.view(np.float32, dn.shape)[...] = dn
+            hb_d.view(dn.dtype, dn.shape)[...] = dn
             hb_i.view(ix.dtype, ix.shape)[...] = ix
             h_dense.append((hb_d, hb_d.ptr))
             h_idx.append((hb_i, hb_i.ptr))
@@ -415,7 +418,7 @@ def run_ours(args, rank, world, local):
     b2b = sum(int(sizes[q]) for q in qs2) * sls_bytes_per_item(spec) / (svc2.sum() * 1e-3) / 1e9
 
     items_step = float(np.mean([sum(int(sizes[q]) for q in window(k)) for k in range(K)]))
-    h2d_step = float(np.mean([sum(int(sizes[q]) * (spec.dense_input_dim * 4 +
+    h2d_step = float(np.mean([sum(int(sizes[q]) * (spec.dense_input_dim * (2 if bf16 else 4) +
                                                    e.num_tables * e.lookups_per_table *
                                                    (4 if i32 else 8))
                                   for q in window(k)) for k in range(K)]))
@@ -449,8 +452,11 @@ def run_ours(args, rank, world, local):
                        "dim": e.embedding_dim, "queries_per_step": Q,
                        "items_per_step": items_step, "sla_s": sla,
                        "fc_path": args.fc, "parallelism": f"replicas{world}",
-                       "input_format": ("int32 indices: LABELLED variant (SURVEY 8f-2), not "
-                                        "the reference byte model" if i32 else
+                       "input_format": ("LABELLED variant (SURVEY 8f-2), not the reference "
+                                        "byte model: " + " + ".join(
+                                            (["int32 indices"] if i32 else []) +
+                                            (["bf16 dense"] if bf16 else []))
+                                        if (i32 or bf16) else
                                         "reference byte model (int64 indices + fp32 dense)"),
                        "query_merging": (f"up to {args.merge} consecutive queries per launch: "
                                          "LABELLED scheduler extension (SURVEY 8f-3)"
@@ -522,6 +528,8 @@ def main():
                     help="LogNormal(ln m, 0.5) query sizes (SURVEY 8d: 300; 30 = small-query regime)")
     ap.add_argument("--merge", type=int, default=1,
                     help=">1 = labelled query-merging variant (SURVEY 8f-3)")
+    ap.add_argument("--dense-bits", type=int, choices=[32, 16], default=32,
+                    help="16 = labelled bf16 dense-feature input variant (SURVEY 8f-2)")
     ap.add_argument("--index-bits", type=int, choices=[64, 32], default=64,
                     help="32 = labelled int32-index input variant (SURVEY 8f-2)")
     ap.add_argument("--max-query", type=int, default=1000)

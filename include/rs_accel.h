@@ -192,18 +192,20 @@ typedef struct rs_init_desc {
  * lookup) — the byte model of accel_input_bytes (platform.cpp:105-111).
  * location RS_MEM_HOST: pointers are host memory (pinned for async copy);
  * RS_MEM_DEVICE: pointers are device memory on the handle's GPU.
- * index_type RS_INDEX_I32 is a LABELLED input-format variant (SURVEY
- * §8f-2): `indices` then points at int32 values (half the host-link bytes);
- * they are widened on the device and the forward is bit-identical to the
- * int64 query with the same values. Default RS_INDEX_I64 = the reference.  */
+ * index_type holds LABELLED input-format flags; 0 = the
+ * reference byte model. RS_INDEX_I32: `indices` points at int32 values (half
+ * the index bytes), widened on the device — bit-identical to the int64
+ * query. RS_DENSE_BF16: `dense` points at bfloat16 values (half the dense
+ * bytes), widened on the device — identical to the fp32 query whose dense
+ * features are those bf16 values.                                           */
 enum { RS_MEM_HOST = 0, RS_MEM_DEVICE = 1 };
-enum { RS_INDEX_I64 = 0, RS_INDEX_I32 = 1 };
+enum { RS_INDEX_I64 = 0, RS_INDEX_I32 = 1, RS_DENSE_BF16 = 2 };
 typedef struct rs_query {
   int64_t size;
   const float* dense;
   const int64_t* indices;   /* int32_t* when index_type == RS_INDEX_I32 */
   int32_t location;
-  int32_t index_type;       /* RS_INDEX_* (0 = int64, the reference)    */
+  int32_t index_type;       /* RS_INDEX_I32 | RS_DENSE_BF16 flags (0 = reference) */
 } rs_query;
 
 /* Per-call timing (CUDA events on the call's stream), milliseconds.        */

@@ -101,6 +101,7 @@ FC_FP32, FC_TF32, FC_AUTO = 0, 1, 2
 RNN_GRU, RNN_AUGRU = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 INDEX_I64, INDEX_I32 = 0, 1  # rs_query.index_type (I32: labelled input variant)
+DENSE_BF16 = 2               # rs_query.index_type flag: bf16 dense (labelled variant)
 OPT_MERGE_QUERIES = 1        # rs_accel_set_option (labelled scheduler extension)
 
 
@@ -555,12 +556,14 @@ class Accelerator:
         """Host numpy in, host numpy out (synchronous): logits [S, stacks*out].
         int32 `idx` selects the labelled INDEX_I32 input variant."""
         S = int(idx.shape[0]) if idx.size else int(dense.shape[0])
-        dense = np.ascontiguousarray(dense, dtype=np.float32)
+        bf16 = dense.dtype == np.uint16  # raw bfloat16 bit patterns: labelled variant
+        dense = np.ascontiguousarray(dense, dtype=np.uint16 if bf16 else np.float32)
         i32 = idx.dtype == np.int32
         idx = np.ascontiguousarray(idx, dtype=np.int32 if i32 else np.int64)
         out = np.empty((S, self.output_dim), dtype=np.float32)
         self.forward_ptr(S, dense.ctypes.data, idx.ctypes.data, out.ctypes.data, MEM_HOST,
-                         timed=True, index_type=INDEX_I32 if i32 else INDEX_I64)
+                         timed=True, index_type=(INDEX_I32 if i32 else INDEX_I64) |
+                         (DENSE_BF16 if bf16 else 0))
         return out
 
     def pooled(self, idx: np.ndarray, dense: Optional[np.ndarray] = None) -> np.ndarray:

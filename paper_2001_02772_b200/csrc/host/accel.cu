@@ -701,8 +701,7 @@ void check_query(rs_accel* a, const rs_query* q) {
   if (q->location != RS_MEM_HOST && q->location != RS_MEM_DEVICE)
     raise(RS_E_INVALID, "bad memory location");
   if (a->T > 0 && !q->indices) raise(RS_E_INVALID, "null indices");
-  if (q->index_type != RS_INDEX_I64 && q->index_type != RS_INDEX_I32)
-    raise(RS_E_INVALID, "bad index_type");
+  if (q->index_type & ~(RS_INDEX_I32 | RS_DENSE_BF16)) raise(RS_E_INVALID, "bad index_type");
 }
 
 // Stage one query's inputs for slot s on stream st: dense features into the
@@ -714,18 +713,18 @@ void check_query(rs_accel* a, const rs_query* q) {
 // previous copy executed.
 void write_desc(rs_accel* a, Slot* s, const QDesc& v, cudaStream_t st) {
   if (a->memops) {
-    const uint64_t vals[4] = {(uint64_t)v.S, (uint64_t)reinterpret_cast<uintptr_t>(v.idx),
+    const uint64_t vals[5] = {(uint64_t)v.S, (uint64_t)reinterpret_cast<uintptr_t>(v.idx),
                               (uint64_t)reinterpret_cast<uintptr_t>(v.dense),
-                              (uint64_t)reinterpret_cast<uintptr_t>(v.out)};
-    CUstreamBatchMemOpParams ops[4];
+                              (uint64_t)reinterpret_cast<uintptr_t>(v.out), (uint64_t)v.flags};
+    CUstreamBatchMemOpParams ops[5];
     std::memset(ops, 0, sizeof(ops));
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 5; ++k) {
       ops[k].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
       ops[k].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
       ops[k].writeValue.address = reinterpret_cast<CUdeviceptr>(s->d_q) + 8 * k;
       ops[k].writeValue.value64 = (cuuint64_t)vals[k];
     }
-    if (a->memops(reinterpret_cast<CUstream>(st), 4, ops, 0) != CUDA_SUCCESS)
+    if (a->memops(reinterpret_cast<CUstream>(st), 5, ops, 0) != CUDA_SUCCESS)
       raise(RS_E_CUDA, "cuStreamBatchMemOp failed");
     return;
   }
@@ -776,7 +775,7 @@ BatchMemOpFn probe_memops(rs_accel* a) {
 // RS_INDEX_I32: widen the slot's int32 indices (landing zone, or the caller's
 // device buffer) into the int64 staging buffer on stream st.
 void widen_indices(rs_accel* a, Slot* s, const rs_query* q, cudaStream_t st) {
-  if (a->T == 0 || q->index_type != RS_INDEX_I32) return;
+  if (a->T == 0 || !(q->index_type & RS_INDEX_I32)) return;
   const int64_t n = q->size * a->T * a->L;
   const int32_t* src = q->location == RS_MEM_HOST ? s->idx32_src
                                                   : reinterpret_cast<const int32_t*>(q->indices);
@@ -792,8 +791,10 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
   const bool host = q->location == RS_MEM_HOST;
   QDesc v{};
   v.S = S;
-  const int64_t dense_bytes = S * a->dense_in * 4;
-  const bool i32 = q->index_type == RS_INDEX_I32;
+  const bool bf16 = (q->index_type & RS_DENSE_BF16) != 0;
+  const int64_t dense_bytes = S * a->dense_in * (bf16 ? 2 : 4);
+  const bool i32 = (q->index_type & RS_INDEX_I32) != 0;
+  v.flags = bf16 ? kDescDenseBf16 : 0;
   s->idx32_src = s->idx32_stage;
   if (host && full && a->dense_in > 0 && a->T > 0 && q->dense && dense_bytes % 8 == 0 &&
       reinterpret_cast<const uint8_t*>(q->indices) ==
@@ -823,7 +824,7 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
   if (full && a->dense_in > 0) {
     if (!q->dense) raise(RS_E_INVALID, "null dense features");
     if (host) {
-      RS_CUDA(cudaMemcpyAsync(s->dense_raw, q->dense, (size_t)(S * a->dense_in * 4),
+      RS_CUDA(cudaMemcpyAsync(s->dense_raw, q->dense, (size_t)dense_bytes,
                               cudaMemcpyHostToDevice, st));
       v.dense = s->dense_raw;
     } else {
@@ -834,7 +835,7 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
   const int64_t* idx = nullptr;
   if (a->T > 0) {
     const int64_t n = S * a->T * a->L;
-    if (q->index_type == RS_INDEX_I32) {
+    if (i32) {
       // labelled variant: int32 over the link (or in place), widened on device
       if (host)
         RS_CUDA(cudaMemcpyAsync(s->idx32_stage, q->indices, (size_t)(n * 4),
@@ -924,7 +925,9 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
 int64_t stage_group(rs_accel* a, Slot* s, const rs_query* qs, int64_t m, cudaStream_t st) {
   const bool host = qs[0].location == RS_MEM_HOST;
   const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  const bool i32 = qs[0].index_type == RS_INDEX_I32;
+  const bool i32 = (qs[0].index_type & RS_INDEX_I32) != 0;
+  if (qs[0].index_type & RS_DENSE_BF16)
+    raise(RS_E_INVALID, "query merging does not take bf16 dense features");
   const int64_t TL = a->T * a->L;
   int64_t off = 0;
   if (!host) {
@@ -1046,6 +1049,7 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
       // the same index type whose items fit one slot
       int64_t j = i + 1, items = qs[i].size;
       while (!pool_only && j < n && j - i < a->merge_queries &&
+             !(qs[i].index_type & RS_DENSE_BF16) &&
              items + qs[j].size <= maxS && qs[j].index_type == qs[i].index_type)
         items += qs[j++].size;
       const int d = (int)(group % depth);
@@ -1076,7 +1080,7 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
           RS_CUDA(cudaEventRecord(s->ready, sst));
           RS_CUDA(cudaStreamWaitEvent(ls, s->ready, 0));
         }
-        if (loc == RS_MEM_HOST && a->T > 0 && qs[i].index_type == RS_INDEX_I32)
+        if (loc == RS_MEM_HOST && a->T > 0 && (qs[i].index_type & RS_INDEX_I32))
           launch_widen_idx(s->idx32_stage, s->idx_stage, S * a->T * a->L, a->sm_count, ls);
         RS_CUDA(cudaGraphLaunch(pick_graph(a, s, S, true), ls));
         int64_t off = 0;

@@ -21,7 +21,9 @@ struct QDesc {
   const int64_t* idx;  // [S, T, L] int64 (device)
   const float* dense;  // [S, dense_in] fp32 contiguous (device), or null
   float* out;          // final logits [S, out_w] (device) or null: slot buffer
+  int64_t flags;       // kDescDenseBf16: `dense` holds bfloat16 values
 };
+constexpr int64_t kDescDenseBf16 = 1;
 
 // Error bits accumulated by kernels and read back with the logits.
 enum : int { kErrIndex = 1 };

@@ -1219,6 +1219,16 @@ stage_dense_kernel(const QDesc* __restrict__ qd, int64_t dense_in, float* __rest
   const float* __restrict__ src = qd->dense;
   const int64_t S = qd->S;
   if (!src) return;
+  if (qd->flags & kDescDenseBf16) {  // labelled bf16-dense input variant
+    const uint16_t* __restrict__ h = reinterpret_cast<const uint16_t*>(src);
+    const int64_t total = S * dense_in;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = i / dense_in, c = i - r * dense_in;
+      dst[r * ld_dst + c] = __uint_as_float((uint32_t)__ldg(h + i) << 16);
+    }
+    return;
+  }
   const bool vec = (dense_in % 4 == 0) && (ld_dst % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
   if (vec) {

@@ -425,3 +425,30 @@ def test_sls_bandwidth_floor():
     gbs = S * (T * L * (D * 4 + 8) + T * D * 4) / (min(times) * 1e-3) / 1e9
     assert gbs >= 5000, f"SLS {gbs:.0f} GB/s"
     acc.close()
+
+
+@pytest.mark.parametrize("name", ["WND", "DLRM-RMC1"])
+def test_bf16_dense_variant_matches_rounded_fp32(name):
+    """RS_DENSE_BF16 (labelled input-format flag): bfloat16 dense
+    features over the link, widened on the device — identical to the fp32
+    query whose dense features are the same bf16 values; combinable with int32
+    indices; packed single-transfer path included."""
+    spec = rs.builtin_model(name)
+    rows = 4000
+    acc = rs.Accelerator(spec, rows, seed=5, max_query_size=200, fc_mode=rs.FC_AUTO)
+    for S in (2, 150):
+        dense, idx = rs.fill_query(spec, rows, 8, S, S)
+        bits = (dense.view(np.uint32) >> 16).astype(np.uint16)  # truncate to bf16
+        rounded = (bits.astype(np.uint32) << 16).view(np.float32)
+        ref = acc.forward(rounded, idx)
+        assert np.array_equal(acc.forward(bits, idx), ref)
+        assert np.array_equal(acc.forward(bits, idx.astype(np.int32)), ref)
+        buf = rs.PinnedBuffer(bits.nbytes + idx.nbytes)
+        raw = buf.view(np.uint8, (bits.nbytes + idx.nbytes,))
+        raw[:bits.nbytes] = bits.reshape(-1).view(np.uint8)
+        raw[bits.nbytes:] = idx.reshape(-1).view(np.uint8)
+        out = rs.PinnedBuffer(S * acc.output_dim * 4)
+        acc.forward_ptr(S, buf.ptr, buf.ptr + bits.nbytes, out.ptr, rs.MEM_HOST, timed=True,
+                        index_type=rs.DENSE_BF16)
+        assert np.array_equal(out.view(np.float32, (S, acc.output_dim)), ref)
+    acc.close()
