@@ -359,6 +359,28 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
                   float* final_out, int64_t ld_final, int64_t final_sCz, bool allow_tc,
                   cudaStream_t st, bool final_to_desc = false) {
   const int64_t maxS = a->init.max_query_size;
+  // The whole stack as one tcgen05 kernel when every layer fits (activations
+  // stay in shared memory between layers): one launch instead of one per layer.
+  if (allow_tc && !layers.empty() && (int)layers.size() <= kChainMaxLayers + 1) {
+    FcArgs ly[kChainMaxLayers + 1];
+    for (size_t l = 0; l < layers.size(); ++l) {
+      const FcLayer& f = layers[l];
+      FcArgs& x = ly[l];
+      x = FcArgs{};
+      x.A = l == 0 ? in0 : nullptr; x.lda = ld_in0;
+      x.W = f.W; x.ldw = f.ldk; x.sWz = f.out * f.ldk;
+      x.bias = f.b; x.sbz = f.out;
+      x.N = (int)f.out; x.K = (int)f.in; x.relu = f.relu; x.batch = f.batch;
+    }
+    FcArgs& fin = ly[layers.size() - 1];
+    fin.C = final_out; fin.ldc = ld_final; fin.sCz = final_sCz;
+    fin.c_desc = final_to_desc ? 1 : 0;
+    TcChainPlan cp;
+    if (tc_chain_plan(&cp, ly, (int)layers.size(), maxS, in0_rows)) {
+      launch_fc_chain(s->d_q, cp, st);
+      return (int)layers.size();
+    }
+  }
   int tc_count = 0;
   const float* in = in0;
   int64_t lda = ld_in0, sAz = 0, a_rows = in0_rows;

@@ -328,6 +328,240 @@ void set_attr_once() {
   });
 }
 
+// ---------------------------------------------------------------------------
+// fc_chain_kernel: a whole FC stack per 128-row tile (see TcChainPlan).
+// Warps 0-3: epilogue (TMEM lanes 32w..32w+31 = tile rows) and, between
+// layers, the writers of the next layer's A operand; warp 4 lane 0: TMA
+// producer (layer-0 input, then every layer's weight k-blocks through a
+// 2-stage ring, running ahead into the next layer); warp 5 lane 0: MMA issuer.
+constexpr int kChainThreads = 192;
+constexpr int kChainActAtoms = 8;  // activations up to 256 wide stay in smem
+constexpr int kChainMaxStages = 8;
+constexpr int kChainRingBytes = 96 * 1024;
+
+// The k-block ring is one byte pool cut into `stages` slots of `slot` bytes
+// (planned per stack: [A k-block of the streamed layer-0 input] + the widest
+// layer's W k-block), so narrow stacks get a deeper pipeline.
+struct ChainSmem {
+  alignas(1024) float act[kChainActAtoms][BM * BK];  // SW128 K-major, 16 KB per atom
+  alignas(1024) uint8_t ring[kChainRingBytes];
+  uint64_t full[kChainMaxStages];
+  uint64_t empty[kChainMaxStages];
+  uint64_t act_in;     // layer-0 input resident in act
+  uint64_t acc_full;   // a layer's accumulation finished
+  uint64_t act_ready;  // epilogue wrote the next layer's A (128 arrivals)
+  uint32_t tmem_base;
+};
+
+// byte offset of fp32 element (row, c) inside a 128-row x 32-col SW128 atom
+__device__ __forceinline__ uint32_t chain_sw(int row, int c) {
+  return (uint32_t)(row * 128 + ((((c >> 2) ^ row) & 7) << 4) + (c & 3) * 4);
+}
+
+__global__ void __launch_bounds__(kChainThreads, 1)
+fc_chain_kernel(const QDesc* __restrict__ qd, const __grid_constant__ TcChainPlan p) {
+  extern __shared__ uint8_t smem_raw[];
+  ChainSmem& sm = *reinterpret_cast<ChainSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int64_t M = qd->S;
+  const int m0 = blockIdx.x * BM;
+  if (m0 >= M) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 4 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.map_a)) : "memory");
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    mbar_init(&sm.act_in, 1);
+    mbar_init(&sm.acc_full, 1);
+    mbar_init(&sm.act_ready, 4 * 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+  pdl_wait();  // the input rows are the previous kernel's output
+  const int L = p.layers;
+
+  if (warp == 4) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      if (!p.stream_a) {
+        const int na = (p.k[0] + BK - 1) / BK;
+        mbar_expect_tx(&sm.act_in, (uint32_t)(na * BM * BK * 4));
+        for (int a = 0; a < na; ++a) tma_load_2d(sm.act[a], &p.map_a, &sm.act_in, a * BK, m0);
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      for (int l = 0; l < L; ++l) {
+        const int nk = (p.k[l] + BK - 1) / BK;
+        const bool sa = l == 0 && p.stream_a;
+        const uint32_t bytes = (uint32_t)(p.np[l] * BK * 4) + (sa ? (uint32_t)(BM * BK * 4) : 0u);
+        for (int kb = 0; kb < nk; ++kb) {
+          uint8_t* slot = sm.ring + s * p.slot;
+          mbar_wait(&sm.empty[s], ph ^ 1u);
+          mbar_expect_tx(&sm.full[s], bytes);
+          tma_load_2d(slot + p.slot_b, &p.map_w[l], &sm.full[s], kb * BK, 0);
+          if (sa) tma_load_2d(slot, &p.map_a, &sm.full[s], kb * BK, m0);
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int l = 0; l < L; ++l) {
+        if (l == 0 && !p.stream_a) mbar_wait(&sm.act_in, 0);
+        if (l > 0) mbar_wait(&sm.act_ready, (uint32_t)((l - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                               ((uint32_t)(p.np[l] >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+        const bool sa = l == 0 && p.stream_a;
+        const int nk = (p.k[l] + BK - 1) / BK;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&sm.full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* slot = sm.ring + s * p.slot;
+          const uint32_t sa_addr = smem_u32(sa ? slot : reinterpret_cast<const uint8_t*>(sm.act[kb]));
+          const uint32_t sb_addr = smem_u32(slot + p.slot_b);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            asm volatile(
+                "{\n.reg .pred q;\nsetp.ne.b32 q, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n}\n" ::"r"(tmem),
+                "l"(sw128_desc(sa_addr + kk * 32)), "l"(sw128_desc(sb_addr + kk * 32)),
+                "r"(idesc), "r"(acc)
+                : "memory");
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  smem_u32(&sm.empty[s]))
+              : "memory");
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&sm.acc_full))
+            : "memory");
+      }
+    }
+  } else {
+    // ---- epilogue: warps 0-3, thread = tile row ----
+    const int row = warp * 32 + lane;
+    const int64_t m = m0 + row;
+    for (int l = 0; l < L; ++l) {
+      mbar_wait(&sm.acc_full, (uint32_t)(l & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const bool last = l == L - 1;
+      if (last) pdl_trigger();
+      const float* __restrict__ bias = p.bias[l];
+      const int N = p.n[l];
+      float part[kFuseMaxN2] = {0.f, 0.f, 0.f, 0.f};
+      float* __restrict__ Cb = (p.c_desc && qd->out) ? qd->out : p.C;
+      for (int c = 0; c < p.np[l] / 32 + ((p.np[l] & 31) ? 1 : 0); ++c) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32);
+        if (c * 32 + 16 < p.np[l]) {
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+              "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                "=r"(v[30]), "=r"(v[31])
+              : "r"(taddr));
+        } else {  // a 16-column tail (np % 32 == 16)
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+              "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr));
+#pragma unroll
+          for (int i = 16; i < 32; ++i) v[i] = 0u;
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float y[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int n = c * 32 + i;
+          const float val = n < N ? __uint_as_float(v[i]) + __ldg(bias + n) : 0.f;
+          y[i] = (p.relu[l] && n < N) ? fmaxf(val, 0.f) : val;
+        }
+        if (!last) {
+          // next layer's A operand: row `row`, columns 32c..32c+31 (zeros past N)
+          uint8_t* atom = reinterpret_cast<uint8_t*>(sm.act[c]);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(atom + chain_sw(row, 4 * q)) =
+                make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+        } else if (m < M) {
+          if (p.N2 > 0) {
+#pragma unroll
+            for (int o = 0; o < kFuseMaxN2; ++o) {
+              if (o >= p.N2) break;
+              const float* __restrict__ w = p.W2 + (int64_t)o * p.ldw2 + c * 32;
+              float acc2 = part[o];
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (c * 32 + i < N) acc2 = fmaf(y[i], __ldg(w + i), acc2);
+              part[o] = acc2;
+            }
+          } else {
+            float* __restrict__ C = Cb + m * p.ldc;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i < N) C[c * 32 + i] = y[i];
+          }
+        }
+      }
+      if (!last) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.act_ready))
+                     : "memory");
+      } else if (p.N2 > 0 && m < M) {
+#pragma unroll
+        for (int o = 0; o < kFuseMaxN2; ++o) {
+          if (o >= p.N2) break;
+          const float val = part[o] + __ldg(p.b2 + o);
+          Cb[m * p.ldc + o] = p.relu2 ? fmaxf(val, 0.f) : val;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256)
+                 : "memory");
+  }
+}
+
 }  // namespace
 
 bool tc_available() { return encode_fn() != nullptr; }
@@ -396,6 +630,78 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
     default: set_attr_once<64, 8>(); break;
   }
   return true;
+}
+
+bool tc_chain_plan(TcChainPlan* p, const FcArgs* ly, int L, int64_t m_cap, int64_t a_rows) {
+  // Off by default (RS_FC_CHAIN=1 enables): measured slower than one kernel
+  // per layer at the zoo/cfg shapes (cfg1 RMC1 9.4 -> 10.3 us/query pipelined,
+  // 52 -> 67 us alone): a chain CTA must own whole rows, so a 256-wide layer
+  // runs on half the CTAs the per-layer kernels use, and the launches saved
+  // do not pay for the lost parallelism.
+  if (!tc_available() || L < 1) return false;
+  const char* e = getenv("RS_FC_CHAIN");
+  if (!e || !atoi(e)) return false;
+  std::memset(p, 0, sizeof(*p));
+  // a final layer of <= 4 outputs after a <= 256-wide layer runs in the epilogue
+  int nl = L;
+  const bool narrow = L >= 2 && ly[L - 1].N <= kFuseMaxN2 && ly[L - 2].N <= 256;
+  if (narrow) nl = L - 1;
+  if (nl > kChainMaxLayers) return false;
+  for (int l = 0; l < L; ++l) {
+    const FcArgs& a = ly[l];
+    if (a.batch != 1) return false;
+    if (a.ldw % 4 || (reinterpret_cast<uintptr_t>(a.W) & 15)) return false;
+  }
+  if (ly[0].lda % 4 || (reinterpret_cast<uintptr_t>(ly[0].A) & 15)) return false;
+  for (int l = 0; l < nl; ++l) {
+    if (ly[l].N > 256 || ly[l].N < 16 || ly[l].K < 4) return false;
+    if (l > 0 && ly[l].K > kChainActAtoms * BK) return false;
+  }
+  p->layers = nl;
+  p->stream_a = ly[0].K > kChainActAtoms * BK ? 1 : 0;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)ly[0].K, (cuuint64_t)a_rows};
+    cuuint64_t str[1] = {(cuuint64_t)ly[0].lda * 4};
+    cuuint32_t box[2] = {BK, BM};
+    if (!encode(&p->map_a, ly[0].A, 2, dims, str, box)) return false;
+  }
+  for (int l = 0; l < nl; ++l) {
+    const FcArgs& a = ly[l];
+    p->n[l] = a.N;
+    p->np[l] = (a.N + 15) / 16 * 16;
+    p->k[l] = a.K;
+    p->relu[l] = a.relu;
+    p->bias[l] = a.bias;
+    cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.N};
+    cuuint64_t str[1] = {(cuuint64_t)a.ldw * 4};
+    cuuint32_t box[2] = {BK, (cuuint32_t)p->np[l]};
+    if (!encode(&p->map_w[l], a.W, 2, dims, str, box)) return false;
+  }
+  const FcArgs& out = ly[L - 1];
+  p->C = out.C;
+  p->ldc = out.ldc;
+  p->c_desc = out.c_desc;
+  if (narrow) {
+    p->W2 = out.W; p->ldw2 = out.ldw; p->b2 = out.bias; p->N2 = out.N; p->relu2 = out.relu;
+  }
+  int wmax = 0;
+  for (int l = 0; l < nl; ++l) wmax = std::max(wmax, p->np[l] * BK * 4);
+  p->slot_b = p->stream_a ? BM * BK * 4 : 0;           // 1 KB multiples: SW128 atoms
+  p->slot = p->slot_b + (wmax + 1023) / 1024 * 1024;
+  p->stages = std::min(kChainMaxStages, kChainRingBytes / p->slot);
+  if (p->stages < 2) return false;
+  p->m_tiles = (int)((m_cap + BM - 1) / BM);
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(fc_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(ChainSmem) + 1024));
+  });
+  return true;
+}
+
+void launch_fc_chain(const QDesc* qd, const TcChainPlan& p, cudaStream_t s) {
+  launch_pdl(fc_chain_kernel, dim3(p.m_tiles), dim3(kChainThreads), sizeof(ChainSmem) + 1024, s,
+             qd, p);
 }
 
 void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s) {

@@ -83,6 +83,33 @@ bool make_row_gather_map(CUtensorMap* map, const float* base, int64_t total_rows
 bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch);
 void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s);
 
+// A whole FC stack in ONE kernel (fc_tcgen05.cu, fc_chain_kernel): per
+// 128-row tile the activations stay in shared memory between layers (as the
+// next layer's swizzled K-major A operand), weights stream by TMA, each
+// layer accumulates in TMEM. Layers with N <= 256 and hidden widths <= 256;
+// an optional final layer of <= 4 outputs runs in the last epilogue.
+constexpr int kChainMaxLayers = 4;
+struct TcChainPlan {
+  CUtensorMap map_a;                   // layer-0 input [rows][K0], box 32 x 128
+  CUtensorMap map_w[kChainMaxLayers];  // W_l [N_l][K_l], box 32 x NP_l
+  const float* bias[kChainMaxLayers];
+  int n[kChainMaxLayers];              // N_l
+  int np[kChainMaxLayers];             // N_l rounded up to 16 (UMMA N)
+  int k[kChainMaxLayers];              // K_l
+  int relu[kChainMaxLayers];
+  int layers;
+  int stream_a;                        // layer-0 input streamed per k-block (K0 > 256)
+  int slot, slot_b, stages;            // k-block ring: slot bytes, W offset in a slot, depth
+  float* C; int64_t ldc; int c_desc;   // output of the last layer
+  const float* W2; int64_t ldw2; const float* b2; int N2; int relu2;  // fused narrow layer
+  int m_tiles;
+};
+// Plans a chain for layers [0, L) of `layers` (FcArgs of each, batch 1);
+// false if some layer does not fit (the caller runs them one by one).
+bool tc_chain_plan(TcChainPlan* p, const FcArgs* layers, int L, int64_t m_cap,
+                   int64_t a_rows);
+void launch_fc_chain(const QDesc* qd, const TcChainPlan& p, cudaStream_t s);
+
 // ---- gru.cu ----
 struct GruArgs {
   const float* tables; int64_t rows; int T; int L; int D; int H;

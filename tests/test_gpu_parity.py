@@ -87,7 +87,8 @@ def test_cfg1_rmc1_single_query_batch64():
     check_forward(spec, rows=1_000_000, S=64, max_q=64)
 
 
-@pytest.mark.parametrize("name", ["MT-WND", "WND", "DLRM-RMC3"])
+@pytest.mark.parametrize("name", ["MT-WND", "WND", "DLRM-RMC3", "DLRM-RMC1", "DLRM-RMC2", "NCF",
+                                  "DIN", "DIEN"])
 def test_tf32_tcgen05_path(name):
     spec = rs.builtin_model(name)
     acc = rs.Accelerator(spec, 2000, seed=1, max_query_size=300, fc_mode=rs.FC_TF32)
@@ -452,3 +453,14 @@ def test_bf16_dense_variant_matches_rounded_fp32(name):
                         index_type=rs.DENSE_BF16)
         assert np.array_equal(out.view(np.float32, (S, acc.output_dim)), ref)
     acc.close()
+
+
+@pytest.mark.parametrize("name", ["DLRM-RMC1", "DIN", "NCF"])
+def test_fc_chain_kernel_parity(name, monkeypatch):
+    """The whole-stack tcgen05 kernel (RS_FC_CHAIN=1, off by default — measured
+    slower): activations kept in shared memory between layers, streamed
+    layer-0 input (DIN's 640-wide), fused narrow output; tf32 tolerance."""
+    monkeypatch.setenv("RS_FC_CHAIN", "1")
+    spec = rs.builtin_model(name)
+    for S in (1, 130, 300):
+        check_forward(spec, rows=3000, S=S, fc_mode=rs.FC_TF32, tol=TF32_TOL, max_q=300)
