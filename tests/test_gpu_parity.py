@@ -464,3 +464,57 @@ def test_fc_chain_kernel_parity(name, monkeypatch):
     spec = rs.builtin_model(name)
     for S in (1, 130, 300):
         check_forward(spec, rows=3000, S=S, fc_mode=rs.FC_TF32, tol=TF32_TOL, max_q=300)
+
+
+def test_queue_edge_cases():
+    """16 lanes; merged groups of int32 queries (host and device); a bad index
+    inside rs_forward_many and inside rs_serve is reported after the call and
+    the handle keeps serving."""
+    torch = pytest.importorskip("torch")
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 3000
+    acc = rs.Accelerator(spec, rows, seed=3, max_query_size=300, fc_mode=rs.FC_FP32,
+                         queue_depth=16)
+    sizes = [7, 33, 120, 5, 64, 200, 1, 90] * 3
+    qs = [rs.fill_query(spec, rows, 1, k, S) for k, S in enumerate(sizes)]
+    singles = [acc.forward(d, i) for d, i in qs]
+    for merge in (1, 3):
+        acc.set_option(rs.OPT_MERGE_QUERIES, merge)
+        for loc in (rs.MEM_HOST, rs.MEM_DEVICE):
+            if loc == rs.MEM_HOST:
+                bd = [rs.PinnedBuffer(max(d.nbytes, 16)) for d, _ in qs]
+                bi = [rs.PinnedBuffer(i.nbytes // 2) for _, i in qs]
+                for k, (d, i) in enumerate(qs):
+                    bd[k].view(np.float32, d.shape)[...] = d
+                    bi[k].view(np.int32, i.shape)[...] = i.astype(np.int32)
+                outs = [rs.PinnedBuffer(S * acc.output_dim * 4) for S in sizes]
+                b = acc.batch(sizes, [x.ptr for x in bd], [x.ptr for x in bi],
+                              [o.ptr for o in outs], loc, index_type=rs.INDEX_I32)
+                acc.forward_many(None, prepared=b)
+                got = [outs[k].view(np.float32, (S, acc.output_dim)) for k, S in
+                       enumerate(sizes)]
+            else:
+                dd = [torch.from_numpy(d).cuda() for d, _ in qs]
+                di = [torch.from_numpy(i.astype(np.int32)).cuda() for _, i in qs]
+                do = [torch.empty((S, acc.output_dim), device="cuda") for S in sizes]
+                b = acc.batch(sizes, [t.data_ptr() for t in dd], [t.data_ptr() for t in di],
+                              [t.data_ptr() for t in do], loc, index_type=rs.INDEX_I32)
+                acc.forward_many(None, prepared=b)
+                got = [t.cpu().numpy() for t in do]
+            for k in range(len(sizes)):
+                assert np.array_equal(got[k], singles[k]), (merge, loc, k)
+    acc.set_option(rs.OPT_MERGE_QUERIES, 1)
+    # a bad index in the queue and in the real-time executor
+    d, i = qs[2]
+    bad = i.copy()
+    bad[3, 0, 0] = rows
+    dd, dbad = torch.from_numpy(d).cuda(), torch.from_numpy(bad).cuda()
+    out = torch.empty((sizes[2], acc.output_dim), device="cuda")
+    b = acc.batch([sizes[2]], [dd.data_ptr()], [dbad.data_ptr()], [out.data_ptr()],
+                  rs.MEM_DEVICE)
+    with pytest.raises(rs.IndexOutOfRange):
+        acc.forward_many(None, prepared=b)
+    with pytest.raises(rs.IndexOutOfRange):
+        rs.serve([acc], b, np.zeros(1))
+    assert np.array_equal(acc.forward(d, i), singles[2])
+    acc.close()
