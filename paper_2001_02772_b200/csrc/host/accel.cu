@@ -75,7 +75,7 @@ struct Slot {
   cudaStream_t cap = nullptr;  // capture stream
   QDesc* d_q = nullptr;
   int* d_err = nullptr;
-  int* h_err = nullptr;        // pinned [kDescRing] (only [0] is used)
+  int* h_err = nullptr;        // pinned error word read-back
   QDesc* h_q = nullptr;        // pinned descriptor ring [kDescRing]
   cudaEvent_t q_ev[kDescRing] = {};  // last copy out of each ring entry
   int ring = 0;
@@ -629,9 +629,8 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   s->d_q = static_cast<QDesc*>(dmalloc(a, s->allocs, sizeof(QDesc)));
   RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_q), sizeof(QDesc) * kDescRing,
                         cudaHostAllocPortable));
-  RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_err), sizeof(int) * kDescRing,
-                        cudaHostAllocPortable));
-  std::memset(s->h_err, 0, sizeof(int) * kDescRing);
+  RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_err), sizeof(int), cudaHostAllocPortable));
+  s->h_err[0] = 0;
   s->d_err = static_cast<int*>(dmalloc(a, s->allocs, sizeof(int)));
   s->dense_stage = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_dense * 4)));
   s->dense_raw = static_cast<float*>(
@@ -1461,10 +1460,15 @@ extern "C" int rs_service_time(rs_accel* a, int64_t query_size, double* seconds)
       }
     }
     const int64_t S = query_size;
-    void *dense = nullptr, *idx = nullptr, *out = nullptr;
-    RS_CUDA(cudaHostAlloc(&dense, (size_t)std::max<int64_t>(S * a->dense_in * 4, 16), 0));
-    RS_CUDA(cudaHostAlloc(&idx, (size_t)std::max<int64_t>(S * a->T * a->L * 8, 16), 0));
+    // one pinned buffer [dense | indices] (a packed query: one transfer when the
+    // dense block is a multiple of 8 bytes, as for every zoo shape)
+    const size_t dense_b = (size_t)(S * a->dense_in * 4 + 15) / 16 * 16;
+    const size_t idx_b = (size_t)(S * a->T * a->L * 8);
+    void *in = nullptr, *out = nullptr;
+    RS_CUDA(cudaHostAlloc(&in, std::max<size_t>(dense_b + idx_b, 16), 0));
     RS_CUDA(cudaHostAlloc(&out, (size_t)(S * a->out_w * 4), 0));
+    void* dense = in;
+    void* idx = static_cast<uint8_t*>(in) + dense_b;
     std::vector<double> t;
     int rc = rs_fill_query(&a->m, a->init.rows_per_table, a->init.seed ^ 0x5E41CEull, 0, S,
                            static_cast<float*>(dense), static_cast<int64_t*>(idx));
@@ -1474,7 +1478,7 @@ extern "C" int rs_service_time(rs_accel* a, int64_t query_size, double* seconds)
       rc = rs_forward(a, &q, static_cast<float*>(out), nullptr, &tm);
       if (i > 0) t.push_back(tm.total_ms * 1e-3);
     }
-    cudaFreeHost(dense); cudaFreeHost(idx); cudaFreeHost(out);
+    cudaFreeHost(in); cudaFreeHost(out);
     if (rc != RS_OK) raise(rc, rs_last_error());
     std::sort(t.begin(), t.end());
     const double med = t[t.size() / 2];
