@@ -85,6 +85,7 @@ struct Slot {
   int32_t* idx32_stage = nullptr;  // H2D landing zone of RS_INDEX_I32 queries
   uint8_t* landing = nullptr;      // one-DMA landing zone for packed host inputs
   const int32_t* idx32_src = nullptr;  // where this query's int32 indices landed
+  SplitKPool splitk;                   // split-K workspaces of this slot's graphs
   float* act[2] = {nullptr, nullptr};
   float* pooled = nullptr;
   float* X = nullptr;
@@ -415,7 +416,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
         args.skip_c = 1;
       }
       TcPlan p;
-      if (tc_plan(&p, args, maxS, a_rows) && (!fuse || p.n_tiles == 1)) {
+      if (tc_plan(&p, args, maxS, a_rows, &s->splitk) && (!fuse || p.n_tiles == 1)) {
         launch_fc_tc(s->d_q, p, args, st);
         used_tc = true;
         ++tc_count;
@@ -426,7 +427,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
       } else if (fuse) {
         args.single_n_tile = 0; args.N2 = 0; args.skip_c = 0; args.W2 = nullptr;
         args.b2 = nullptr; args.C2 = nullptr;
-        if (tc_plan(&p, args, maxS, a_rows)) {
+        if (tc_plan(&p, args, maxS, a_rows, &s->splitk)) {
           launch_fc_tc(s->d_q, p, args, st);
           used_tc = true;
           ++tc_count;
@@ -451,6 +452,10 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   // green context of the stream it was captured on, so one graph spans both.
   const bool part = s->gcap_d != nullptr;
   cudaStream_t st = part ? s->gcap_d : s->cap;
+  // graphs of one slot never run concurrently (one lane stream): each capture
+  // carves its split-K workspaces from the start of the slot's pool
+  s->splitk.ws_used = 0;
+  s->splitk.cnt_used = 0;
   cudaGraph_t g = nullptr;
   RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   const rs_model_desc& m = a->m;
@@ -641,6 +646,26 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
       dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->T * a->L, 1) * 4), false));
   s->landing = static_cast<uint8_t*>(
       dmalloc(a, s->allocs, (size_t)(maxS * (a->dense_in * 4 + a->T * a->L * 8) + 16), false));
+  {
+    // split-K scratch, sized for the long-K layers of this model (K >= 1024)
+    size_t ws = 0, cnt = 0;
+    auto need = [&](const std::vector<FcLayer>& ls) {
+      for (const FcLayer& f : ls)
+        if (f.in >= 1024) {
+          const size_t tiles = (size_t)f.batch * ((maxS + 127) / 128) * ((f.out + 63) / 64);
+          ws += 4 * tiles * 128 * 128;  // <= 4 splits of 128 x (BN <= 128... 256) partials
+          cnt += tiles;
+        }
+    };
+    need(a->dense_layers);
+    need(a->pred_layers);
+    if (ws) {
+      s->splitk.ws = static_cast<float*>(dmalloc(a, s->allocs, ws * 4 * 2, false));
+      s->splitk.ws_cap = ws * 2;
+      s->splitk.cnt = static_cast<int*>(dmalloc(a, s->allocs, cnt * 4 * 2));
+      s->splitk.cnt_cap = cnt * 2;
+    }
+  }
   for (int i = 0; i < 2; ++i) {
     s->act[i] = static_cast<float*>(
         dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->max_dense_w, 4) * 4)));

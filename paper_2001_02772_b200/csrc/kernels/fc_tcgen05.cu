@@ -96,6 +96,7 @@ struct TcSmem {
   uint64_t empty[STAGES];
   uint64_t tmem_full;
   uint32_t tmem_base;
+  int last;  // split-K: this CTA completes the tile
 };
 
 constexpr int kTcThreads = 128;
@@ -108,10 +109,18 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   TcSmem<BN, STAGES>& sm = *reinterpret_cast<TcSmem<BN, STAGES>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int64_t M = qd->S;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, z = blockIdx.z;
+  // split-K: grid.z = batch x splits; this CTA accumulates k-blocks
+  // [kb0, kb0 + nk) of the tile and the last of its splits to arrive sums the
+  // partials in split order (deterministic) and runs the epilogue
+  const int splits = a.splits > 1 ? a.splits : 1;
+  const int z = blockIdx.z / splits, sp = blockIdx.z - (blockIdx.z / splits) * splits;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   if (m0 >= M) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (a.K + BK - 1) / BK;
+  const int nk_all = (a.K + BK - 1) / BK;
+  const int per = (nk_all + splits - 1) / splits;
+  const int kb0 = sp * per;
+  const int nk = max(0, min(nk_all, kb0 + per) - kb0);
   const int pre = nk < STAGES ? nk : STAGES;  // stages whose weights load before the wait
 
   if (warp == 0 && lane == 0) {
@@ -144,7 +153,7 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < pre; ++kb) {
       mbar_expect_tx(&sm.full[kb], kBytes);
-      tma_load_3d(sm.b[kb], &map_w, &sm.full[kb], kb * BK, n0, z);
+      tma_load_3d(sm.b[kb], &map_w, &sm.full[kb], (kb0 + kb) * BK, n0, z);
     }
   }
   pdl_wait();  // the activations A are the previous layer's output
@@ -157,10 +166,10 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
       if (kb >= pre) {
         mbar_wait(&sm.empty[s], ph ^ 1u);
         mbar_expect_tx(&sm.full[s], kBytes);
-        tma_load_3d(sm.b[s], &map_w, &sm.full[s], kb * BK, n0, z);
+        tma_load_3d(sm.b[s], &map_w, &sm.full[s], (kb0 + kb) * BK, n0, z);
       }
-      if (a_batched) tma_load_3d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0, z);
-      else tma_load_2d(sm.a[s], &map_a, &sm.full[s], kb * BK, m0);
+      if (a_batched) tma_load_3d(sm.a[s], &map_a, &sm.full[s], (kb0 + kb) * BK, m0, z);
+      else tma_load_2d(sm.a[s], &map_a, &sm.full[s], (kb0 + kb) * BK, m0);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -204,6 +213,89 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
     pdl_trigger();
     const int quad = warp;
     const int64_t m = m0 + quad * 32 + lane;
+    if (splits > 1) {
+      // partial tile -> workspace; the last split to arrive reduces
+      const int64_t tile = ((int64_t)z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      const int64_t tiles = (int64_t)(gridDim.z / splits) * gridDim.y * gridDim.x;
+      const int rl = quad * 32 + lane;
+      float* __restrict__ mine = a.ws + ((int64_t)sp * tiles + tile) * (BM * BN) + rl * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+              "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (m < M) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            __stcg(reinterpret_cast<float4*>(mine + c * 32) + i,
+                   make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                               __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])));
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int old = atomicAdd(a.cnt + tile, 1);
+        sm.last = old == splits - 1;
+        if (sm.last) a.cnt[tile] = 0;  // ready for the next launch of this graph
+      }
+      __syncthreads();
+      if (sm.last && m < M) {
+        __threadfence();
+        float* __restrict__ Cb = (a.c_desc && qd->out) ? qd->out : a.C;
+        float* __restrict__ C = Cb + (int64_t)z * a.sCz + m * a.ldc;
+        const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int nb = n0 + c * 32;
+          float y[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) y[i] = 0.f;
+          // all splits' loads of a 16-column half in flight before the adds
+          // (split order kept: s2 = 0, 1, 2, 3)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float4 t4[4][4];
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+              const float4* src = reinterpret_cast<const float4*>(
+                  a.ws + ((int64_t)s2 * tiles + tile) * (BM * BN) + rl * BN + c * 32 + h * 16);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                t4[s2][i] = s2 < splits ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                float* yy = y + h * 16 + 4 * i;
+                yy[0] += t4[s2][i].x; yy[1] += t4[s2][i].y; yy[2] += t4[s2][i].z;
+                yy[3] += t4[s2][i].w;
+              }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int n = nb + i;
+            const float val = y[i] + (n < a.N ? __ldg(bias + n) : 0.f);
+            y[i] = a.relu ? fmaxf(val, 0.f) : val;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (nb + i < a.N) C[nb + i] = y[i];
+        }
+      }
+    } else {
     float* __restrict__ Cb = (a.c_desc && qd->out) ? qd->out : a.C;
     float* __restrict__ C = Cb + (int64_t)z * a.sCz + m * a.ldc;
     const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
@@ -273,6 +365,7 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
         C2[o] = a.relu2 ? fmaxf(val, 0.f) : val;
       }
     }
+    }  // splits == 1
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -576,7 +669,8 @@ bool make_row_gather_map(CUtensorMap* map, const float* base, int64_t total_rows
   return encode(map, base, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
-bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch) {
+bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch,
+             SplitKPool* pool) {
   if (a.N < 64 || a.K < BK) return false;
   if (a.lda % 4 || a.ldw % 4 || (a.sAz % 4) || (a.sWz % 4)) return false;
   if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.W) & 15))
@@ -628,6 +722,30 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
     case 2: set_attr_once<128, 6>(); break;
     case 4: set_attr_once<256, 4>(); break;
     default: set_attr_once<64, 8>(); break;
+  }
+  // Split-K for long reductions (K >= 1024: RMC3's 2560 -> 512, MT-WND/WND's
+  // 1640 -> 1024), RS_SPLITK=n (2..4) enables: a tile's k-blocks are spread
+  // over n CTAs and the last to arrive sums the partials in split order. Off
+  // by default: measured slower at every split count (tools/fc_micro.py, K=2560
+  // -> 512: 36 us unsplit vs 42-44 us split, independent of n — the layer's
+  // time is not in the per-CTA k-block chain). Not with a fused narrow layer.
+  p->splits = 1;
+  p->ws = nullptr;
+  p->cnt = nullptr;
+  const char* sk = getenv("RS_SPLITK");
+  const int nk = (a.K + BK - 1) / BK;
+  if (pool && a.N2 == 0 && nk >= 32 && sk && atoi(sk) > 1) {
+    int splits = std::min(std::min(4, atoi(sk)), nk / 16);
+    while (splits > 1 && (splits - 1) * ((nk + splits - 1) / splits) >= nk) --splits;
+    const size_t tiles = (size_t)a.batch * p->m_tiles * p->n_tiles;
+    const size_t ws = (size_t)splits * tiles * BM * p->block_n;
+    if (splits > 1 && pool->ws_used + ws <= pool->ws_cap && pool->cnt_used + tiles <= pool->cnt_cap) {
+      p->splits = splits;
+      p->ws = pool->ws + pool->ws_used;
+      p->cnt = pool->cnt + pool->cnt_used;
+      pool->ws_used += ws;
+      pool->cnt_used += tiles;
+    }
   }
   return true;
 }
@@ -704,8 +822,12 @@ void launch_fc_chain(const QDesc* qd, const TcChainPlan& p, cudaStream_t s) {
              qd, p);
 }
 
-void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s) {
-  const dim3 grid(p.n_tiles, p.m_tiles, a.batch);
+void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a0, cudaStream_t s) {
+  FcArgs a = a0;
+  a.splits = p.splits;
+  a.ws = p.ws;
+  a.cnt = p.cnt;
+  const dim3 grid(p.n_tiles, p.m_tiles, a.batch * std::max(1, p.splits));
   const int a_batched = a.sAz != 0 ? 1 : 0;
 #define RS_TC(BN, ST)                                                                   \
   launch_pdl(fc_tc_kernel<BN, ST>, grid, dim3(kTcThreads), tc_smem_bytes<BN, ST>(), s, qd, p.map_a, \

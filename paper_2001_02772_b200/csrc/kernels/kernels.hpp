@@ -64,6 +64,7 @@ struct FcArgs {
   int N2; int relu2; int c2_desc;
   int skip_c;          // 1: C itself is not needed (only C2)
   int single_n_tile;   // planning hint: prefer one N tile (BN = 128) when N <= 128
+  int splits; float* ws; int* cnt;  // split-K (set by launch_fc_tc from the plan)
 };
 constexpr int kFuseMaxN2 = 4;
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);
@@ -74,13 +75,22 @@ void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStr
 struct TcPlan {
   CUtensorMap map_a;   // A: [batch][M_cap][K] fp32, box 128 x 32
   CUtensorMap map_w;   // W: [batch][N][K] fp32, box BN x 32
-  int block_n;         // 64 / 128
+  int block_n;         // 64 / 128 / 256
   int cfg;             // tile/pipeline configuration (fc_tcgen05.cu)
   int m_tiles, n_tiles;
+  int splits;          // split-K factor (1 = none)
+  float* ws;           // split-K partial tiles [batch*splits][m_tiles][n_tiles][128*BN]
+  int* cnt;            // split-K arrival counters [batch][m_tiles][n_tiles] (self-resetting)
+};
+// Device scratch the plans of one graph carve split-K workspaces from.
+struct SplitKPool {
+  float* ws = nullptr; size_t ws_cap = 0, ws_used = 0;    // floats
+  int* cnt = nullptr; size_t cnt_cap = 0, cnt_used = 0;   // ints (zeroed)
 };
 bool tc_available();
 bool make_row_gather_map(CUtensorMap* map, const float* base, int64_t total_rows, int D);
-bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch);
+bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch,
+             SplitKPool* pool = nullptr);
 void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a, cudaStream_t s);
 
 // A whole FC stack in ONE kernel (fc_tcgen05.cu, fc_chain_kernel): per

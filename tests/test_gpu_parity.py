@@ -518,3 +518,21 @@ def test_queue_edge_cases():
         rs.serve([acc], b, np.zeros(1))
     assert np.array_equal(acc.forward(d, i), singles[2])
     acc.close()
+
+
+@pytest.mark.parametrize("splits", ["2", "4"])
+def test_split_k_parity(splits, monkeypatch):
+    """Split-K tcgen05 layers (RS_SPLITK=n, off by default — measured slower):
+    the last split to arrive sums the partials in split order, so results are
+    deterministic run to run; tf32 tolerance vs the oracle; RMC3's 2560-wide
+    bottom layer and MT-WND's 1640-wide stacked layer."""
+    monkeypatch.setenv("RS_SPLITK", splits)
+    for name in ("DLRM-RMC3", "MT-WND"):
+        spec = rs.builtin_model(name)
+        for S in (1, 200):
+            check_forward(spec, rows=2000, S=S, fc_mode=rs.FC_TF32, tol=TF32_TOL, max_q=300)
+    acc = rs.Accelerator(rs.builtin_model("DLRM-RMC3"), 2000, seed=2, max_query_size=300,
+                         fc_mode=rs.FC_TF32)
+    d, i = rs.fill_query(rs.builtin_model("DLRM-RMC3"), 2000, 4, 0, 257)
+    assert np.array_equal(acc.forward(d, i), acc.forward(d, i))
+    acc.close()
