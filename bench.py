@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local):
     sizes = np.minimum(sizes, args.max_query)
     acc = rs.Accelerator(spec, rows, seed=1, device=local, max_query_size=args.max_query,
                          fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc],
-                         queue_depth=args.depth)
+                         queue_depth=args.depth, l2_persist_mb=args.l2_persist_mb)
     if args.merge > 1:
         acc.set_option(rs.OPT_MERGE_QUERIES, args.merge)
     e = spec.embeddings
@@ -302,7 +302,7 @@ def run_ours(args, rank, world, local):
     bf16 = args.dense_bits == 16
     ity = (rs.INDEX_I32 if i32 else rs.INDEX_I64) | (rs.DENSE_BF16 if bf16 else 0)
     for q in range(P):
-        dn, ix = rs.fill_query(spec, rows, seed, q, int(sizes[q]))
+        dn, ix = rs.fill_query(spec, rows, seed, q, int(sizes[q]), zipf_alpha=args.zipf)
         if i32:
             ix = ix.astype(np.int32)
         if bf16:
@@ -464,6 +464,13 @@ def run_ours(args, rank, world, local):
                                          "as the reference's accelerator server)"),
                        "l2": "inputs >> L2 (tables %.1f GB, ~%.0f MB of indices per step)" % (
                            acc.info.table_bytes / 1e9, h2d_step / 1e6),
+                       "index_distribution": (
+                           f"LABELLED variant (SURVEY 8d): bounded power law alpha={args.zipf:g} "
+                           "over [0, rows), low ids hot" if args.zipf > 0 else "uniform"),
+                       "l2_persist": (
+                           f"hot block of {acc.info.hot_rows} rows/table "
+                           f"({acc.info.hot_rows * e.num_tables * e.embedding_dim * 4 / 2**20:.1f} MiB) "
+                           "in the L2 persisting set-aside" if acc.info.hot_rows else "off"),
                        "qps_method": "open-loop Poisson replay (n=50,000, sim.hpp:79) of the "
                                      "per-query CUDA-event service times measured in the timed "
                                      "region (FIFO delivery per GPU, in-pipeline residence "
@@ -532,6 +539,10 @@ def main():
                     help="16 = labelled bf16 dense-feature input variant (SURVEY 8f-2)")
     ap.add_argument("--index-bits", type=int, choices=[64, 32], default=64,
                     help="32 = labelled int32-index input variant (SURVEY 8f-2)")
+    ap.add_argument("--zipf", type=float, default=0.0,
+                    help=">0 = labelled skewed-index variant (SURVEY 8d Zipf(1.05))")
+    ap.add_argument("--l2-persist-mb", type=int, default=0,
+                    help="hot-row block kept in the L2 persisting set-aside (MiB)")
     ap.add_argument("--max-query", type=int, default=1000)
     ap.add_argument("--fc", choices=["fp32", "tf32", "auto"], default="auto")
     ap.add_argument("--no-cpu", action="store_true")

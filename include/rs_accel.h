@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 1
+#define RS_ABI_VERSION 2
 
 /* ---- error codes -------------------------------------------------------- */
 enum {
@@ -183,7 +183,10 @@ typedef struct rs_init_desc {
   int64_t max_query_size;   /* scratch capacity, items (reference max 1000) */
   int32_t fc_mode;          /* RS_FC_*                                       */
   int32_t rnn_cell;         /* RS_RNN_* (AttentionRNN only)                  */
-  int32_t l2_persist_mb;    /* >0: L2 persisting window over table rows     */
+  int32_t l2_persist_mb;    /* >0: hot-row block of up to this many MiB (rows
+                               [0, R) of every table) kept in the L2
+                               persisting set-aside; capped by the device's
+                               persisting/window limits. Sum pooling only.  */
   int32_t queue_depth;      /* rs_forward_many lanes in flight (0 = 4, <= 16) */
 } rs_init_desc;
 
@@ -228,6 +231,8 @@ typedef struct rs_accel_info {
   int64_t table_bytes;
   int64_t weight_bytes;
   int64_t l2_bytes;
+  int64_t hot_rows;                /* rows per table in the L2-persisting
+                                      hot block (0 = off; l2_persist_mb)  */
 } rs_accel_info;
 
 /* Create one model replica on one GPU: allocate and initialise tables and
@@ -308,6 +313,15 @@ int rs_service_time(rs_accel* a, int64_t query_size, double* seconds);
 int rs_fill_query(const rs_model_desc* m, int64_t rows_per_table,
                   uint64_t seed, uint64_t query_id, int64_t size,
                   float* dense, int64_t* indices);
+
+/* As rs_fill_query, but indices follow a bounded power law (Zipf-like,
+ * exponent alpha > 0): index k in [0, rows) drawn with probability ~
+ * (k+1)^-alpha by inverse transform of the continuous density on
+ * [1, rows+1), so low indices are the hot rows (frequency-sorted ids).
+ * SURVEY §8d's Zipf(1.05) variant for the L2-persistence run.             */
+int rs_fill_query_zipf(const rs_model_desc* m, int64_t rows_per_table,
+                       uint64_t seed, uint64_t query_id, int64_t size,
+                       double alpha, float* dense, int64_t* indices);
 
 /* Pinned host memory for rs_query buffers. rs_alloc_pinned_flags accepts
  * RS_PINNED_WRITE_COMBINED for input buffers the host only writes (faster

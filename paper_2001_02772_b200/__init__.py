@@ -156,7 +156,8 @@ class CAccelInfo(C.Structure):
                 ("fc_layers_tcgen05", C.c_int32),
                 ("predict_input_dim", C.c_int64), ("output_dim", C.c_int64),
                 ("pooled_dim", C.c_int64), ("table_bytes", C.c_int64),
-                ("weight_bytes", C.c_int64), ("l2_bytes", C.c_int64)]
+                ("weight_bytes", C.c_int64), ("l2_bytes", C.c_int64),
+                ("hot_rows", C.c_int64)]
 
 
 def _sig(name, restype, *argtypes):
@@ -197,6 +198,8 @@ _sig("rs_serve", C.c_int, P(C.c_void_p), C.c_int32, C.c_int64, P(CQuery), P(C.c_
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
+_sig("rs_fill_query_zipf", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
+     C.c_double, C.c_void_p, C.c_void_p)
 _sig("rs_alloc_pinned", C.c_int, C.c_size_t, P(C.c_void_p))
 _sig("rs_alloc_pinned_flags", C.c_int, C.c_size_t, C.c_uint32, P(C.c_void_p))
 _sig("rs_free_pinned", C.c_int, C.c_void_p)
@@ -208,7 +211,7 @@ EXPORTED_SYMBOLS = [
     "rs_dist_production", "rs_gen_trace", "rs_qps_under_sla", "rs_accel_create",
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
     "rs_pooled", "rs_service_time",
-    "rs_fill_query", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
+    "rs_fill_query", "rs_fill_query_zipf", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
     "rs_device_count", "rs_accel_set_option", "rs_serve"]
 
 
@@ -442,13 +445,20 @@ def device_count() -> int:
     return n.value
 
 
-def fill_query(model: ModelSpec, rows: int, seed: int, query_id: int, size: int):
-    """Synthetic inputs of DESIGN.md §3: (dense f32[S,dense_in], idx i64[S,T,L])."""
+def fill_query(model: ModelSpec, rows: int, seed: int, query_id: int, size: int,
+               zipf_alpha: float = 0.0):
+    """Synthetic inputs of DESIGN.md §3: (dense f32[S,dense_in], idx i64[S,T,L]).
+    zipf_alpha > 0: indices from the bounded power law of rs_fill_query_zipf
+    (low indices hot), same dense features."""
     e = model.embeddings
     dense = np.empty((size, model.dense_input_dim), dtype=np.float32)
     idx = np.empty((size, e.num_tables, e.lookups_per_table), dtype=np.int64)
-    _check(_lib.rs_fill_query(C.byref(model.to_c()), rows, seed, query_id, size,
-                              dense.ctypes.data, idx.ctypes.data))
+    if zipf_alpha > 0:
+        _check(_lib.rs_fill_query_zipf(C.byref(model.to_c()), rows, seed, query_id, size,
+                                       float(zipf_alpha), dense.ctypes.data, idx.ctypes.data))
+    else:
+        _check(_lib.rs_fill_query(C.byref(model.to_c()), rows, seed, query_id, size,
+                                  dense.ctypes.data, idx.ctypes.data))
     return dense, idx
 
 
@@ -467,12 +477,13 @@ class Accelerator:
 
     def __init__(self, model: ModelSpec, rows_per_table: int, seed: int = 1,
                  device: int = 0, max_query_size: int = 1000, fc_mode: int = FC_FP32,
-                 rnn_cell: int = RNN_GRU, queue_depth: int = 4):
+                 rnn_cell: int = RNN_GRU, queue_depth: int = 4, l2_persist_mb: int = 0):
         self.model = model
         self.rows = rows_per_table
         self.seed = seed
         self._desc = model.to_c()
-        init = CInitDesc(seed, rows_per_table, max_query_size, fc_mode, rnn_cell, 0, queue_depth)
+        init = CInitDesc(seed, rows_per_table, max_query_size, fc_mode, rnn_cell, l2_persist_mb,
+                         queue_depth)
         h = C.c_void_p()
         _check(_lib.rs_accel_create(C.byref(self._desc), C.byref(init), device, C.byref(h)))
         self._h = h

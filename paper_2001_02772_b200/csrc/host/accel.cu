@@ -123,6 +123,10 @@ struct rs_accel {
   int64_t max_dense_w = 0, max_pred_w = 0;
   // device state
   float* tables = nullptr;
+  // L2-persisting hot block: rows [0, hot_rows) of every table, [T][hot_rows][D]
+  float* hot = nullptr;
+  int64_t hot_rows = 0;
+  size_t hot_bytes = 0;
   std::vector<rs::FcLayer> dense_layers, pred_layers;
   float* att_w = nullptr;
   float *gru_wih = nullptr, *gru_whh = nullptr, *gru_bih = nullptr, *gru_bhh = nullptr,
@@ -206,6 +210,32 @@ std::vector<float> fill_param(uint64_t seed, uint64_t id, int64_t n, float bound
   return v;
 }
 
+// L2 persistence for skewed (Zipf) index streams: rows
+// [0, hot_rows) of every table are copied into one contiguous block that an
+// access-policy window keeps in the persisting L2 set-aside, so hot rows stay
+// resident while the cold gathers stream past them. A pure copy — the SLS
+// result does not depend on which of the two copies a row is read from.
+void setup_hot(rs_accel* a) {
+  cudaDeviceProp prop;
+  RS_CUDA(cudaGetDeviceProperties(&prop, a->device));
+  size_t want = (size_t)a->init.l2_persist_mb << 20;
+  want = std::min(want, (size_t)prop.persistingL2CacheMaxSize);
+  want = std::min(want, (size_t)prop.accessPolicyMaxWindowSize);
+  const size_t per_row = (size_t)a->T * a->D * sizeof(float);  // one row of every table
+  const int64_t hr = std::min<int64_t>(a->init.rows_per_table, (int64_t)(want / per_row));
+  if (hr < 1) return;
+  a->hot_rows = hr;
+  a->hot_bytes = (size_t)hr * per_row;
+  a->hot = static_cast<float*>(dmalloc(a, a->allocs, a->hot_bytes, false));
+  const size_t w = (size_t)hr * a->D * sizeof(float);
+  RS_CUDA(cudaMemcpy2DAsync(a->hot, w, a->tables, (size_t)a->init.rows_per_table * a->D * sizeof(float),
+                            w, (size_t)a->T, cudaMemcpyDeviceToDevice, a->own));
+  size_t cur = 0;
+  RS_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  if (cur < a->hot_bytes) RS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, a->hot_bytes));
+}
+
+
 void build_model(rs_accel* a) {
   const rs_model_desc& m = a->m;
   a->T = m.num_tables;
@@ -243,6 +273,7 @@ void build_model(rs_accel* a) {
     launch_init_tables(a->tables, a->T, a->init.rows_per_table, a->D, a->init.seed,
                        a->sm_count, a->own);
     RS_CUDA(cudaGetLastError());
+    if (m.pooling == RS_POOL_SUM && a->init.l2_persist_mb > 0) setup_hot(a);
   }
   // dense stack: ReLU after every layer (DLRM bottom MLP)
   if (m.has_dense_fc) {
@@ -328,7 +359,7 @@ void enqueue_pooling(rs_accel* a, Slot* s, float* out, int64_t ld, int64_t off, 
   switch (m.pooling) {
     case RS_POOL_SUM:
       launch_sls_sum(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out + off, ld,
-                     s->d_err, maxS, s->emb_sms, st);
+                     s->d_err, maxS, s->emb_sms, st, a->hot, a->hot_rows);
       break;
     case RS_POOL_CONCAT:
       launch_gather_concat(s->d_q, a->tables, rows, (int)a->T, (int)a->L, (int)a->D, out, ld,
@@ -540,7 +571,17 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   for (auto nd : nodes) {
     cudaGraphNodeType ty;
     RS_CUDA(cudaGraphNodeGetType(nd, &ty));
-    if (ty == cudaGraphNodeTypeKernel) ++k;
+    if (ty != cudaGraphNodeTypeKernel) continue;
+    ++k;
+    if (a->hot) {  // the hot block's lines persist in L2 (setup_hot)
+      cudaKernelNodeAttrValue v{};
+      v.accessPolicyWindow.base_ptr = a->hot;
+      v.accessPolicyWindow.num_bytes = a->hot_bytes;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      RS_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v));
+    }
   }
   cudaGraphExec_t exec = nullptr;
   RS_CUDA(cudaGraphInstantiate(&exec, g,
@@ -1288,6 +1329,7 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
       if (a->lane[d]) cudaStreamDestroy(a->lane[d]);
       if (a->lane_join[d]) cudaEventDestroy(a->lane_join[d]);
     }
+    if (a->hot) cudaCtxResetPersistingL2Cache();
     for (void* p : a->allocs) cudaFree(p);
     if (a->own) cudaStreamDestroy(a->own);
     if (a->g_dense) green_api().destroy(a->g_dense);
@@ -1313,6 +1355,7 @@ extern "C" int rs_accel_info_get(const rs_accel* ca, rs_accel_info* out) {
     i.table_bytes = a->table_bytes;
     i.weight_bytes = a->weight_bytes;
     i.l2_bytes = a->l2_bytes;
+    i.hot_rows = a->hot_rows;
     *out = i;
   });
 }

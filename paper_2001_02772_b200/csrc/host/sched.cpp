@@ -257,3 +257,28 @@ extern "C" int rs_fill_query(const rs_model_desc* m, int64_t rows_per_table, uin
     }
   });
 }
+
+extern "C" int rs_fill_query_zipf(const rs_model_desc* m, int64_t rows_per_table, uint64_t seed,
+                                  uint64_t query_id, int64_t size, double alpha, float* dense,
+                                  int64_t* indices) {
+  return guarded([&] {
+    if (!(alpha > 0.0)) raise(RS_E_INVALID, "zipf alpha must be > 0");
+    int rc = rs_fill_query(m, rows_per_table, seed, query_id, size, dense, nullptr);
+    if (rc != RS_OK) raise(rc, rs_last_error());
+    const uint64_t ni = static_cast<uint64_t>(size * m->num_tables * m->lookups_per_table);
+    if (!indices || !ni) return;
+    // inverse CDF of x^-alpha on [1, N+1): x = (1 + u((N+1)^(1-a) - 1))^(1/(1-a))
+    // (a = 1: x = (N+1)^u); index = floor(x) - 1
+    const double n1 = static_cast<double>(rows_per_table) + 1.0;
+    const bool one = std::fabs(alpha - 1.0) < 1e-12;
+    const double e = 1.0 - alpha;
+    const double span = one ? std::log(n1) : std::pow(n1, e) - 1.0;
+    const uint64_t k = stream_key(seed, id_query_idx(query_id));
+    for (uint64_t i = 0; i < ni; ++i) {
+      const double u = static_cast<double>(splitmix64(k + i) >> 11) * 0x1.0p-53;
+      const double x = one ? std::exp(u * span) : std::pow(1.0 + u * span, 1.0 / e);
+      int64_t r = static_cast<int64_t>(x) - 1;
+      indices[i] = r < 0 ? 0 : (r >= rows_per_table ? rows_per_table - 1 : r);
+    }
+  });
+}

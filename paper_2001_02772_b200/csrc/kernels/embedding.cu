@@ -255,7 +255,8 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
 template <int LPR, int VPL, int U, int IPL>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
-                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err) {
+                int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
+                const float* __restrict__ hot, int64_t hot_rows) {
   constexpr int R = 32 / LPR;
   constexpr int D = LPR * 4 * VPL;
   constexpr int B = R * U;  // rows per batch
@@ -285,6 +286,10 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
     const int t = (int)(bag % T);
     const float4* __restrict__ tab =
         reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
+    // rows [0, hot_rows) of every table also live in the L2-persisting hot
+    // block [T][hot_rows][D] (an exact copy; hot_rows = 0 when disabled)
+    const float4* __restrict__ htab =
+        reinterpret_cast<const float4*>(hot + (int64_t)t * hot_rows * D);
     auto load_batch = [&](int j, float4 (&v)[U][VPL], bool (&ok)[U]) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -294,7 +299,7 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
           const int64_t r = sidx[warp][l];
           if ((uint64_t)r < (uint64_t)rows) {
             ok[u] = true;
-            const float4* p = tab + r * (D / 4) + c;
+            const float4* p = (r < hot_rows ? htab : tab) + r * (D / 4) + c;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream(p + k * LPR);
           } else {
@@ -965,7 +970,7 @@ int env_int(const char* name, int dflt) {
 template <int LPR, int VPL, int U, int IPL>
 void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                      float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
-                     cudaStream_t s) {
+                     cudaStream_t s, const float* hot, int64_t hot_rows) {
   const int wpc = std::min(kWarps, std::max(1, env_int("RS_SLS_WPC", kWarps)));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sls_pipe_kernel<LPR, VPL, U, IPL>,
@@ -974,7 +979,7 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
   const int grid = grid_for(max_items * T, wpc, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
   max_carveout(reinterpret_cast<const void*>(sls_pipe_kernel<LPR, VPL, U, IPL>));
   sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, wpc * 32, 0, s>>>(
-      qd, tables, rows, T, L, out, ld_out, err);
+      qd, tables, rows, T, L, out, ld_out, err, hot, hot_rows);
 }
 
 template <int LPR, int VPL, int U, int IPL>
@@ -1014,11 +1019,13 @@ bool try_sls_stream(const QDesc* qd, const float* tables, int64_t rows, int T, i
 
 template <int LPR, int VPL>
 bool try_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L, float* out,
-                  int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s) {
+                  int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s,
+                  const float* hot, int64_t hot_rows) {
   if (L > 96) return false;
   const int ub = sls_ub();
 #define RS_PIPE(U, IPL) \
-  launch_sls_pipe<LPR, VPL, U, IPL>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, s)
+  launch_sls_pipe<LPR, VPL, U, IPL>(qd, tables, rows, T, L, out, ld_out, err, max_items, sm_count, \
+                                    s, hot, hot_rows)
   if (L <= 32) {
     if (ub >= 8) RS_PIPE((VPL == 2 ? 4 : 8), 1);
     else if (ub <= 2) RS_PIPE((VPL == 2 ? 1 : 2), 1);
@@ -1114,7 +1121,7 @@ bool launch_sls_tma(const QDesc* qd, const float* tables, int64_t rows, int T, i
 
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
                     float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
-                    cudaStream_t s) {
+                    cudaStream_t s, const float* hot, int64_t hot_rows) {
 #define RS_SLS(LPR, VPL)                                                                    \
   do {                                                                                      \
     if (sls_variant() == 1 && launch_sls_tma<LPR, VPL, 2>(qd, tables, rows, T, L, out,      \
@@ -1122,7 +1129,8 @@ void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, i
                                                           s))                               \
       break;                                                                                \
     if (sls_variant() == 2 && try_sls_pipe<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,   \
-                                                     err, max_items, sm_count, s))          \
+                                                     err, max_items, sm_count, s, hot,      \
+                                                     hot_rows))                             \
       break;                                                                                \
     if (sls_variant() == 3 && try_sls_stage<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,  \
                                                       err, max_items, sm_count, s))         \

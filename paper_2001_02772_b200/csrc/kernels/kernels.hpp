@@ -10,9 +10,12 @@ struct QDesc;
 
 // ---- embedding.cu ----
 bool sls_vector_path(int64_t D);
+// hot/hot_rows: optional exact copy of rows [0, hot_rows) of every table,
+// [T][hot_rows][D], kept in the L2 persisting set-aside (rs_init_desc
+// l2_persist_mb); the default SLS kernel reads those rows from it.
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
                     float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
-                    cudaStream_t s);
+                    cudaStream_t s, const float* hot = nullptr, int64_t hot_rows = 0);
 void launch_gather_concat(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                           int D, float* out, int64_t ld_out, int64_t col_off, int* err,
                           int64_t max_items, int sm_count, cudaStream_t s);

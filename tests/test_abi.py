@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol(rs):
 
 
 def test_abi_version(rs):
-    assert rs._lib.rs_abi_version() == 1
+    assert rs._lib.rs_abi_version() == 2
 
 
 def test_errors_cross_the_abi_as_codes(rs):
@@ -67,3 +67,25 @@ def test_tcgen05_and_tma_in_sass(rs):
     assert "UTCHMMA" in sass        # tcgen05.mma
     assert "UTMALDG" in sass        # TMA tensor loads
     assert "LDTM" in sass           # tcgen05.ld TMEM -> registers
+
+
+def test_zipf_fill_query(rs):
+    """rs_fill_query_zipf: deterministic, in range, the dense features of
+    rs_fill_query, and the bounded power law's CDF at a few cut points."""
+    import numpy as np
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows, a = 1_000_000, 1.05
+    d0, i0 = rs.fill_query(spec, rows, 3, 7, 200)
+    d1, i1 = rs.fill_query(spec, rows, 3, 7, 200, zipf_alpha=a)
+    d2, i2 = rs.fill_query(spec, rows, 3, 7, 200, zipf_alpha=a)
+    assert np.array_equal(d0, d1) and np.array_equal(i1, i2)
+    assert i1.min() >= 0 and i1.max() < rows
+    n1 = rows + 1.0
+    for K in (10, 1000, 100_000):
+        want = ((K + 1.0) ** (1 - a) - 1) / (n1 ** (1 - a) - 1)
+        assert abs(float(np.mean(i1 < K)) - want) < 0.01
+    _, iu = rs.fill_query(spec, rows, 3, 7, 200, zipf_alpha=1.0)
+    assert abs(float(np.mean(iu < 1000)) - np.log(1001) / np.log(n1)) < 0.01
+    d, i = np.empty((2, spec.dense_input_dim), np.float32), np.empty(2 * 8 * 80, np.int64)
+    assert rs._lib.rs_fill_query_zipf(C.byref(spec.to_c()), rows, 3, 7, 2, 0.0,
+                                      d.ctypes.data, i.ctypes.data) == rs.InvalidArgument.code

@@ -536,3 +536,27 @@ def test_split_k_parity(splits, monkeypatch):
     d, i = rs.fill_query(rs.builtin_model("DLRM-RMC3"), 2000, 4, 0, 257)
     assert np.array_equal(acc.forward(d, i), acc.forward(d, i))
     acc.close()
+
+
+@pytest.mark.parametrize("name", ["DLRM-RMC1", "DLRM-RMC2"])
+def test_l2_hot_block_is_bit_identical(name):
+    """l2_persist_mb (SURVEY §8d Zipf/L2-persistence variant): rows [0, R) of
+    every table are served from the persisting hot block. Pooled sums stay
+    bit-identical to the oracle's canonical order and the logits to the
+    accelerator without the block, for Zipf and uniform indices, including
+    rows on both sides of the hot boundary."""
+    spec = rs.builtin_model(name)
+    rows = 50_000
+    plain = rs.Accelerator(spec, rows, seed=4, max_query_size=300, fc_mode=rs.FC_AUTO)
+    hot = rs.Accelerator(spec, rows, seed=4, max_query_size=300, fc_mode=rs.FC_AUTO,
+                         l2_persist_mb=2)
+    R = hot.info.hot_rows
+    assert 0 < R < rows
+    orc = Oracle(spec, rows, seed=4)
+    for S, alpha in ((1, 1.05), (130, 1.05), (300, 0.0)):
+        dense, idx = rs.fill_query(spec, rows, 9, S, S, zipf_alpha=alpha)
+        idx[0, 0, :2] = [R - 1, R]  # both sides of the boundary
+        assert np.array_equal(hot.pooled(idx), orc.sls_canonical(idx))
+        assert np.array_equal(hot.forward(dense, idx), plain.forward(dense, idx))
+    hot.close()
+    plain.close()
