@@ -252,7 +252,7 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
 // bag's rows stream, and row batch j+1 is in flight while batch j accumulates.
 // Same per-lane accumulation order as sls_sum_kernel (bit-identical results).
 // Bags of up to 32*IPL lookups; longer bags use sls_sum_kernel.
-template <int LPR, int VPL, int U, int IPL>
+template <int LPR, int VPL, int U, int IPL, bool HOT>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                 int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
@@ -286,10 +286,11 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
     const int t = (int)(bag % T);
     const float4* __restrict__ tab =
         reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
-    // rows [0, hot_rows) of every table also live in the L2-persisting hot
-    // block [T][hot_rows][D] (an exact copy; hot_rows = 0 when disabled)
+    // HOT: rows [0, hot_rows) of every table also live in the L2-persisting
+    // hot block [T][hot_rows][D] (an exact copy); a separate instantiation so
+    // the default kernel carries no extra work
     const float4* __restrict__ htab =
-        reinterpret_cast<const float4*>(hot + (int64_t)t * hot_rows * D);
+        HOT ? reinterpret_cast<const float4*>(hot + (int64_t)t * hot_rows * D) : nullptr;
     auto load_batch = [&](int j, float4 (&v)[U][VPL], bool (&ok)[U]) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -299,7 +300,7 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
           const int64_t r = sidx[warp][l];
           if ((uint64_t)r < (uint64_t)rows) {
             ok[u] = true;
-            const float4* p = (r < hot_rows ? htab : tab) + r * (D / 4) + c;
+            const float4* p = (HOT && r < hot_rows ? htab : tab) + r * (D / 4) + c;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream(p + k * LPR);
           } else {
@@ -972,14 +973,14 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
                      float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
                      cudaStream_t s, const float* hot, int64_t hot_rows) {
   const int wpc = std::min(kWarps, std::max(1, env_int("RS_SLS_WPC", kWarps)));
+  auto kern = hot_rows > 0 ? sls_pipe_kernel<LPR, VPL, U, IPL, true>
+                           : sls_pipe_kernel<LPR, VPL, U, IPL, false>;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sls_pipe_kernel<LPR, VPL, U, IPL>,
-                                                wpc * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, 0);
   per_sm = std::max(per_sm, 1);
   const int grid = grid_for(max_items * T, wpc, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
-  max_carveout(reinterpret_cast<const void*>(sls_pipe_kernel<LPR, VPL, U, IPL>));
-  sls_pipe_kernel<LPR, VPL, U, IPL><<<grid, wpc * 32, 0, s>>>(
-      qd, tables, rows, T, L, out, ld_out, err, hot, hot_rows);
+  max_carveout(reinterpret_cast<const void*>(kern));
+  kern<<<grid, wpc * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err, hot, hot_rows);
 }
 
 template <int LPR, int VPL, int U, int IPL>
