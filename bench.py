@@ -425,10 +425,9 @@ def run_ours(args, rank, world, local):
     d2h_step = float(np.mean([sum(int(sizes[q]) * acc.output_dim * 4 + 4 for q in window(k))
                               for k in range(K)]))
     # kernel nodes of the graph each timed query launched (pick_graph in
-    # csrc/host/accel.cu: FC_AUTO takes the tcgen05 graph at >= 128 items)
-    kl, ks = acc.info.kernels_per_forward, acc.info.kernels_per_forward_small
-    launches = int(sum((kl if (ks == 0 or (int(sizes[q]) >= 128 and kl != ks)) else ks)
-                       for k in range(K) for q in window(k)))
+    # csrc/host/accel.cu: one graph per FC path; FC_AUTO/TF32 = the tcgen05 graph)
+    kl = acc.info.kernels_per_forward
+    launches = int(sum(kl for k in range(K) for q in window(k)))
     # DRAM traffic per launch from the committed ncu --set full capture
     # (profiles/sls_traffic.json: dram read+write bytes / items of that launch),
     # scaled to this run's mean items per roofline launch like `achieved`

@@ -170,7 +170,8 @@ typedef struct rs_accel rs_accel;
 enum {
   RS_FC_FP32 = 0,  /* FFMA fp32 path (tight parity)                        */
   RS_FC_TF32 = 1,  /* tcgen05 kind::tf32 (fp32 operands, fp32 accumulate)   */
-  RS_FC_AUTO = 2   /* tcgen05 where the layer shape fills a tile, else FFMA */
+  RS_FC_AUTO = 2   /* the measured-fastest path: today the tcgen05 graph at
+                      every query size (= RS_FC_TF32)                   */
 };
 enum { RS_RNN_GRU = 0, RS_RNN_AUGRU = 1 };
 
@@ -222,8 +223,8 @@ typedef struct rs_timing {
 typedef struct rs_accel_info {
   int32_t device;
   int32_t sm_count;
-  int32_t kernels_per_forward;     /* kernel nodes, large-batch graph      */
-  int32_t kernels_per_forward_small; /* kernel nodes, small-batch graph     */
+  int32_t kernels_per_forward;     /* kernel nodes of the graph a query runs */
+  int32_t kernels_per_forward_small; /* kernel nodes, FFMA graph (0 if none) */
   int32_t fc_layers_tcgen05;       /* FC layers routed to tcgen05          */
   int64_t predict_input_dim;
   int64_t output_dim;              /* per item: stacks * last predict dim  */
@@ -251,8 +252,7 @@ int rs_accel_info_get(const rs_accel* a, rs_accel_info* out);
  * events, waits for completion and reports index errors; otherwise it is
  * asynchronous on `stream`, errors stay sticky until rs_sync, and the
  * caller owns synchronisation. Inputs and outputs must stay valid until the
- * stream reaches the end of this call. With RS_FC_AUTO, queries of at least
- * 128 items run the tcgen05 FC graph, smaller ones the FFMA graph.          */
+ * stream reaches the end of this call.                                     */
 int rs_forward(rs_accel* a, const rs_query* q, float* out, void* stream,
                rs_timing* timing);
 

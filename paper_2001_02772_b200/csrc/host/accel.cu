@@ -475,7 +475,6 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
 // forward with FFMA FC layers (small batches / fp32 parity) and the whole
 // forward with tcgen05 FC layers wherever the layer shape fills a tile.
 enum GraphKind { kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kNumGraphs = 3 };
-constexpr int64_t kAutoTcMinItems = 128;  // one full UMMA M tile
 
 cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_layers) {
   // A partitioned slot captures the gathers on the gather partition's stream
@@ -497,12 +496,12 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
     if (part && a->T > 0) {
       RS_CUDA(cudaEventRecord(s->fork, st));
       RS_CUDA(cudaStreamWaitEvent(s->gcap_e, s->fork, 0));
-      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode == RS_FC_TF32,
+      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode != RS_FC_FP32,
                       s->gcap_e);
       RS_CUDA(cudaEventRecord(s->join, s->gcap_e));
       RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
     } else {
-      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode == RS_FC_TF32, st);
+      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode != RS_FC_FP32, st);
     }
   } else {
     // diagnostic only (tools/pipe_micro.py): RS_DIAG_SKIP bit 1 drops the
@@ -725,7 +724,10 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   RS_CUDA(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
   RS_CUDA(cudaDeviceSynchronize());
   s->graph[kGraphPool] = capture(a, s.get(), kGraphPool, nullptr, nullptr);
-  if (a->init.fc_mode != RS_FC_TF32 || !tc_available())
+  // FC_AUTO routes every query size to the tcgen05 graph (measured faster
+  // than the FFMA graph at every size, alone and pipelined: DESIGN.md §2);
+  // the FFMA graph serves FC_FP32 and devices without tcgen05
+  if (a->init.fc_mode == RS_FC_FP32 || !tc_available())
     s->graph[kGraphSmall] = capture(a, s.get(), kGraphSmall, &s->kernels[kGraphSmall], nullptr);
   if (a->init.fc_mode != RS_FC_FP32 && tc_available())
     s->graph[kGraphLarge] =
@@ -944,9 +946,8 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
 cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full) {
   if (!full) return s->graph[kGraphPool];
   cudaGraphExec_t small = s->graph[kGraphSmall], large = s->graph[kGraphLarge];
-  if (!large) return small;
-  if (!small) return large;
-  return S >= kAutoTcMinItems ? large : small;
+  (void)S;
+  return large ? large : small;
 }
 
 void launch_stage(rs_accel* a, Slot* s, const rs_query* q, float* out, bool full,
