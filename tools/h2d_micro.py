@@ -80,6 +80,43 @@ def main():
     e1.record(streams[0])
     torch.cuda.synchronize()
     out["pinned_7MB_256_buffers"] = round(reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
+    # duplex: H2D on one stream while D2H runs on another (is the link's
+    # other direction free for outputs?)
+    hdst = [rs.PinnedBuffer(nbytes) for _ in range(2)]
+    hd = [torch.frombuffer((ctypes.c_char * nbytes).from_address(b.ptr), dtype=torch.uint8)
+          for b in hdst]
+    d2h_stream = torch.cuda.Stream()
+    for mode in ("d2h_only", "duplex"):
+        torch.cuda.synchronize()
+        e0.record(streams[0])
+        d2h_stream.wait_event(e0)
+        for i in range(reps):
+            if mode == "duplex":
+                with torch.cuda.stream(streams[0]):
+                    dsts[0].copy_(srcs[i % 4], non_blocking=True)
+            with torch.cuda.stream(d2h_stream):
+                hd[i % 2].copy_(dsts[1], non_blocking=True)
+        streams[0].wait_stream(d2h_stream)
+        e1.record(streams[0])
+        torch.cuda.synchronize()
+        gbs = reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+        out[f"pinned_7MB_{mode}_gbs_per_direction"] = round(gbs, 1)
+    # duplex with two H2D streams alternating (the library's host queue)
+    torch.cuda.synchronize()
+    e0.record(streams[0])
+    streams[1].wait_event(e0)
+    d2h_stream.wait_event(e0)
+    for i in range(reps):
+        with torch.cuda.stream(streams[i % 2]):
+            dsts[i % 2].copy_(srcs[i % 4], non_blocking=True)
+        with torch.cuda.stream(d2h_stream):
+            hd[i % 2].copy_(dsts[(i + 1) % 2], non_blocking=True)
+    streams[0].wait_stream(streams[1])
+    streams[0].wait_stream(d2h_stream)
+    e1.record(streams[0])
+    torch.cuda.synchronize()
+    out["pinned_7MB_duplex_two_h2d_streams_gbs_per_direction"] = round(
+        reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
     print(json.dumps(out))
 
 
