@@ -682,9 +682,21 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   // (tools/pipe_micro.py: 44.0 -> 41.4 us/query on cfg3 RMC2 vs <128,3>).
   // Long-K or wide layers (MT-WND's 1640 -> 1024 x 4 stacks) are bound by
   // feeding the tensor cores from L2, not by latency: there two shallower
-  // CTAs per SM win (MT-WND 27.0 -> 21.5 us/query), so they keep <128,3>/<64,4>.
+  // CTAs per SM win (MT-WND 27.0 -> 21.5 us/query), so they keep <128,3>/<64,4>
+  // (RS_TC_WIDE_K / RS_TC_WIDE_K1: the K threshold for batched / single stacks).
   const int64_t ctas = (int64_t)((a.N + 127) / 128) * ((m_cap + BM - 1) / BM) * a.batch;
-  const bool wide = a.K >= 1024 || ctas > 148;
+  static const int wide_k = [] {
+    const char* e = getenv("RS_TC_WIDE_K");
+    return e ? atoi(e) : 1024;
+  }();
+  // single-stack layers stay deep up to K < 2048: WND's 1640 -> 1024 and
+  // 1024 -> 512 run 25% faster pipelined on <128,6> (73.6K -> 91.9K QPS),
+  // RMC3's 2560 -> 512 2.4% slower (45.9K -> 44.7K), so it keeps <128,3>
+  static const int wide_k1 = [] {
+    const char* e = getenv("RS_TC_WIDE_K1");
+    return e ? atoi(e) : 2048;
+  }();
+  const bool wide = a.K >= (a.batch > 1 ? wide_k : wide_k1) || ctas > 148;
   p->cfg = a.N >= 128 ? (wide ? 0 : 2) : (wide ? 1 : 3);
   // cfg 4 <256,4>: one CTA covers 256 output columns (half the CTAs of a
   // 512-wide layer, same k-block round trips per CTA); RS_TC_WIDE=1 selects it

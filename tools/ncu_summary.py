@@ -12,8 +12,11 @@ def launch_shares(path):
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name")
     agg = collections.defaultdict(list)
     for r in data:
+        if r[mi] != "gpu__time_duration.sum":  # other --metrics columns
+            continue
         v = float(r[vi].replace(",", ""))
         scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
                  "ms": 1e3}.get(r[ui], 1.0)
