@@ -228,41 +228,51 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
       for (int c = 0; c < D; ++c) ua[c] = fmaf(xi, __ldg(Wa + i * D + c), ua[c]);
     }
   }
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
-                         ((uint32_t)(kSeq >> 4) << 24);
+  // instruction descriptors by N: the x-part covers gate blocks [r|z|n_x]
+  // (3H columns), the h-part [r|z] (2H) and [n_h] (H, at column 3H) — the
+  // zero blocks of the packed weights (W_x for n_h, W_h for n_x) are skipped
+  auto make_idesc = [](int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(kSeq >> 4) << 24);
+  };
+  const uint32_t id_x = make_idesc(3 * H), id_rz = make_idesc(2 * H), id_nh = make_idesc(H);
 
   // Two TMEM accumulators: while step l's cell math runs, the tensor core
   // already computes step l+1's input projection x_{l+1} W_x (it does not
   // depend on h); after the epilogue only the h-part is on the critical path.
+  // n0: first gate row / accumulator column of the block, id: its N
   auto issue = [&](uint32_t acc_tmem, int a_begin, int a_end, const uint8_t* ax_buf,
-                   bool first_init) {
+                   bool first_init, int n0, uint32_t id) {
 #pragma unroll
     for (int a = a_begin; a < a_end; ++a) {
       const uint32_t abase = a < DA ? s_u32(ax_buf + a * kSeq * 128) : s_u32(sm.ah[a - DA]);
-      const uint32_t bbase = s_u32(sm.b[a]);
+      const uint32_t bbase = s_u32(sm.b[a]) + (uint32_t)n0 * 128;  // 8-row groups: 1024 B
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint32_t acc = (first_init && a == a_begin && kk == 0) ? 0u : 1u;
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc_tmem),
-            "l"(sw128(abase + kk * 32)), "l"(sw128(bbase + kk * 32)), "r"(idesc), "r"(acc)
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                acc_tmem + (uint32_t)n0),
+            "l"(sw128(abase + kk * 32)), "l"(sw128(bbase + kk * 32)), "r"(id), "r"(acc)
             : "memory");
       }
     }
   };
-  if (tid == 0) issue(tmem, 0, DA, sm.ax[0][0], true);  // x_0 W_x
+  if (tid == 0) issue(tmem, 0, DA, sm.ax[0][0], true, 0, id_x);  // x_0 W_x
 
   for (int l = 0; l < L; ++l) {
     const int xb = l & 1;
     const uint32_t tcur = tmem + (uint32_t)(xb * N);
     if (tid == 0) {
-      issue(tcur, DA, KA, nullptr, false);  // += h_l W_h
+      issue(tcur, DA, KA, nullptr, false, 0, id_rz);     // [r|z] += h_l W_h
+      issue(tcur, DA, KA, nullptr, true, 3 * H, id_nh);  // [n_h]  = h_l W_hn
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
               s_u32(&sm.mma_done))
           : "memory");
-      if (l + 1 < L) issue(tmem + (uint32_t)((xb ^ 1) * N), 0, DA, sm.ax[xb ^ 1][0], true);
+      if (l + 1 < L)
+        issue(tmem + (uint32_t)((xb ^ 1) * N), 0, DA, sm.ax[xb ^ 1][0], true, 0, id_x);
     }
     float att = 1.f;
     if (g.augru) {  // a_l = sigmoid(<ua, x_l>) from the x row in shared memory
