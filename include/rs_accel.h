@@ -215,9 +215,12 @@ typedef struct rs_query {
 /* Per-call timing (CUDA events on the call's stream), milliseconds.        */
 typedef struct rs_timing {
   double h2d_ms;
-  double compute_ms;
+  double compute_ms;   /* the forward (or embedding-stage) graph             */
   double d2h_ms;
   double total_ms;
+  double embed_ms;     /* rs_pooled: the embedding kernel alone, between
+                          event-record nodes captured around it in the
+                          graph; 0 for rs_forward                          */
 } rs_timing;
 
 typedef struct rs_accel_info {

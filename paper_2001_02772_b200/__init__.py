@@ -147,7 +147,7 @@ class CQuery(C.Structure):
 
 class CTiming(C.Structure):
     _fields_ = [("h2d_ms", C.c_double), ("compute_ms", C.c_double), ("d2h_ms", C.c_double),
-                ("total_ms", C.c_double)]
+                ("total_ms", C.c_double), ("embed_ms", C.c_double)]
 
 
 class CAccelInfo(C.Structure):
@@ -469,6 +469,7 @@ class Timing:
     compute_ms: float
     d2h_ms: float
     total_ms: float
+    embed_ms: float = 0.0
 
 
 class Accelerator:
@@ -516,7 +517,7 @@ class Accelerator:
         t = CTiming()
         _check(_lib.rs_forward(self._h, C.byref(q), out_ptr, stream or None,
                                C.byref(t) if timed else None))
-        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms) if timed else None
+        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms, t.embed_ms) if timed else None
 
     def pooled_ptr(self, size: int, idx_ptr: int, out_ptr: int, location: int,
                    stream: int = 0, timed: bool = False, dense_ptr: int = 0,
@@ -525,7 +526,7 @@ class Accelerator:
         t = CTiming()
         _check(_lib.rs_pooled(self._h, C.byref(q), out_ptr, stream or None,
                               C.byref(t) if timed else None))
-        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms) if timed else None
+        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms, t.embed_ms) if timed else None
 
     @staticmethod
     def batch(sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int, index_type: int = 0):

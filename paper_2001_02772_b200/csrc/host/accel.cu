@@ -91,10 +91,12 @@ struct Slot {
   float* X = nullptr;
   float* pact[2] = {nullptr, nullptr};
   float* out = nullptr;
-  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};  // GraphKind
   int kernels[3] = {0, 0, 0};
   int tc_layers = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // event-record nodes around the embedding kernel in the pool graph
+  cudaEvent_t kev[2] = {nullptr, nullptr};
   cudaEvent_t ready = nullptr, free = nullptr;  // pipelined queue hand-off
   cudaStream_t cap2 = nullptr;                  // capture: parallel graph branch
   // SM-partitioned slots (rs_forward_many lanes when the device is split):
@@ -474,7 +476,12 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
 // Graph kinds per slot: the embedding stage alone (rs_pooled), the whole
 // forward with FFMA FC layers (small batches / fp32 parity) and the whole
 // forward with tcgen05 FC layers wherever the layer shape fills a tile.
-enum GraphKind { kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kNumGraphs = 3 };
+// kGraphPoolTimed: the pool graph with event-record nodes around the
+// embedding kernel (rs_pooled with timing; the untimed graph stays lean)
+enum GraphKind {
+  kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kGraphPoolTimed = 3, kNumGraphs = 4
+};
+static_assert(kNumGraphs == sizeof(Slot::graph) / sizeof(Slot::graph[0]), "Slot::graph size");
 
 cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_layers) {
   // A partitioned slot captures the gathers on the gather partition's stream
@@ -492,16 +499,23 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   const int64_t maxS = a->init.max_query_size;
   const bool tc = kind == kGraphLarge;
   int ntc = 0;
-  if (kind == kGraphPool) {
+  if (kind == kGraphPool || kind == kGraphPoolTimed) {
+    // timestamps of the embedding kernel alone (rs_timing.embed_ms): external
+    // event-record nodes on the kernel's own stream, right around it
+    const bool stamp = kind == kGraphPoolTimed;
+    auto pool = [&](cudaStream_t ps) {
+      if (stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[0], ps, cudaEventRecordExternal));
+      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode != RS_FC_FP32, ps);
+      if (stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[1], ps, cudaEventRecordExternal));
+    };
     if (part && a->T > 0) {
       RS_CUDA(cudaEventRecord(s->fork, st));
       RS_CUDA(cudaStreamWaitEvent(s->gcap_e, s->fork, 0));
-      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode != RS_FC_FP32,
-                      s->gcap_e);
+      pool(s->gcap_e);
       RS_CUDA(cudaEventRecord(s->join, s->gcap_e));
       RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
     } else {
-      enqueue_pooling(a, s, s->pooled, a->pooled_dim, 0, a->init.fc_mode != RS_FC_FP32, st);
+      pool(st);
     }
   } else {
     // diagnostic only (tools/pipe_micro.py): RS_DIAG_SKIP bit 1 drops the
@@ -717,6 +731,7 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   s->X = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_x * 4)));
   s->out = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->out_w * 4)));
   for (auto& e : s->ev) RS_CUDA(cudaEventCreate(&e));
+  for (auto& e : s->kev) RS_CUDA(cudaEventCreate(&e));
   RS_CUDA(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&s->free, cudaEventDisableTiming));
   RS_CUDA(cudaStreamCreateWithFlags(&s->cap2, cudaStreamNonBlocking));
@@ -724,6 +739,7 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   RS_CUDA(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
   RS_CUDA(cudaDeviceSynchronize());
   s->graph[kGraphPool] = capture(a, s.get(), kGraphPool, nullptr, nullptr);
+  s->graph[kGraphPoolTimed] = capture(a, s.get(), kGraphPoolTimed, nullptr, nullptr);
   // FC_AUTO routes every query size to the tcgen05 graph (measured faster
   // than the FFMA graph at every size, alone and pipelined: DESIGN.md §2);
   // the FFMA graph serves FC_FP32 and devices without tcgen05
@@ -762,6 +778,7 @@ Slot* get_pipe_slot(rs_accel* a, int i) {
 void free_slot(Slot* s) {
   for (auto g : s->graph) if (g) cudaGraphExecDestroy(g);
   for (auto e : s->ev) if (e) cudaEventDestroy(e);
+  for (auto e : s->kev) if (e) cudaEventDestroy(e);
   if (s->ready) cudaEventDestroy(s->ready);
   if (s->free) cudaEventDestroy(s->free);
   for (void* p : s->allocs) cudaFree(p);
@@ -943,8 +960,8 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
   write_desc(a, s, v, st);
 }
 
-cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full) {
-  if (!full) return s->graph[kGraphPool];
+cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full, bool timed = false) {
+  if (!full) return s->graph[timed ? kGraphPoolTimed : kGraphPool];
   cudaGraphExec_t small = s->graph[kGraphSmall], large = s->graph[kGraphLarge];
   (void)S;
   return large ? large : small;
@@ -987,7 +1004,7 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
     if (timing) RS_CUDA(cudaEventRecord(s->ev[0], st));
     stage_inputs(a, s, q, full, st, out);
     if (timing) RS_CUDA(cudaEventRecord(s->ev[1], st));
-    RS_CUDA(cudaGraphLaunch(pick_graph(a, s, q->size, full), st));
+    RS_CUDA(cudaGraphLaunch(pick_graph(a, s, q->size, full, timing != nullptr), st));
     if (timing) RS_CUDA(cudaEventRecord(s->ev[2], st));
     const int64_t w = full ? a->out_w : a->pooled_dim;
     if (!full || q->location == RS_MEM_HOST)
@@ -1002,6 +1019,7 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
       timing->compute_ms = elapsed(s->ev[1], s->ev[2]);
       timing->d2h_ms = elapsed(s->ev[2], s->ev[3]);
       timing->total_ms = elapsed(s->ev[0], s->ev[3]);
+      timing->embed_ms = full || a->T == 0 ? 0.0 : elapsed(s->kev[0], s->kev[1]);
       collect_errors(s, st);
     }
   });

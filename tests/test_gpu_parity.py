@@ -559,3 +559,24 @@ def test_l2_hot_block_is_bit_identical(name):
         assert np.array_equal(hot.forward(dense, idx), plain.forward(dense, idx))
     hot.close()
     plain.close()
+
+
+def test_embed_kernel_timing():
+    """rs_timing.embed_ms: the embedding kernel alone (event nodes captured
+    around it in the pool graph) — positive, inside the graph's own time, and
+    0 for a full forward."""
+    torch = pytest.importorskip("torch")
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 10_000
+    acc = rs.Accelerator(spec, rows, seed=2, max_query_size=256, fc_mode=rs.FC_AUTO)
+    d, i = rs.fill_query(spec, rows, 4, 0, 200)
+    td, ti = torch.from_numpy(d).cuda(), torch.from_numpy(i).cuda()
+    pooled = torch.empty((200, acc.pooled_dim), device="cuda")
+    out = torch.empty((200, acc.output_dim), device="cuda")
+    for _ in range(3):
+        t = acc.pooled_ptr(200, ti.data_ptr(), pooled.data_ptr(), rs.MEM_DEVICE, timed=True)
+    assert 0 < t.embed_ms <= t.compute_ms
+    f = acc.forward_ptr(200, td.data_ptr(), ti.data_ptr(), out.data_ptr(), rs.MEM_DEVICE,
+                        timed=True)
+    assert f.embed_ms == 0.0 and f.compute_ms > 0
+    acc.close()
