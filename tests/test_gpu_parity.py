@@ -557,6 +557,24 @@ def test_l2_hot_block_is_bit_identical(name):
         idx[0, 0, :2] = [R - 1, R]  # both sides of the boundary
         assert np.array_equal(hot.pooled(idx), orc.sls_canonical(idx))
         assert np.array_equal(hot.forward(dense, idx), plain.forward(dense, idx))
+        # int32 indices (widened on the device) and the pipelined queue
+        assert np.array_equal(hot.forward(dense, idx.astype(np.int32)), plain.forward(dense, idx))
+    torch = pytest.importorskip("torch")
+    sizes = [7, 300, 64]
+    qs = [rs.fill_query(spec, rows, 5, k, S, zipf_alpha=1.05) for k, S in enumerate(sizes)]
+    dd = [torch.from_numpy(d).cuda() for d, _ in qs]
+    di = [torch.from_numpy(i).cuda() for _, i in qs]
+    outs = [torch.empty((S, hot.output_dim), device="cuda") for S in sizes]
+    b = hot.batch(sizes, [t.data_ptr() for t in dd], [t.data_ptr() for t in di],
+                  [o.data_ptr() for o in outs], rs.MEM_DEVICE)
+    hot.forward_many(None, prepared=b)
+    for (d, i), o in zip(qs, outs):
+        assert np.array_equal(o.cpu().numpy(), plain.forward(d, i))
+    # bad index still reported on the hot path
+    d, i = rs.fill_query(spec, rows, 5, 9, 4, zipf_alpha=1.05)
+    i[2, 1, 3] = rows
+    with pytest.raises(rs.IndexOutOfRange):
+        hot.forward(d, i)
     hot.close()
     plain.close()
 
