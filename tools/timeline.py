@@ -42,6 +42,28 @@ def summarize(events):
         cover += cur_e - cur_s
     out = {"window_us": t1 - t0, "kernels": len(ks), "sls_live_fraction": cover / (t1 - t0),
            "per_kernel": []}
+    # host-link activity (--host): H2D copy durations, GB/s per copy, and the
+    # fraction of the window with at least one H2D copy in flight
+    cps = [e for e in events if e.get("cat") == "gpu_memcpy" and "HtoD" in e.get("name", "")]
+    big = [e for e in cps if e.get("args", {}).get("bytes", 0) >= (1 << 20)]
+    if big:
+        iv = sorted((e["ts"], e["ts"] + e["dur"]) for e in big)
+        lo, hi = iv[0][0], max(b for _, b in iv)
+        cov, cs, ce = 0.0, None, None
+        for a, b in iv:
+            if ce is None or a > ce:
+                if ce is not None:
+                    cov += ce - cs
+                cs, ce = a, b
+            else:
+                ce = max(ce, b)
+        cov += ce - cs
+        out["h2d"] = {"copies": len(big), "small_h2d_copies": len(cps) - len(big),
+                      "mean_us": float(np.mean([e["dur"] for e in big])),
+                      "mean_gbs_per_copy": float(np.mean([e["args"]["bytes"] / e["dur"] / 1e3
+                                                          for e in big])),
+                      "busy_fraction": cov / (hi - lo),
+                      "overall_gbs": sum(e["args"]["bytes"] for e in big) / (hi - lo) / 1e3}
     for k, v in sorted(by.items(), key=lambda kv: -sum(kv[1])):
         out["per_kernel"].append({"kernel": k, "launches": len(v), "mean_us": float(np.mean(v)),
                                   "p50_us": float(np.median(v)), "max_us": float(np.max(v)),
@@ -57,6 +79,7 @@ def main():
     ap.add_argument("--pool", type=int, default=64)
     ap.add_argument("--max-query", type=int, default=1000)
     ap.add_argument("--trace", default="")
+    ap.add_argument("--host", action="store_true", help="pinned host inputs (e2e path)")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -75,8 +98,22 @@ def main():
                          queue_depth=args.depth)
     out = torch.empty((args.max_query, acc.output_dim), device="cuda")
     qs = [k % args.pool for k in range(args.n)]
-    b = acc.batch([int(sizes[q]) for q in qs], [dq[q].data_ptr() for q in qs],
-                  [iq[q].data_ptr() for q in qs], [out.data_ptr()] * len(qs), rs.MEM_DEVICE)
+    if args.host:  # one packed pinned buffer per query, as bench.py's e2e
+        keep, dp, ip = [], [], []
+        for q in range(args.pool):
+            d, i = dq[q].cpu().numpy(), iq[q].cpu().numpy()
+            hb = rs.PinnedBuffer(d.nbytes + i.nbytes)
+            hb.view(np.uint8, (d.nbytes + i.nbytes,))[...] = np.concatenate(
+                [d.reshape(-1).view(np.uint8), i.reshape(-1).view(np.uint8)])
+            keep.append(hb)
+            dp.append(hb.ptr)
+            ip.append(hb.ptr + d.nbytes)
+        ob = rs.PinnedBuffer(args.max_query * acc.output_dim * 4)
+        b = acc.batch([int(sizes[q]) for q in qs], [dp[q] for q in qs], [ip[q] for q in qs],
+                      [ob.ptr] * len(qs), rs.MEM_HOST)
+    else:
+        b = acc.batch([int(sizes[q]) for q in qs], [dq[q].data_ptr() for q in qs],
+                      [iq[q].data_ptr() for q in qs], [out.data_ptr()] * len(qs), rs.MEM_DEVICE)
     acc.forward_many(None, prepared=b)
     acc.forward_many(None, prepared=b)
     torch.cuda.synchronize()
