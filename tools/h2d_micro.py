@@ -1,6 +1,8 @@
 """Host-link microbenchmark: H2D GB/s for query-sized copies (~7 MB, the int64
 indices of a 300-item cfg3 RMC2 query) from regular vs write-combined pinned
-memory (rs_alloc_pinned_flags), back to back on one stream.
+memory (rs_alloc_pinned_flags), back to back on one stream; two alternating
+streams; 256 distinct source buffers; D2H alone and duplex (H2D and D2H on
+separate streams at once: ~45 GB/s each way on the B200 box).
 
   python tools/h2d_micro.py
 """
