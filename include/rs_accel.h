@@ -326,6 +326,17 @@ int rs_fill_query_zipf(const rs_model_desc* m, int64_t rows_per_table,
                        uint64_t seed, uint64_t query_id, int64_t size,
                        double alpha, float* dense, int64_t* indices);
 
+/* SparseLengthsSum on the host cores for the CPU side of the split
+ * (replaces the costed EmbeddingLookup/Sum work of
+ * cpu_service_time, proj/src/platform.cpp:71-103, for sub-queries routed to
+ * CPU by proj/src/sim.cpp:173-191). tables f32[T][rows][D] in host memory,
+ * indices i64[S][T][L], pooled f32[S][T][D]. Bit-identical to rs_pooled's
+ * Sum path (same canonical order). threads <= 0: all hardware threads.
+ * RS_E_INDEX for an index outside [0, rows_per_table).                     */
+int rs_host_sls(const float* tables, int64_t rows_per_table, int32_t num_tables,
+                int32_t lookups, int32_t dim, int64_t query_size,
+                const int64_t* indices, float* pooled, int32_t threads);
+
 /* Pinned host memory for rs_query buffers. rs_alloc_pinned_flags accepts
  * RS_PINNED_WRITE_COMBINED for input buffers the host only writes (faster
  * H2D over PCIe; host reads from it are very slow).                         */

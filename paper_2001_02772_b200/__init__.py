@@ -196,6 +196,8 @@ _sig("rs_accel_set_option", C.c_int, C.c_void_p, C.c_int32, C.c_int64)
 _sig("rs_serve", C.c_int, P(C.c_void_p), C.c_int32, C.c_int64, P(CQuery), P(C.c_double),
      P(C.c_void_p), P(C.c_double))
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
+_sig("rs_host_sls", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+     C.c_int64, C.c_void_p, C.c_void_p, C.c_int32)
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
 _sig("rs_fill_query_zipf", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
@@ -210,7 +212,7 @@ EXPORTED_SYMBOLS = [
     "rs_work", "rs_predict_input_dim", "rs_accel_input_bytes", "rs_sla_target", "rs_route",
     "rs_dist_production", "rs_gen_trace", "rs_qps_under_sla", "rs_accel_create",
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
-    "rs_pooled", "rs_service_time",
+    "rs_pooled", "rs_service_time", "rs_host_sls",
     "rs_fill_query", "rs_fill_query_zipf", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
     "rs_device_count", "rs_accel_set_option", "rs_serve"]
 
@@ -460,6 +462,22 @@ def fill_query(model: ModelSpec, rows: int, seed: int, query_id: int, size: int,
         _check(_lib.rs_fill_query(C.byref(model.to_c()), rows, seed, query_id, size,
                                   dense.ctypes.data, idx.ctypes.data))
     return dense, idx
+
+
+def host_sls(tables: np.ndarray, idx: np.ndarray, threads: int = 0) -> np.ndarray:
+    """SparseLengthsSum on the host cores (the CPU side of the split, SURVEY
+    §8f-4): tables f32[T, rows, D], idx i64[S, T, L] -> pooled f32[S, T*D],
+    bit-identical to Accelerator.pooled's Sum path. threads <= 0: all."""
+    tables = np.ascontiguousarray(tables, dtype=np.float32)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    T, rows, D = tables.shape
+    S, Ti, L = idx.shape
+    if Ti != T:
+        raise InvalidArgument(f"indices name {Ti} tables, tables hold {T}")
+    out = np.empty((S, T * D), dtype=np.float32)
+    _check(_lib.rs_host_sls(tables.ctypes.data, rows, T, L, D, S, idx.ctypes.data,
+                            out.ctypes.data, int(threads)))
+    return out
 
 
 # ---- the accelerator -------------------------------------------------------
