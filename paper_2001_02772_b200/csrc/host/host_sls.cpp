@@ -17,7 +17,7 @@
 // the next rows of a bag are prefetched a few lookups ahead (the gather is
 // DRAM-latency bound on the host exactly as on the device).
 #include <algorithm>
-#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -28,7 +28,6 @@
 namespace rs {
 namespace {
 
-constexpr int kPrefetch = 8;  // lookups ahead
 
 int canonical_r(int D) {
   if (D == 8 || D == 16 || D == 32 || D == 64 || D == 128 || D == 256) {
@@ -42,7 +41,7 @@ int canonical_r(int D) {
 __attribute__((target_clones("avx512f", "avx2", "default")))
 int64_t pool_range(const float* __restrict__ tables, int64_t rows, int T, int L, int D, int R,
                    const int64_t* __restrict__ idx, float* __restrict__ pooled, int64_t b0,
-                   int64_t b1) {
+                   int64_t b1, int pf) {
   std::vector<float> part_buf((size_t)R * D);
   float* __restrict__ part = part_buf.data();
   for (int64_t bag = b0; bag < b1; ++bag) {
@@ -51,8 +50,8 @@ int64_t pool_range(const float* __restrict__ tables, int64_t rows, int T, int L,
     const int64_t* __restrict__ bi = idx + bag * L;
     std::memset(part, 0, sizeof(float) * (size_t)R * D);
     for (int l = 0; l < L; ++l) {
-      if (l + kPrefetch < L) {
-        const int64_t rp = bi[l + kPrefetch];
+      if (l + pf < L) {
+        const int64_t rp = bi[l + pf];
         if ((uint64_t)rp < (uint64_t)rows)
           for (int o = 0; o < D; o += 16) __builtin_prefetch(tab + rp * D + o);
       }
@@ -89,13 +88,17 @@ extern "C" int rs_host_sls(const float* tables, int64_t rows_per_table, int32_t 
   if (!tables || !pooled || (lookups > 0 && !indices))
     return fail(RS_E_INVALID, "rs_host_sls: null buffer");
   const int R = canonical_r(dim);
+  static const int pf = [] {  // lookups prefetched ahead (RS_HOST_PREFETCH)
+    const char* v = getenv("RS_HOST_PREFETCH");
+    return v ? std::max(1, atoi(v)) : 8;
+  }();
   int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
   nt = (int)std::min<int64_t>(nt, bags);
   std::vector<int64_t> bad(nt, -1);
   auto run = [&](int i) {
     const int64_t b0 = bags * i / nt, b1 = bags * (i + 1) / nt;
     bad[i] = pool_range(tables, rows_per_table, num_tables, lookups, dim, R, indices, pooled,
-                        b0, b1);
+                        b0, b1, pf);
   };
   if (nt == 1) {
     run(0);
