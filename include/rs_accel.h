@@ -337,6 +337,16 @@ int rs_host_sls(const float* tables, int64_t rows_per_table, int32_t num_tables,
                 int32_t lookups, int32_t dim, int64_t query_size,
                 const int64_t* indices, float* pooled, int32_t threads);
 
+/* Fully connected layer on the host cores (the GEMM half of
+ * the CPU side of the split; replaces the costed DenseFC/PredictFC flops of
+ * cpu_service_time, proj/src/platform.cpp:71-103):
+ * y[rows][out] = act(bias + x[rows][in] * weight^T), weight f32[out][in]
+ * (the device layout), bias may be NULL, relu != 0 applies ReLU. fp32 with
+ * FMA; DESIGN.md §4 tolerance, not bit identity. threads <= 0: all.       */
+int rs_host_fc(const float* x, int64_t rows, int32_t in_dim, const float* weight,
+               const float* bias, int32_t out_dim, int32_t relu, float* y,
+               int32_t threads);
+
 /* Pinned host memory for rs_query buffers. rs_alloc_pinned_flags accepts
  * RS_PINNED_WRITE_COMBINED for input buffers the host only writes (faster
  * H2D over PCIe; host reads from it are very slow).                         */

@@ -198,6 +198,8 @@ _sig("rs_serve", C.c_int, P(C.c_void_p), C.c_int32, C.c_int64, P(CQuery), P(C.c_
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
 _sig("rs_host_sls", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
      C.c_int64, C.c_void_p, C.c_void_p, C.c_int32)
+_sig("rs_host_fc", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+     C.c_int32, C.c_int32, C.c_void_p, C.c_int32)
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
 _sig("rs_fill_query_zipf", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
@@ -212,7 +214,7 @@ EXPORTED_SYMBOLS = [
     "rs_work", "rs_predict_input_dim", "rs_accel_input_bytes", "rs_sla_target", "rs_route",
     "rs_dist_production", "rs_gen_trace", "rs_qps_under_sla", "rs_accel_create",
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
-    "rs_pooled", "rs_service_time", "rs_host_sls",
+    "rs_pooled", "rs_service_time", "rs_host_sls", "rs_host_fc",
     "rs_fill_query", "rs_fill_query_zipf", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
     "rs_device_count", "rs_accel_set_option", "rs_serve"]
 
@@ -478,6 +480,26 @@ def host_sls(tables: np.ndarray, idx: np.ndarray, threads: int = 0) -> np.ndarra
     _check(_lib.rs_host_sls(tables.ctypes.data, rows, T, L, D, S, idx.ctypes.data,
                             out.ctypes.data, int(threads)))
     return out
+
+
+def host_fc(x: np.ndarray, weight: np.ndarray, bias: Optional[np.ndarray] = None,
+            relu: bool = True, threads: int = 0) -> np.ndarray:
+    """Fully connected layer on the host cores: x f32[M, in],
+    weight f32[out, in] (device layout), bias f32[out] or None -> f32[M, out]."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    weight = np.ascontiguousarray(weight, dtype=np.float32)
+    M, K = x.shape
+    N, Kw = weight.shape
+    if Kw != K:
+        raise InvalidArgument(f"weight is [{N}, {Kw}], x has {K} features")
+    b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+    if b is not None and b.shape != (N,):
+        raise InvalidArgument(f"bias shape {b.shape}, expected ({N},)")
+    y = np.empty((M, N), dtype=np.float32)
+    _check(_lib.rs_host_fc(x.ctypes.data, M, K, weight.ctypes.data,
+                           None if b is None else b.ctypes.data, N, int(relu),
+                           y.ctypes.data, int(threads)))
+    return y
 
 
 # ---- the accelerator -------------------------------------------------------

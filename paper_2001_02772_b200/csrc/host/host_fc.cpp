@@ -1,0 +1,98 @@
+// host_fc.cpp — fully connected layer on the host cores for the CPU side of
+// the split (the GEMM half; host_sls.cpp is the gather half).
+// The reference costs this work (DenseFC/PredictFC flops of work(),
+// proj/src/model_zoo.cpp:177-245, priced by cpu_service_time,
+// proj/src/platform.cpp:71-103); this executes it.
+//
+// y[m][n] = act(b[n] + sum_k x[m][k] * W[n][k]) with W in the device layout
+// [out][in]. W is transposed once per call into [in][out] so
+// the inner loop runs across n (vectorised by the AVX-512/AVX2 clones without
+// reassociating a reduction); four rows of x share each W^T row load. Rows of
+// x are dealt to std::threads in contiguous blocks. fp32 with FMA
+// contraction: parity is the floating-point tolerance rule of DESIGN.md §4,
+// not bit identity.
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace rs {
+namespace {
+
+constexpr int kRows = 4;  // rows of x per pass over W^T
+
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void fc_rows(const float* __restrict__ x, int64_t m0, int64_t m1, int K, int N,
+             const float* __restrict__ wt, const float* __restrict__ b, int relu,
+             float* __restrict__ y) {
+  for (int64_t m = m0; m < m1; m += kRows) {
+    const int nr = (int)std::min<int64_t>(kRows, m1 - m);
+    float* __restrict__ yr[kRows];
+    for (int r = 0; r < kRows; ++r) yr[r] = y + (m + std::min(r, nr - 1)) * N;
+    for (int r = 0; r < nr; ++r)
+      for (int n = 0; n < N; ++n) yr[r][n] = b ? b[n] : 0.0f;
+    for (int k = 0; k < K; ++k) {
+      const float* __restrict__ w = wt + (int64_t)k * N;
+      if (nr == kRows) {
+        const float a0 = x[(m + 0) * K + k], a1 = x[(m + 1) * K + k];
+        const float a2 = x[(m + 2) * K + k], a3 = x[(m + 3) * K + k];
+        float* __restrict__ y0 = yr[0];
+        float* __restrict__ y1 = yr[1];
+        float* __restrict__ y2 = yr[2];
+        float* __restrict__ y3 = yr[3];
+        for (int n = 0; n < N; ++n) {
+          const float wn = w[n];
+          y0[n] += a0 * wn;
+          y1[n] += a1 * wn;
+          y2[n] += a2 * wn;
+          y3[n] += a3 * wn;
+        }
+      } else {
+        for (int r = 0; r < nr; ++r) {
+          const float a = x[(m + r) * K + k];
+          float* __restrict__ yy = yr[r];
+          for (int n = 0; n < N; ++n) yy[n] += a * w[n];
+        }
+      }
+    }
+    if (relu)
+      for (int r = 0; r < nr; ++r)
+        for (int n = 0; n < N; ++n) yr[r][n] = yr[r][n] > 0.0f ? yr[r][n] : 0.0f;
+  }
+}
+
+}  // namespace
+}  // namespace rs
+
+extern "C" int rs_host_fc(const float* x, int64_t rows, int32_t in_dim, const float* weight,
+                          const float* bias, int32_t out_dim, int32_t relu, float* y,
+                          int32_t threads) {
+  using namespace rs;
+  clear_error();
+  if (rows < 0 || in_dim < 0 || out_dim < 1)
+    return fail(RS_E_INVALID, "rs_host_fc: bad shape");
+  if (rows == 0) return RS_OK;
+  if (!y || (in_dim > 0 && (!x || !weight))) return fail(RS_E_INVALID, "rs_host_fc: null buffer");
+  std::vector<float> wt((size_t)in_dim * out_dim);
+  for (int n = 0; n < out_dim; ++n)
+    for (int k = 0; k < in_dim; ++k) wt[(size_t)k * out_dim + n] = weight[(size_t)n * in_dim + k];
+  int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  nt = (int)std::min<int64_t>(nt, (rows + kRows - 1) / kRows);
+  auto run = [&](int i) {
+    const int64_t blocks = (rows + kRows - 1) / kRows;
+    const int64_t m0 = std::min(rows, blocks * i / nt * kRows);
+    const int64_t m1 = std::min(rows, blocks * (i + 1) / nt * kRows);
+    fc_rows(x, m0, m1, in_dim, out_dim, wt.data(), bias, relu, y);
+  };
+  if (nt == 1) {
+    run(0);
+  } else {
+    std::vector<std::thread> pool;
+    pool.reserve(nt);
+    for (int i = 0; i < nt; ++i) pool.emplace_back(run, i);
+    for (auto& th : pool) th.join();
+  }
+  return RS_OK;
+}

@@ -1,6 +1,7 @@
-"""Host-core SparseLengthsSum (the CPU side of the split):
+"""The CPU side of the split. Host-core SparseLengthsSum:
 bit-identical to the oracle's canonical order (oracle/forward.c
-or_sls_canonical) on CPU, and to the B200 kernel's pooled output on the GPU."""
+or_sls_canonical) on CPU, and to the B200 kernel's pooled output on the GPU.
+Host FC: the fp32 tolerance rule of DESIGN.md §4 against an fp64 product."""
 import numpy as np
 import pytest
 
@@ -70,3 +71,37 @@ def test_host_sls_matches_b200_pooled(name):
         assert np.array_equal(rs.host_sls(tab, idx).view(np.uint32), dev.view(np.uint32))
     finally:
         acc.close()
+
+
+# ---- host FC (the GEMM half of §8f-4) --------------------------------------
+@pytest.mark.parametrize("M,K,N", [(1, 13, 512), (7, 64, 1), (33, 256, 128), (5, 0, 8),
+                                   (130, 1024, 67)])
+@pytest.mark.parametrize("relu", [True, False])
+def test_host_fc_matches_fp64(M, K, N, relu):
+    """DESIGN.md §4 fp32 tolerance rule: |y - ref| / mag <= 1e-5, with mag the
+    absolute-value forward (|b| + |x| @ |W|^T)."""
+    rng = np.random.default_rng(M * 1000 + K + N)
+    x = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (N, K)) / np.sqrt(max(K, 1))).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+    ref = x.astype(np.float64) @ w.T.astype(np.float64) + b
+    mag = np.abs(x.astype(np.float64)) @ np.abs(w.T.astype(np.float64)) + np.abs(b) + 1e-30
+    if relu:
+        ref = np.maximum(ref, 0)
+    for threads in (1, 3):
+        y = rs.host_fc(x, w, b, relu=relu, threads=threads)
+        assert y.shape == (M, N) and y.dtype == np.float32
+        assert np.max(np.abs(y - ref) / mag, initial=0) <= 1e-5
+        if relu:
+            assert np.all(y >= 0)
+
+
+def test_host_fc_edges():
+    x = np.ones((3, 4), np.float32)
+    w = np.ones((2, 4), np.float32)
+    assert np.array_equal(rs.host_fc(x, w, None, relu=False), np.full((3, 2), 4, np.float32))
+    assert rs.host_fc(np.zeros((0, 4), np.float32), w).shape == (0, 2)
+    with pytest.raises(rs.InvalidArgument):
+        rs.host_fc(x, np.ones((2, 5), np.float32))
+    with pytest.raises(rs.InvalidArgument):
+        rs.host_fc(x, w, np.ones(3, np.float32))

@@ -1,4 +1,4 @@
-"""Throughput of rs_host_sls (host-core SparseLengthsSum) on a
+"""Throughput of rs_host_sls and rs_host_fc (host-core SparseLengthsSum) on a
 cfg3-RMC2-like bag shape: T tables x rows x D=64, L=80 lookups, uniform
 indices, tables larger than the host's last-level cache. Algorithmic bytes
 per bag = L*D*4 (rows read) + L*8 (indices) + D*4 (pooled written), the same
@@ -43,6 +43,19 @@ def main():
         out["runs"].append({"threads": threads, "ms_per_query": dt * 1e3,
                             "GBps": bags * bag_bytes / dt / 1e9,
                             "items_per_s": a.S / dt})
+    # host FC at a predict-layer shape: x[S, 512] @ W[256, 512]^T, bias + ReLU
+    x = rng.standard_normal((a.S, 512), dtype=np.float32)
+    w = rng.standard_normal((256, 512), dtype=np.float32)
+    bias = np.zeros(256, np.float32)
+    out["fc"] = {"shape": [a.S, 512, 256], "runs": []}
+    for threads in sorted({1, 4, 16, os.cpu_count() or 1}):
+        rs.host_fc(x, w, bias, True, threads)
+        t0 = time.perf_counter()
+        for _ in range(a.reps):
+            rs.host_fc(x, w, bias, True, threads)
+        dt = (time.perf_counter() - t0) / a.reps
+        out["fc"]["runs"].append({"threads": threads, "ms": dt * 1e3,
+                                  "GFLOPs": 2 * a.S * 512 * 256 / dt / 1e9})
     print(json.dumps(out))
 
 
