@@ -7,7 +7,8 @@
 // y[m][n] = act(b[n] + sum_k x[m][k] * W[n][k]) with W in the device layout
 // [out][in]. W is transposed once per call into [in][out] so
 // the inner loop runs across n (vectorised by the AVX-512/AVX2 clones without
-// reassociating a reduction); four rows of x share each W^T row load. Rows of
+// reassociating a reduction); a 4 x 32 tile of y stays in vector registers
+// across the K loop, so each W^T load feeds four rows of x. Rows of
 // x are dealt to std::threads in contiguous blocks. fp32 with FMA
 // contraction: parity is the floating-point tolerance rule of DESIGN.md §4,
 // not bit identity.
@@ -23,16 +24,55 @@ namespace {
 
 constexpr int kRows = 4;  // rows of x per pass over W^T
 
+typedef float v16 __attribute__((vector_size(64)));
+
+#define LOAD16(dst, p) std::memcpy(&(dst), (p), sizeof(v16))
+
 __attribute__((target_clones("avx512f", "avx2", "default")))
 void fc_rows(const float* __restrict__ x, int64_t m0, int64_t m1, int K, int N,
              const float* __restrict__ wt, const float* __restrict__ b, int relu,
              float* __restrict__ y) {
+  const int n32 = N / 32 * 32;
   for (int64_t m = m0; m < m1; m += kRows) {
     const int nr = (int)std::min<int64_t>(kRows, m1 - m);
+    if (nr == kRows && n32 > 0) {
+      // 4 rows x 32 columns of y in eight vector registers across the K loop
+      for (int n0 = 0; n0 < n32; n0 += 32) {
+        v16 acc[kRows][2];
+        for (int r = 0; r < kRows; ++r) {
+          acc[r][0] = v16{};
+          acc[r][1] = v16{};
+          if (b) {
+            LOAD16(acc[r][0], b + n0);
+            LOAD16(acc[r][1], b + n0 + 16);
+          }
+        }
+        for (int k = 0; k < K; ++k) {
+          v16 w0, w1;
+          LOAD16(w0, wt + (int64_t)k * N + n0);
+          LOAD16(w1, wt + (int64_t)k * N + n0 + 16);
+          for (int r = 0; r < kRows; ++r) {
+            const float a = x[(m + r) * K + k];
+            acc[r][0] += a * w0;
+            acc[r][1] += a * w1;
+          }
+        }
+        for (int r = 0; r < kRows; ++r) {
+          if (relu) {
+            acc[r][0] = acc[r][0] > 0.0f ? acc[r][0] : v16{};
+            acc[r][1] = acc[r][1] > 0.0f ? acc[r][1] : v16{};
+          }
+          std::memcpy(y + (m + r) * N + n0, &acc[r][0], sizeof(v16));
+          std::memcpy(y + (m + r) * N + n0 + 16, &acc[r][1], sizeof(v16));
+        }
+      }
+      if (n32 == N) continue;
+    }
+    const int nb = (nr == kRows) ? n32 : 0;  // columns already written
     float* __restrict__ yr[kRows];
     for (int r = 0; r < kRows; ++r) yr[r] = y + (m + std::min(r, nr - 1)) * N;
     for (int r = 0; r < nr; ++r)
-      for (int n = 0; n < N; ++n) yr[r][n] = b ? b[n] : 0.0f;
+      for (int n = nb; n < N; ++n) yr[r][n] = b ? b[n] : 0.0f;
     for (int k = 0; k < K; ++k) {
       const float* __restrict__ w = wt + (int64_t)k * N;
       if (nr == kRows) {
@@ -42,7 +82,7 @@ void fc_rows(const float* __restrict__ x, int64_t m0, int64_t m1, int K, int N,
         float* __restrict__ y1 = yr[1];
         float* __restrict__ y2 = yr[2];
         float* __restrict__ y3 = yr[3];
-        for (int n = 0; n < N; ++n) {
+        for (int n = nb; n < N; ++n) {
           const float wn = w[n];
           y0[n] += a0 * wn;
           y1[n] += a1 * wn;
@@ -53,13 +93,13 @@ void fc_rows(const float* __restrict__ x, int64_t m0, int64_t m1, int K, int N,
         for (int r = 0; r < nr; ++r) {
           const float a = x[(m + r) * K + k];
           float* __restrict__ yy = yr[r];
-          for (int n = 0; n < N; ++n) yy[n] += a * w[n];
+          for (int n = nb; n < N; ++n) yy[n] += a * w[n];
         }
       }
     }
     if (relu)
       for (int r = 0; r < nr; ++r)
-        for (int n = 0; n < N; ++n) yr[r][n] = yr[r][n] > 0.0f ? yr[r][n] : 0.0f;
+        for (int n = nb; n < N; ++n) yr[r][n] = yr[r][n] > 0.0f ? yr[r][n] : 0.0f;
   }
 }
 
