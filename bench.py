@@ -45,33 +45,100 @@ METRIC = "QPS at p95 tail-latency SLA per model at 1/2/4/8 B200; SLS HBM GB/s vs
 NOMINAL_HBM_GBS = 8000.0
 
 
+# Workloads as neutral shape descriptions, so that the CPU reference arm can
+# build them without importing the product package (it uses the compiled
+# reference's own zoo through oracle/cpu_arm.py). zoo=… without shapes means
+# the reference's builtin_model (proj/src/model_zoo.cpp:141-170).
+WORKLOADS = {
+    "cfg3-rmc2": dict(name="cfg3-DLRM-RMC2", zoo="DLRM-RMC2", rows=10_000_000,
+                      dense_fc=[256, 128, 64], predict_fc=[512, 128, 1], T=32, L=80, D=64,
+                      pooling="Sum", dense_in=256),
+    "cfg3-rmc3": dict(name="cfg3-DLRM-RMC3", zoo="DLRM-RMC3", rows=10_000_000,
+                      dense_fc=[2560, 512, 64], predict_fc=[512, 128, 1], T=32, L=20, D=64,
+                      pooling="Sum", dense_in=256),
+    "cfg1-rmc1": dict(name="cfg1-DLRM-RMC1", zoo="DLRM-RMC1", rows=1_000_000,
+                      dense_fc=[256, 128, 32], predict_fc=[256, 64, 1], T=8, L=80, D=32,
+                      pooling="Sum", dense_in=256),
+    # BASELINE configs[4]: DIEN GRU seq len 100
+    "cfg5-dien": dict(name="cfg5-DIEN", zoo="DIEN", rows=1_000_000, predict_fc=[200, 80, 2],
+                      T=20, L=100, D=32, pooling="AttentionRNN", hidden=64),
+    "cfg5-din": dict(zoo="DIN", rows=1_000_000),
+    "ncf": dict(zoo="NCF", rows=1_000_000), "wnd": dict(zoo="WND", rows=1_000_000),
+    "mt-wnd": dict(zoo="MT-WND", rows=1_000_000), "din": dict(zoo="DIN", rows=1_000_000),
+    "dien": dict(zoo="DIEN", rows=1_000_000), "rmc1": dict(zoo="DLRM-RMC1", rows=1_000_000),
+    "rmc2": dict(zoo="DLRM-RMC2", rows=1_000_000), "rmc3": dict(zoo="DLRM-RMC3", rows=1_000_000),
+}
+# workloads whose dominant kernel is the predict stack (tensor-pipe roofline)
+TENSOR_BOUND = ("mt-wnd", "wnd")
+
+
 def workload_spec(rs, name):
-    if name == "cfg3-rmc2":
-        return rs.ModelSpec("cfg3-DLRM-RMC2", dense_fc=rs.LayerStack([256, 128, 64]),
-                            predict_fc=rs.LayerStack([512, 128, 1]),
-                            embeddings=rs.EmbeddingConfig(32, 80, 64, "Sum"),
-                            dense_input_dim=256), 10_000_000, "DLRM-RMC2"
-    if name == "cfg3-rmc3":
-        return rs.ModelSpec("cfg3-DLRM-RMC3", dense_fc=rs.LayerStack([2560, 512, 64]),
-                            predict_fc=rs.LayerStack([512, 128, 1]),
-                            embeddings=rs.EmbeddingConfig(32, 20, 64, "Sum"),
-                            dense_input_dim=256), 10_000_000, "DLRM-RMC3"
-    if name == "cfg1-rmc1":
-        return rs.ModelSpec("cfg1-DLRM-RMC1", dense_fc=rs.LayerStack([256, 128, 32]),
-                            predict_fc=rs.LayerStack([256, 64, 1]),
-                            embeddings=rs.EmbeddingConfig(8, 80, 32, "Sum"),
-                            dense_input_dim=256), 1_000_000, "DLRM-RMC1"
-    if name == "cfg5-dien":   # BASELINE configs[4]: DIEN GRU seq len 100
-        return rs.ModelSpec("cfg5-DIEN", predict_fc=rs.LayerStack([200, 80, 2]),
-                            embeddings=rs.EmbeddingConfig(20, 100, 32, "AttentionRNN"),
-                            recurrent_hidden_dim=64), 1_000_000, "DIEN"
-    if name == "cfg5-din":    # BASELINE configs[4]: DIN attention (zoo shape, T20 L200)
-        return rs.builtin_model("DIN"), 1_000_000, "DIN"
-    # zoo models with 1M-row tables
-    zoo = {"ncf": "NCF", "wnd": "WND", "mt-wnd": "MT-WND", "din": "DIN", "dien": "DIEN",
-           "rmc1": "DLRM-RMC1", "rmc2": "DLRM-RMC2", "rmc3": "DLRM-RMC3"}
-    m = zoo[name]
-    return rs.builtin_model(m), 1_000_000, m
+    """(product ModelSpec, rows per table, zoo name for sla_target)."""
+    w = WORKLOADS[name]
+    if "T" not in w:
+        return rs.builtin_model(w["zoo"]), w["rows"], w["zoo"]
+    return rs.ModelSpec(w["name"], dense_fc=rs.LayerStack(w["dense_fc"]) if w.get("dense_fc") else None,
+                        predict_fc=rs.LayerStack(w["predict_fc"]),
+                        embeddings=rs.EmbeddingConfig(w["T"], w["L"], w["D"], w["pooling"]),
+                        dense_input_dim=w.get("dense_in", 0),
+                        recurrent_hidden_dim=w.get("hidden")), w["rows"], w["zoo"]
+
+
+def workload_or_model(name):
+    """The same workload as the oracle's C model struct (no product import)."""
+    from oracle import cpu_arm
+    w = WORKLOADS[name]
+    if "T" not in w:
+        return cpu_arm.builtin_model(w["zoo"]), w["rows"], w["zoo"]
+    pool = {"Sum": 0, "Concat": 1, "AttentionFC": 2, "AttentionRNN": 3}[w["pooling"]]
+    return cpu_arm.make_model(w["name"], w["predict_fc"], w["T"], w["L"], w["D"], pool,
+                              dense_in=w.get("dense_in", 0), dense_fc=w.get("dense_fc"),
+                              hidden=w.get("hidden", 0)), w["rows"], w["zoo"]
+
+
+def sla_for(args, zoo_name, sla_target):
+    """configs[4] states a 100 ms p95 SLA for DIN/DIEN; elsewhere
+    the reference's medium target (proj/src/autotune.cpp:73-88)."""
+    if args.sla > 0:
+        return args.sla
+    return 0.100 if args.workload.startswith("cfg5") else sla_target(zoo_name, "medium")
+
+
+def window(k, Q):
+    base = (k % 2) * Q
+    return range(base, base + Q)
+
+
+def make_config(args, name, shape, rows, sizes, world, sla):
+    """The JSON line's `config`: a function of the workload and the flags only,
+    identical in both arms (the driver compares them)."""
+    T, L, D, dense_in = shape
+    Q, K = args.queries_per_step, args.steps
+    i32, bf16 = args.index_bits == 32, args.dense_bits == 16
+    items_step = float(np.mean([sum(int(sizes[q]) for q in window(k, Q)) for k in range(K)]))
+    h2d_step = items_step * (dense_in * (2 if bf16 else 4) + T * L * (4 if i32 else 8))
+    return {
+        "workload": args.workload, "model": name, "rows_per_table": rows,
+        "tables": T, "lookups": L, "dim": D, "queries_per_step": Q,
+        "items_per_step": items_step, "sla_s": sla,
+        "size_distribution": f"LogNormal(ln {args.size_median:g}, 0.5) clamped to "
+                             f"[1, {args.max_query}] (SURVEY 8d (i))",
+        "fc_path": args.fc, "parallelism": f"replicas{world}",
+        "input_format": ("LABELLED variant (SURVEY 8f-2), not the reference byte model: " +
+                         " + ".join((["int32 indices"] if i32 else []) +
+                                    (["bf16 dense"] if bf16 else []))
+                         if (i32 or bf16) else
+                         "reference byte model (int64 indices + fp32 dense)"),
+        "query_merging": (f"up to {args.merge} consecutive queries per launch: LABELLED "
+                          "scheduler extension (SURVEY 8f-3)" if args.merge > 1 else
+                          "off (one query per launch, as the reference's accelerator server)"),
+        "l2": "inputs >> L2 (tables %.1f GB, ~%.0f MB of indices per step)" % (
+            T * rows * D * 4 / 1e9, h2d_step / 1e6),
+        "index_distribution": (
+            f"LABELLED variant (SURVEY 8d): bounded power law alpha={args.zipf:g} "
+            "over [0, rows), low ids hot" if args.zipf > 0 else "uniform"),
+        "l2_persist_mb": args.l2_persist_mb,
+    }
 
 
 def sls_bytes_per_item(spec):
@@ -201,6 +268,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_tensor_peak(fc):
+    """Tensor roofline denominator: tcgen05 kind::tf32 issues at half the bf16
+    rate, so 0.5 x the measured dense bf16 burst (MEASURED_PEAKS.json); fp32
+    FFMA path: the datasheet 75 TF/s fp32 (B200_PROFILING.md)."""
+    if fc == "fp32":
+        return 75.0, "fp32 FFMA datasheet ~75 TF/s (nothing measured for fp32)"
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            bf = json.load(f).get("bf16_tflops")
+        if bf:
+            return 0.5 * bf, f"0.5 x measured bf16 {bf:.0f} TF/s (MEASURED_PEAKS.json): tf32 rate"
+    return 1100.0, "fallback: tf32 dense 1.1 PF/s (B200_PROFILING.md)"
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -211,58 +293,86 @@ def measured_peaks():
 
 
 # ---- CPU baseline ------------------------------------------------------------
-class CpuArm:
-    """The oracle's fp32 forward (oracle/forward.c, kind "port") on the host's
-    cores: every worker thread serves whole queries of the same stream. Tables
-    are materialised at rows_cpu rows (>> LLC, so gathers still miss to DRAM)."""
+def cpu_deeprecsched(args, workload, sla, rounds, budget_s, threads=0, rank=0):
+    """The CPU side of DeepRecSched run for real (oracle/cpu_arm.py): the
+    oracle's fp32 forward (kind "port") timed on REQUESTS of b items on this
+    host's cores (1 and all cores busy), tables materialised at the workload's
+    full row count; the measured times replace the reference's modeled
+    cpu_service_time and the UNMODIFIED reference tune() (CPU only: batch
+    ladder, split rule floor(S/B) x B + S mod B over C cores, exact p95,
+    lambda bisection; proj/src/autotune.cpp:90-152, proj/src/sim.cpp:114-124,
+    184-188, 246-290) gives QPS@p95 <= SLA. Returns (result dict, per-round
+    wall seconds)."""
+    from oracle import cpu_arm
+    m, rows, _ = workload_or_model(workload)
+    arm = cpu_arm.CpuDeepRecSched(m, rows, threads=threads)
+    walls = [arm.sample(budget_s) for _ in range(rounds)]
+    t0 = time.time()
+    res = arm.tune(sla, math.log(args.size_median), 0.5, n=50_000, seed=rank_seed(rank),
+                   max_size=args.max_query)
+    res["tune_s"] = time.time() - t0
+    res["fill_s"] = arm.fill_s
+    bs, t1, tc = arm.table()
+    res["table"] = {"request_items": bs.tolist(), "s_1core": t1.tolist(),
+                    f"s_{arm.threads}cores": tc.tolist()}
+    res["threads"] = arm.threads
+    res["rows"] = rows
+    arm.close()
+    return res, walls
 
-    def __init__(self, spec, sizes, threads, rows_cpu=1_000_000):
-        from oracle import Oracle
-        self.orc = Oracle(spec, rows_cpu, seed=1, materialize=True)
-        self.sizes, self.threads, self.rows = sizes, threads, rows_cpu
-        t1 = self.orc.bench_queries(sizes[:1], 1, seed=5)   # calibrate on one query
-        self.per_query = max(t1, 1e-4) / threads
 
-    def sample(self, budget_s):
-        nq = int(min(len(self.sizes), max(self.threads, budget_s / self.per_query)))
-        secs = self.orc.bench_queries(self.sizes[:nq], self.threads, seed=5)
-        return {"value": nq / secs, "unit": "queries/s", "cores": self.threads, "kind": "port",
-                "sample": f"{nq} queries of the same LogNormal stream (mean "
-                          f"{float(np.mean(self.sizes[:nq])):.0f} items), fp32 oracle forward, "
-                          f"one query per thread, {self.threads} threads, tables materialised "
-                          f"at {self.rows:,} rows/table, {secs:.1f} s wall"}
-
-
-def cpu_baseline(spec, sizes, threads, budget_s=15.0):
-    return CpuArm(spec, sizes, threads).sample(budget_s)
+def cpu_sample_text(res, rounds):
+    return (f"{rounds} timing rounds: oracle fp32 forward (oracle/forward.c) on requests of "
+            f"{res['table']['request_items']} items, each timed with 1 and with all "
+            f"{res['threads']} cores busy, tables materialised at {res['rows']:,} rows/table "
+            f"(fill {res['fill_s']:.0f} s); QPS@p95 from the UNMODIFIED reference tune() "
+            f"(CPU only) with cpu_service_time replaced by those times "
+            f"(oracle/ref_cpu_adapter.cpp): chosen batch B={res['batch']}, "
+            f"p95 {res['p95_s'] * 1e3:.1f} ms, n=50,000 queries per evaluation")
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU implementation of the path (oracle port) on all
-    host cores, same metric/config; rank 0 only under torchrun."""
+    """--impl reference: the reference's CPU path on this host (oracle port of
+    the forward, the reference's own scheduler), same metric and config as the
+    B200 arm. Rank 0 only under torchrun. Imports nothing from the product."""
     if rank != 0:
         return
-    import paper_2001_02772_b200 as rs
-    spec, rows, zoo_name = workload_spec(rs, args.workload)
-    _, sizes = rs.gen_trace(rank_seed(0), 1000.0, rs.SizeDistribution.log_normal(math.log(args.size_median), 0.5),
-                            4096)
-    threads = os.cpu_count() or 1
-    arm = CpuArm(spec, sizes, threads)
-    budget = max(2.0, 90.0 / (args.steps + args.warmup))
-    vals = []
-    cb = None
-    for _ in range(args.warmup + args.steps):
-        cb = arm.sample(budget)
-        vals.append(cb["value"])
-    v = statistics.median(vals[args.warmup:])
-    cb["value"] = v
+    from oracle import cpu_arm
+    m, rows, zoo_name = workload_or_model(args.workload)
+    sla = sla_for(args, zoo_name, cpu_arm.sla_target)
+    sizes = np.minimum(cpu_arm.gen_trace_sizes(rank_seed(0), math.log(args.size_median), 0.5,
+                                               2 * args.queries_per_step, args.max_query),
+                       args.max_query)
+    name = m.name.decode()
+    cfg = make_config(args, name, (m.T, m.L, m.D, m.dense_in), rows, sizes, world, sla)
+    # every round is a bounded sample; warm-up rounds are discarded
+    budget = max(1.0, 60.0 / (args.steps + args.warmup))
+    arm = cpu_arm.CpuDeepRecSched(m, rows)
+    for _ in range(args.warmup):
+        arm.sample(budget)
+    arm.samples = {b: ([], []) for b in cpu_arm.REQUEST_SIZES}
+    walls = [arm.sample(budget) for _ in range(args.steps)]
+    res = arm.tune(sla, math.log(args.size_median), 0.5, n=50_000, seed=rank_seed(0),
+                   max_size=args.max_query)
+    bs, t1, tc = arm.table()
+    res.update(fill_s=arm.fill_s, threads=arm.threads, rows=rows,
+               table={"request_items": bs.tolist(), "s_1core": t1.tolist(),
+                      f"s_{arm.threads}cores": tc.tolist()})
+    arm.close()
+    v = res["qps"]
+    cb = {"value": v, "unit": "queries/s", "cores": res["threads"], "kind": "port",
+          "sample": cpu_sample_text(res, args.steps)}
     line = {"metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": args.workload, "model": spec.name,
-                       "rows_per_table": rows, "sla_s": rs.sla_target(zoo_name, "medium")},
-            "cpu_baseline": cb,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean(walls)) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "impl": "reference", "config": cfg,
+            "method": "CPU-only DeepRecSched on this host: reference tune() over measured "
+                      "per-request times (oracle/cpu_arm.py)",
+            "cpu_deeprecsched": {"batch": res["batch"], "p95_ms": res["p95_s"] * 1e3,
+                                 "tune_search_steps": res["search_steps"],
+                                 "request_time_table": res["table"]},
+            "cpu_baseline": cb, "gpu_launches": 0,
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -280,10 +390,7 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=device)
 
     spec, rows, zoo_name = workload_spec(rs, args.workload)
-    # configs[4] states a 100 ms p95 SLA for DIN/DIEN; elsewhere the
-    # reference's medium target (proj/src/autotune.cpp:73-88)
-    sla = args.sla if args.sla > 0 else (
-        0.100 if args.workload.startswith("cfg5") else rs.sla_target(zoo_name, "medium"))
+    sla = sla_for(args, zoo_name, rs.sla_target)
     Q, K, W = args.queries_per_step, args.steps, args.warmup
     seed = rank_seed(rank)
     _, sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(math.log(args.size_median), 0.5),
@@ -329,13 +436,9 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.current_stream(device)
     sp = stream.cuda_stream
 
-    def window(k):
-        base = (k % 2) * Q
-        return range(base, base + Q)
-
     def prepare(n_steps, host):
         """rs_forward_many arguments for n_steps windows (built before timing)."""
-        qs = [q for k in range(n_steps) for q in window(k)]
+        qs = [q for k in range(n_steps) for q in window(k, Q)]
         if host:
             dp = [h_dense[q][1] for q in qs]
             ip = [h_idx[q][1] for q in qs]
@@ -348,22 +451,25 @@ def run_ours(args, rank, world, local):
             loc = rs.MEM_DEVICE
         return acc.batch([int(sizes[q]) for q in qs], dp, ip, op, loc, index_type=ity)
 
-    def serve(batch):
-        return acc.forward_many(None, stream=sp, timed=True, residence=True, prepared=batch)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    end.record(stream)               # creates the event the library stamps at completion
+    torch.cuda.synchronize(device)
 
     def timed(host):
         with ClockSampler(local) as clk:         # started before warm-up (tool start-up)
-            serve(prepare(W, host))              # warm-up (untimed), synchronous
+            acc.forward_many(None, stream=sp, prepared=prepare(W, host))  # warm-up, untimed
             batch = prepare(K, host)
             torch.cuda.synchronize(device)
             barrier(device)
             torch.cuda.synchronize(device)
-            start = torch.cuda.Event(enable_timing=True)
-            end = torch.cuda.Event(enable_timing=True)
             t0 = time.time()
             start.record(stream)
-            svc_ms, res_ms = serve(batch)        # per-query CUDA-event times
-            end.record(stream)
+            # per-query CUDA-event times; `end` is recorded by the library on
+            # this stream when the last query completed, before it reads the
+            # per-query timestamps back (rs_forward_many_ev)
+            svc_ms, res_ms = acc.forward_many(None, stream=sp, timed=True, residence=True,
+                                              prepared=batch, done_event=end.cuda_event)
             torch.cuda.synchronize(device)
             clk.mark(t0, time.time())
         barrier(device)
@@ -374,42 +480,65 @@ def run_ours(args, rank, world, local):
         extra = np.maximum(res_ms - svc_ms, 0.0) * 1e-3
         return total_s, svc_ms * 1e-3, extra, clk.summary()
 
-    def sla_qps(svc, extra):
+    def sla_qps(svc, extra, lambda_hi=0.0):
         # the reference evaluates traces of n = 50,000 queries
         # (proj/include/recsim/sim.hpp:79): the measured per-query service
         # times are cycled to that length, so an overloaded rate cannot hide
         # behind a short trace
         n = 50_000
         return rs.qps_under_sla(np.resize(svc, n), sla, servers=1, warmup_fraction=0.1,
-                                base_seed=seed, extra_s=np.resize(extra, n))
+                                base_seed=seed, extra_s=np.resize(extra, n), lambda_hi=lambda_hi)
+
+    def stable_point(svc, extra):
+        """p50/p95 at a stable load: 0.9x the measured service capacity."""
+        lam = 0.9 / float(np.mean(svc))
+        r = sla_qps(svc, extra, lambda_hi=lam)
+        return {"load": 0.9, "lambda": lam, "p50_ms": r.p50 * 1e3, "p95_ms": r.p95 * 1e3,
+                "evaluated_at_lambda": r.at_lambda}
 
     # ---- value: device-resident inputs
     t_dev, svc_dev, extra_dev, clocks = timed(host=False)
     r_dev = sla_qps(svc_dev, extra_dev)
     agg = aggregate(r_dev.qps, t_dev, len(svc_dev), world, device)
+    st_dev = stable_point(svc_dev, extra_dev)
     # ---- e2e: host pinned inputs, H2D/D2H inside every query
     t_host, svc_host, extra_host, clocks_e2e = timed(host=True)
     r_host = sla_qps(svc_host, extra_host)
     agg_e2e = aggregate(r_host.qps, t_host, len(svc_host), world, device)
+    st_host = stable_point(svc_host, extra_host)
 
-    # ---- roofline of the dominant kernel (SLS), live CUDA-event timing on the
-    # launching stream: event-record nodes captured right around the SLS
-    # kernel inside the embedding-stage graph (rs_timing.embed_ms)
-    sls_ms, sls_bytes = 0.0, 0.0
-    pooled_dev = torch.empty((args.max_query, acc.pooled_dim), device=device)
-    for q in window(0):
+    # ---- per-stage kernel timing (RS_OPT_STAGE_TIMING): event-record nodes
+    # captured right around the embedding stage and the predict stack in a
+    # timed copy of the forward graph, on the kernels' own stream
+    peak_hbm, peak_src = measured_peaks()
+    acc.set_option(rs.OPT_STAGE_TIMING, 1)
+    emb_ms, fc_ms, fwd_ms, items_roof = 0.0, 0.0, 0.0, 0
+    out_roof = torch.empty((args.max_query, acc.output_dim), device=device)
+    for q in window(0, Q):
         S = int(sizes[q])
-        t = acc.pooled_ptr(S, d_idx[q].data_ptr(), pooled_dev.data_ptr(), rs.MEM_DEVICE,
-                           stream=sp, timed=True, index_type=ity)
+        t = acc.forward_ptr(S, d_dense[q].data_ptr(), d_idx[q].data_ptr(), out_roof.data_ptr(),
+                            rs.MEM_DEVICE, stream=sp, timed=True, index_type=ity)
+        emb_ms += t.embed_ms
+        fc_ms += t.fc_ms
+        fwd_ms += t.compute_ms
+        items_roof += S
+    acc.set_option(rs.OPT_STAGE_TIMING, 0)
+    n_roof = len(window(0, Q))
+    sls_bytes = items_roof * sls_bytes_per_item(spec)
+    pred_flops = rs.work(spec, items_roof)["PredictFC"][0]
+    # the SLS kernel alone (pool graph, no concurrent dense branch)
+    pooled_dev = torch.empty((args.max_query, acc.pooled_dim), device=device)
+    sls_ms = 0.0
+    for q in window(0, Q):
+        t = acc.pooled_ptr(int(sizes[q]), d_idx[q].data_ptr(), pooled_dev.data_ptr(),
+                           rs.MEM_DEVICE, stream=sp, timed=True, index_type=ity)
         sls_ms += t.embed_ms
-        sls_bytes += S * sls_bytes_per_item(spec)
-    peak, peak_src = measured_peaks()
     achieved = sls_bytes / (sls_ms * 1e-3) / 1e9
     # the same kernel back to back: embedding stage only over the queue's
     # lanes (one query's tail overlaps the next one's ramp), CUDA-event
     # delivery times of rs_forward_many over two windows
     os.environ["RS_MANY_POOL_ONLY"] = "1"
-    qs2 = [q for k in range(2) for q in window(k)]
+    qs2 = [q for k in range(2) for q in window(k, Q)]
     b2 = acc.batch([int(sizes[q]) for q in qs2], [d_dense[q].data_ptr() for q in qs2],
                    [d_idx[q].data_ptr() for q in qs2], [pooled_dev.data_ptr()] * len(qs2),
                    rs.MEM_DEVICE, index_type=ity)
@@ -418,107 +547,214 @@ def run_ours(args, rank, world, local):
     os.environ["RS_MANY_POOL_ONLY"] = "0"
     b2b = sum(int(sizes[q]) for q in qs2) * sls_bytes_per_item(spec) / (svc2.sum() * 1e-3) / 1e9
 
-    items_step = float(np.mean([sum(int(sizes[q]) for q in window(k)) for k in range(K)]))
-    h2d_step = float(np.mean([sum(int(sizes[q]) * (spec.dense_input_dim * (2 if bf16 else 4) +
-                                                   e.num_tables * e.lookups_per_table *
-                                                   (4 if i32 else 8))
-                                  for q in window(k)) for k in range(K)]))
-    d2h_step = float(np.mean([sum(int(sizes[q]) * acc.output_dim * 4 + 4 for q in window(k))
+    cfg = make_config(args, spec.name, (e.num_tables, e.lookups_per_table, e.embedding_dim,
+                                        spec.dense_input_dim), rows, sizes, world, sla)
+    h2d_step = cfg["items_per_step"] * (spec.dense_input_dim * (2 if bf16 else 4) +
+                                        e.num_tables * e.lookups_per_table * (4 if i32 else 8))
+    d2h_step = float(np.mean([sum(int(sizes[q]) * acc.output_dim * 4 + 4 for q in window(k, Q))
                               for k in range(K)]))
     # kernel nodes of the graph each timed query launched (pick_graph in
     # csrc/host/accel.cu: one graph per FC path; FC_AUTO/TF32 = the tcgen05 graph)
-    kl = acc.info.kernels_per_forward
-    launches = int(sum(kl for k in range(K) for q in window(k)))
+    launches = int(acc.info.kernels_per_forward * K * Q)
     # DRAM traffic per launch from the committed ncu --set full capture
     # (profiles/sls_traffic.json: dram read+write bytes / items of that launch),
     # scaled to this run's mean items per roofline launch like `achieved`
-    n_roof = len(window(0))
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "sls_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f).get(args.workload)
         if tj:
-            traffic = tj["dram_bytes_per_item"] * sls_bytes / sls_bytes_per_item(spec) / n_roof
+            traffic = tj["dram_bytes_per_item"] * items_roof / n_roof
             traffic_src = tj.get("source")
+    step_s = t_dev / K
+    hbm_roof = {
+        "bound": "hbm",
+        "kernel": {"Sum": "sls_pipe_kernel", "Concat": "gather_concat_kernel",
+                   "AttentionFC": "din_pool_kernel",
+                   "AttentionRNN": ("gru_kernel" if args.fc == "fp32" else "gru_tc_kernel") +
+                   " (latency-bound recurrence; bytes shown)"}[e.pooling],
+        "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+        "timing": "CUDA events recorded by graph nodes right before and after the kernel, "
+                  "on its stream (rs_timing.embed_ms of the embedding-stage graph)",
+        "frac": achieved / peak_hbm, "peak_source": peak_src,
+        "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
+        "traffic": traffic, "traffic_source": traffic_src,
+        "algorithmic_bytes_per_launch": sls_bytes / n_roof,
+        "algorithmic_bytes_per_item": sls_bytes_per_item(spec),
+        "kernel_share_of_step": (sls_ms * 1e-3 / n_roof) / max(step_s / Q, 1e-12),
+        "back_to_back": {"achieved": b2b, "frac": b2b / peak_hbm,
+                         "method": "embedding stage only, rs_forward_many over the lanes "
+                                   "(RS_MANY_POOL_ONLY), algorithmic bytes / summed delivery "
+                                   "gaps; the measured peak is a read+write copy, a gather "
+                                   "is read-mostly"}}
+    peak_tf, tf_src = measured_tensor_peak(args.fc)
+    fc_tflops = pred_flops / max(fc_ms * 1e-3, 1e-12) / 1e12
+    tensor_roof = {
+        "bound": "tensor", "kernel": "fc_tc_kernel (predict stack: " +
+        f"{len(spec.predict_fc.dims)} layers x {spec.num_parallel_predict_stacks} stacks)"
+        if args.fc != "fp32" else "fc_ffma_kernel (predict stack, FFMA)",
+        "achieved": fc_tflops, "peak": peak_tf, "unit": "TFLOP/s", "frac": fc_tflops / peak_tf,
+        "peak_source": tf_src, "traffic": None,
+        "timing": "CUDA events recorded by graph nodes right before and after the predict "
+                  "stack in the forward graph, on its stream (rs_timing.fc_ms)",
+        "algorithmic_flops_per_launch": pred_flops / n_roof,
+        "algorithmic_flops_per_item": rs.work(spec, 1)["PredictFC"][0],
+        "kernel_share_of_step": (fc_ms * 1e-3 / n_roof) / max(step_s / Q, 1e-12)}
+    want_tensor = args.roofline == "tensor" or (args.roofline == "auto" and
+                                                args.workload in TENSOR_BOUND)
+    roof = dict(tensor_roof if want_tensor else hbm_roof)
+    roof["other"] = hbm_roof if want_tensor else tensor_roof
     if rank == 0:
         line = {
             "metric": METRIC, "value": agg["value"], "unit": "queries/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": agg["time_s"] * 1e3 / K,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp32" if args.fc == "fp32" else "fp32 SLS / tf32 FC",
             "data": f"synthetic (seeded random-init tables/weights, LogNormal(ln{args.size_median:g},0.5) sizes)",
-            "config": {"workload": args.workload, "model": spec.name, "rows_per_table": rows,
-                       "tables": e.num_tables, "lookups": e.lookups_per_table,
-                       "dim": e.embedding_dim, "queries_per_step": Q,
-                       "items_per_step": items_step, "sla_s": sla,
-                       "fc_path": args.fc, "parallelism": f"replicas{world}",
-                       "input_format": ("LABELLED variant (SURVEY 8f-2), not the reference "
-                                        "byte model: " + " + ".join(
-                                            (["int32 indices"] if i32 else []) +
-                                            (["bf16 dense"] if bf16 else []))
-                                        if (i32 or bf16) else
-                                        "reference byte model (int64 indices + fp32 dense)"),
-                       "query_merging": (f"up to {args.merge} consecutive queries per launch: "
-                                         "LABELLED scheduler extension (SURVEY 8f-3)"
-                                         if args.merge > 1 else "off (one query per launch, "
-                                         "as the reference's accelerator server)"),
-                       "l2": "inputs >> L2 (tables %.1f GB, ~%.0f MB of indices per step)" % (
-                           acc.info.table_bytes / 1e9, h2d_step / 1e6),
-                       "index_distribution": (
-                           f"LABELLED variant (SURVEY 8d): bounded power law alpha={args.zipf:g} "
-                           "over [0, rows), low ids hot" if args.zipf > 0 else "uniform"),
-                       "l2_persist": (
-                           f"hot block of {acc.info.hot_rows} rows/table "
-                           f"({acc.info.hot_rows * e.num_tables * e.embedding_dim * 4 / 2**20:.1f} MiB) "
-                           "in the L2 persisting set-aside" if acc.info.hot_rows else "off"),
-                       "qps_method": "open-loop Poisson replay (n=50,000, sim.hpp:79) of the "
-                                     "per-query CUDA-event service times measured in the timed "
-                                     "region (FIFO delivery per GPU, in-pipeline residence "
-                                     "added to latency, exact p95, lambda bisection to 1%, "
-                                     "sim.cpp:246-290); whole job = N x min over ranks"},
+            "config": cfg,
+            "method": "open-loop Poisson replay (n=50,000, sim.hpp:79) of the per-query CUDA-event "
+                      "service times measured in the timed region (FIFO delivery per GPU, "
+                      "in-pipeline residence added to latency, exact p95, lambda bisection to "
+                      "1%, sim.cpp:246-290); whole job = N x min over ranks",
             "sla": {"p95_ms": r_dev.p95 * 1e3, "p50_ms": r_dev.p50 * 1e3,
                     "at_lambda": r_dev.at_lambda, "saturated_qps": agg["saturated_qps"],
                     "mean_service_ms": float(svc_dev.mean() * 1e3),
-                    "queue_depth": args.depth,
+                    "service_capacity_qps": world / float(svc_dev.mean()),
+                    "stable_load": st_dev, "queue_depth": args.depth,
                     "p95_extra_residence_ms": float(np.percentile(extra_dev, 95) * 1e3)},
             "e2e": {"value": agg_e2e["value"], "unit": "queries/s",
                     "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step,
                     "p95_ms": r_host.p95 * 1e3, "saturated_qps": agg_e2e["saturated_qps"],
+                    "stable_load": st_host,
                     "h2d_gbs": h2d_step * K / max(t_host, 1e-9) / 1e9},
-            "roofline": {"bound": "hbm",
-                         "kernel": {"Sum": "sls_pipe_kernel", "Concat": "gather_concat_kernel",
-                                    "AttentionFC": "din_pool_kernel",
-                                    "AttentionRNN": ("gru_kernel" if args.fc == "fp32" else
-                                                     "gru_tc_kernel") +
-                                    " (latency-bound recurrence; bytes shown)"}[e.pooling],
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "timing": "CUDA events recorded by graph nodes right before and "
-                                   "after the kernel, on its stream (rs_timing.embed_ms)",
-                         "frac": achieved / peak, "peak_source": peak_src,
-                         "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
-                         "traffic": traffic, "traffic_source": traffic_src,
-                         "algorithmic_bytes_per_launch": sls_bytes / n_roof,
-                         "algorithmic_bytes_per_item": sls_bytes_per_item(spec),
-                         "kernel_share_of_step": (sls_ms * 1e-3) / max(t_dev / K, 1e-12),
-                         "back_to_back": {"achieved": b2b, "frac": b2b / peak,
-                                          "method": "embedding stage only, rs_forward_many "
-                                                    "over the lanes (RS_MANY_POOL_ONLY), "
-                                                    "algorithmic bytes / summed delivery "
-                                                    "gaps; the measured peak is a read+write "
-                                                    "copy, a gather is read-mostly"}},
+            "stages": {"items": items_roof, "forward_ms": fwd_ms, "embedding_stage_ms": emb_ms,
+                       "predict_stack_ms": fc_ms,
+                       "method": "RS_OPT_STAGE_TIMING forward graph, one query at a time"},
+            "roofline": roof,
             "gpu_launches": launches,
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu:
-            _, cpu_sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
-                math.log(args.size_median), 0.5), 8192)
-            line["cpu_baseline"] = cpu_baseline(spec, np.minimum(cpu_sizes, args.max_query),
-                                                os.cpu_count() or 1)
+            res, walls = cpu_deeprecsched(args, args.workload, sla, rounds=3, budget_s=4.0)
+            line["cpu_baseline"] = {"value": res["qps"], "unit": "queries/s",
+                                    "cores": res["threads"], "kind": "port",
+                                    "sample": cpu_sample_text(res, 3)}
         print(json.dumps(line), flush=True)
     acc.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+# ---- real-time serving over K GPUs (--serve) -------------------------------------
+def run_serve(args):
+    """One Poisson stream over every visible GPU, served in REAL time by the
+    K-replica executor (rs_serve: the reference's single FIFO accelerator,
+    proj/src/sim.cpp:95-97, 126-136, as a least-outstanding-items pool with one
+    dispatcher thread per replica). QPS@p95 <= SLA is found with the
+    reference's search (evaluate, geometric bisection to 1%, feasible iff the
+    exact p95 of post-warm-up queries meets the SLA; sim.cpp:246-290) where each
+    evaluation EXECUTES n queries instead of simulating them. Host pinned
+    inputs (packed [dense | int64 indices], the reference byte model): every
+    query's H2D and D2H is inside its latency. One process, replica r on GPU r."""
+    import paper_2001_02772_b200 as rs
+    spec, rows, zoo_name = workload_spec(rs, args.workload)
+    sla = sla_for(args, zoo_name, rs.sla_target)
+    K = args.gpus
+    if rs.device_count() < K:
+        raise SystemExit(f"--serve --gpus {K}: only {rs.device_count()} devices visible")
+    fc = {"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc]
+    reps = [rs.Accelerator(spec, rows, seed=1, device=r, max_query_size=args.max_query,
+                           fc_mode=fc, queue_depth=args.depth) for r in range(K)]
+    P = 2 * args.queries_per_step
+    seed = rank_seed(0)
+    _, pool_sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
+        math.log(args.size_median), 0.5), P)
+    pool_sizes = np.minimum(pool_sizes, args.max_query)
+    bufs = []
+    for q in range(P):
+        dn, ix = rs.fill_query(spec, rows, seed, q, int(pool_sizes[q]))
+        hb = rs.PinnedBuffer(dn.nbytes + ix.nbytes)
+        raw = hb.view(np.uint8, (dn.nbytes + ix.nbytes,))
+        raw[:dn.nbytes] = dn.reshape(-1).view(np.uint8)
+        raw[dn.nbytes:] = ix.reshape(-1).view(np.uint8)
+        bufs.append((hb, dn.nbytes))
+    outs = [rs.PinnedBuffer(args.max_query * reps[0].output_dim * 4) for _ in range(16)]
+    n = args.serve_n
+    dist = rs.SizeDistribution.log_normal(math.log(args.size_median), 0.5)
+
+    def batch_for(sizes_idx):
+        sizes = [int(pool_sizes[j]) for j in sizes_idx]
+        return reps[0].batch(sizes, [bufs[j][0].ptr for j in sizes_idx],
+                             [bufs[j][0].ptr + bufs[j][1] for j in sizes_idx],
+                             [outs[i % 16].ptr for i in range(len(sizes_idx))], rs.MEM_HOST)
+
+    pool_of = np.arange(n) % P
+    prepared = batch_for(pool_of)
+    warm = int(0.1 * n)
+
+    def evaluate(lam, eval_idx):
+        arr, _ = rs.gen_trace(seed + eval_idx, lam, dist, n)  # Poisson gaps at rate lam
+        arr = arr - arr[0]
+        t0 = time.time()
+        lat = rs.serve(reps, prepared, arr) * 1e-3
+        wall = time.time() - t0
+        post = lat[warm:]
+        p95 = float(np.sort(post)[max(int(math.ceil(0.95 * len(post))), 1) - 1])
+        p50 = float(np.sort(post)[max(int(math.ceil(0.50 * len(post))), 1) - 1])
+        span = float(np.max(arr + lat) - arr[warm])
+        return {"lambda": lam, "p95_ms": p95 * 1e3, "p50_ms": p50 * 1e3,
+                "achieved_qps": (n - warm) / span, "wall_s": wall, "feasible": p95 <= sla}
+
+    # warm-up, then a burst (all arrivals at t=0): the saturated throughput
+    rs.serve(reps, batch_for(pool_of[:min(n, 2000)]), np.zeros(min(n, 2000)))
+    t0 = time.time()
+    lat = rs.serve(reps, prepared, np.zeros(n))
+    burst_qps = n / (float(lat.max()) * 1e-3)
+    evals = []
+    lo, hi = 0.5 * burst_qps, 1.5 * burst_qps
+    e_lo = evaluate(lo, 0)
+    evals.append(e_lo)
+    best = e_lo if e_lo["feasible"] else None
+    e_hi = evaluate(hi, 1)
+    evals.append(e_hi)
+    if e_hi["feasible"]:
+        best = e_hi
+    else:
+        k = 2
+        while hi / lo > 1.01 and best is not None:
+            mid = math.sqrt(lo * hi)
+            e = evaluate(mid, k)
+            k += 1
+            evals.append(e)
+            if e["feasible"]:
+                lo, best = mid, e
+            else:
+                hi = mid
+    stable = evaluate(0.9 * burst_qps, 99)
+    line = {"metric": METRIC + " (real-time serving, --serve)", "mode": "serve",
+            "value": best["achieved_qps"] if best else 0.0, "unit": "queries/s", "n_gpus": K,
+            "higher_is_better": True, "scaling": "weak", "dtype":
+            "fp32" if args.fc == "fp32" else "fp32 SLS / tf32 FC",
+            "config": {"workload": args.workload, "model": spec.name, "rows_per_table": rows,
+                       "sla_s": sla, "replicas": K, "queries_per_evaluation": n,
+                       "distinct_queries": P, "inputs": "host pinned, packed [dense | int64 "
+                       "indices] (reference byte model)", "fc_path": args.fc,
+                       "lanes_per_replica": args.depth},
+            "qps_at_sla": {"qps": best["achieved_qps"] if best else 0.0,
+                           "at_lambda": best["lambda"] if best else 0.0,
+                           "p95_ms": best["p95_ms"] if best else None,
+                           "p50_ms": best["p50_ms"] if best else None},
+            "burst": {"qps": burst_qps, "queries": n,
+                      "method": "all n arrivals at t=0: saturated real throughput"},
+            "stable_load": stable, "evaluations": evals,
+            "method": "rs_serve real-time executor: host clock releases, least-outstanding-"
+                      "items routing, one dispatcher thread per replica, CUDA-event "
+                      "completions; reference search rule (sim.cpp:246-290) over real runs"}
+    print(json.dumps(line), flush=True)
+    for r in reps:
+        r.close()
 
 
 def main():
@@ -550,8 +786,18 @@ def main():
     ap.add_argument("--fc", choices=["fp32", "tf32", "auto"], default="auto")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--depth", type=int, default=8, help="queries in flight per GPU (lanes)")
+    ap.add_argument("--roofline", choices=["auto", "hbm", "tensor"], default="auto",
+                    help="which kernel the roofline object reports (auto: tensor for "
+                         "mt-wnd/wnd, else the embedding kernel)")
+    ap.add_argument("--serve", action="store_true",
+                    help="real-time serving over --gpus replicas in one process (rs_serve)")
+    ap.add_argument("--serve-n", type=int, default=50_000,
+                    help="--serve: queries per evaluation (reference n = 50,000)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.serve:
+        run_serve(args)
+        return
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -220,7 +220,10 @@ typedef struct rs_timing {
   double total_ms;
   double embed_ms;     /* rs_pooled: the embedding kernel alone, between
                           event-record nodes captured around it in the
-                          graph; 0 for rs_forward                          */
+                          graph; rs_forward: the embedding stage when
+                          RS_OPT_STAGE_TIMING is on, else 0              */
+  double fc_ms;        /* rs_forward with RS_OPT_STAGE_TIMING: the predict
+                          stack (PredictFC kernels) alone; else 0         */
 } rs_timing;
 
 typedef struct rs_accel_info {
@@ -276,6 +279,15 @@ int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
                     float* const* outs, void* stream, double* service_ms,
                     double* latency_ms);
 
+/* rs_forward_many plus a completion stamp: `done_event` (a cudaEvent_t the
+ * caller created; may be NULL) is recorded on `stream` once every query of
+ * the call has completed on the device — before the host reads the
+ * per-query timestamps — so a caller's CUDA-event bracket around the call
+ * measures device time only.                                                */
+int rs_forward_many_ev(rs_accel* a, int64_t n, const rs_query* queries,
+                       float* const* outs, void* stream, double* service_ms,
+                       double* latency_ms, void* done_event);
+
 /* Real-time serving over K replicas (one handle per GPU, same model): query i
  * is released at host time t0 + arrival_s[i] (non-decreasing), dispatched to
  * the replica with the least outstanding items (ties to the lowest index; the
@@ -291,8 +303,12 @@ int rs_serve(rs_accel* const* replicas, int32_t k, int64_t n, const rs_query* qu
  *   max_query_size back to back in one slot and serves them with ONE graph
  *   launch; every merged query completes with the group. A LABELLED
  *   scheduler extension: the reference never merges distinct
- *   queries.                                                  */
-enum { RS_OPT_MERGE_QUERIES = 1 };
+ *   queries.
+ * RS_OPT_STAGE_TIMING (default 0): 1 = a timed rs_forward runs a copy of the
+ *   forward graph with event-record nodes around the embedding stage and the
+ *   predict stack and reports them in rs_timing.embed_ms / fc_ms (the
+ *   per-kernel roofline measurement; untimed calls are unaffected).        */
+enum { RS_OPT_MERGE_QUERIES = 1, RS_OPT_STAGE_TIMING = 2 };
 int rs_accel_set_option(rs_accel* a, int32_t option, int64_t value);
 
 /* Wait for `stream` and report (then clear) errors that asynchronous calls

@@ -69,6 +69,8 @@ if lib is not None:
         getattr(lib, f).argtypes = [C.c_void_p]
     lib.or_forward64.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.or_forward64_mt.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
     lib.or_forward32.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.or_sls_canonical.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
     lib.or_table_value.restype = C.c_float
@@ -106,7 +108,9 @@ class Oracle:
             lib.or_destroy(self.h)
             self.h = None
 
-    def forward64(self, dense, idx):
+    def forward64(self, dense, idx, threads: int = 0):
+        """fp64 forward; items are spread over `threads` host threads
+        (0 = every core; results do not depend on the thread count)."""
         S = idx.shape[0] if idx.size else dense.shape[0]
         dense = np.ascontiguousarray(dense, dtype=np.float32)
         idx = np.ascontiguousarray(idx, dtype=np.int64)
@@ -114,8 +118,9 @@ class Oracle:
         mag = np.zeros((S, self.out_dim))
         pooled = np.zeros((S, max(self.pooled_dim, 1)))
         pmag = np.zeros((S, max(self.pooled_dim, 1)))
-        rc = lib.or_forward64(self.h, S, _ptr(dense), _ptr(idx), out.ctypes.data,
-                              mag.ctypes.data, pooled.ctypes.data, pmag.ctypes.data)
+        rc = lib.or_forward64_mt(self.h, S, _ptr(dense), _ptr(idx), out.ctypes.data,
+                                 mag.ctypes.data, pooled.ctypes.data, pmag.ctypes.data,
+                                 threads or (os.cpu_count() or 1))
         if rc:
             raise RuntimeError(f"or_forward64 rc={rc}")
         return out, mag, pooled[:, :self.pooled_dim], pmag[:, :self.pooled_dim]
@@ -190,19 +195,36 @@ def ref_available() -> bool:
 
 
 # The same reference with accel_service_time wrapped to the B200 path
-# (oracle/ref_b200_adapter.cpp).
-ref_b200 = _load(os.path.join(_HERE, "_ref", "librecsim_ref_b200.so"))
-for _lib_ in (ref, ref_b200):
-    if _lib_ is None:
-        continue
-    _lib_.ref_max_qps_accel.argtypes = [
-        P(OrModel), C.c_char_p, C.c_char_p, C.c_double, C.c_uint64, C.c_int, C.c_double,
-        C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
-        P(C.c_double), P(C.c_double), P(C.c_double)]
-    _lib_.ref_tune.argtypes = [
-        P(OrModel), C.c_char_p, C.c_char_p, C.c_double, C.c_uint64, C.c_int, C.c_double,
-        C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int,
-        P(C.c_int64), P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_int64)]
+# (oracle/ref_b200_adapter.cpp). It links the product library,
+# so it is loaded only on request (load_ref_b200), never by the CPU arms.
+_ACCEL_ARGTYPES = [
+    P(OrModel), C.c_char_p, C.c_char_p, C.c_double, C.c_uint64, C.c_int, C.c_double,
+    C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+    P(C.c_double), P(C.c_double), P(C.c_double)]
+_TUNE_ARGTYPES = [
+    P(OrModel), C.c_char_p, C.c_char_p, C.c_double, C.c_uint64, C.c_int, C.c_double,
+    C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int,
+    P(C.c_int64), P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_int64)]
+
+
+def _bind_accel(lib_):
+    lib_.ref_max_qps_accel.argtypes = _ACCEL_ARGTYPES
+    lib_.ref_tune.argtypes = _TUNE_ARGTYPES
+
+
+if ref is not None:
+    _bind_accel(ref)
+_ref_b200 = None
+
+
+def load_ref_b200():
+    """oracle/_ref/librecsim_ref_b200.so (reference + B200 adapter), or None."""
+    global _ref_b200
+    if _ref_b200 is None:
+        _ref_b200 = _load(os.path.join(_HERE, "_ref", "librecsim_ref_b200.so"))
+        if _ref_b200 is not None:
+            _bind_accel(_ref_b200)
+    return _ref_b200
 
 
 def ref_max_qps(lib_, spec, accel: str, cpu: str, sla: float, dist, n: int, batch: int,

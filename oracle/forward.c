@@ -12,6 +12,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
+#include <unistd.h>
 
 /* ---- seeded parameter lattice -------------------------------- */
 static uint64_t sm64(uint64_t x) {
@@ -82,6 +83,43 @@ static const float* or_row(const or_state* s, int64_t t, int64_t r, float* buf) 
   return buf;
 }
 
+/* Materialise every table element (tables of the 10M-row configs are 82 GB:
+ * the fill runs on every core, chunks of rows per work item). */
+typedef struct {
+  or_state* s;
+  atomic_llong next;
+} fill_ctx;
+
+static void* fill_worker(void* p) {
+  fill_ctx* c = (fill_ctx*)p;
+  or_state* s = c->s;
+  const int64_t D = s->m.D, rows = s->rows, chunk = 1 << 16;
+  const int64_t total = s->m.T * rows;
+  for (;;) {
+    const int64_t r0 = atomic_fetch_add(&c->next, chunk);
+    if (r0 >= total) break;
+    const int64_t r1 = r0 + chunk < total ? r0 + chunk : total;
+    for (int64_t g = r0; g < r1; ++g) {
+      const int64_t t = g / rows, r = g % rows;
+      float* dst = s->tables + g * D;
+      for (int64_t cc = 0; cc < D; ++cc) dst[cc] = pval(s->tkey[t], (uint64_t)(r * D + cc), 0.05f);
+    }
+  }
+  return NULL;
+}
+
+static void fill_tables(or_state* s) {
+  long n = sysconf(_SC_NPROCESSORS_ONLN);
+  if (n < 1) n = 1;
+  fill_ctx c;
+  c.s = s;
+  atomic_init(&c.next, 0);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)n);
+  for (long i = 0; i < n; ++i) pthread_create(&th[i], NULL, fill_worker, &c);
+  for (long i = 0; i < n; ++i) pthread_join(th[i], NULL);
+  free(th);
+}
+
 or_state* or_create(const or_model* m, int64_t rows, uint64_t seed, int augru, int materialize) {
   if (m->T > 4096 || m->D > 256 || m->dense_fc.n > 8 || m->predict_fc.n > 8) return NULL;
   or_state* s = (or_state*)calloc(1, sizeof(or_state));
@@ -109,11 +147,9 @@ or_state* or_create(const or_model* m, int64_t rows, uint64_t seed, int augru, i
   }
   for (int64_t t = 0; t < m->T; ++t) s->tkey[t] = key_of(seed, 0x1000ull + (uint64_t)t);
   if (materialize && m->T > 0) {
-    const int64_t per = rows * m->D;
-    s->tables = (float*)malloc(sizeof(float) * (size_t)(m->T * per));
+    s->tables = (float*)malloc(sizeof(float) * (size_t)(m->T * rows * m->D));
     if (!s->tables) { free(s); return NULL; }
-    for (int64_t t = 0; t < m->T; ++t)
-      for (int64_t e = 0; e < per; ++e) s->tables[t * per + e] = pval(s->tkey[t], (uint64_t)e, 0.05f);
+    fill_tables(s);
   }
   if (m->has_dense_fc) {
     int64_t in = m->dense_in;
@@ -205,6 +241,52 @@ int or_forward64(const or_state* s, int64_t S, const float* dense, const int64_t
                  double* out, double* mag, double* pooled, double* pooled_mag) {
   if (!s || S < 1 || !out) return -1;
   return forward_f64(s, S, dense, idx, out, mag, pooled, pooled_mag);
+}
+
+/* Items are independent: the fp64 forward over item chunks on `threads`
+ * pthreads (test-time speed only; each item's arithmetic is unchanged). */
+typedef struct {
+  const or_state* s;
+  int64_t S, chunk;
+  const float* dense;
+  const int64_t* idx;
+  double *out, *mag, *pooled, *pmag;
+  atomic_llong next;
+  atomic_int rc;
+} f64_ctx;
+
+static void* f64_worker(void* p) {
+  f64_ctx* c = (f64_ctx*)p;
+  const or_state* s = c->s;
+  const int64_t ow = or_output_dim(s), pd = s->pooled_dim, TL = s->m.T * s->m.L;
+  for (;;) {
+    const int64_t i0 = atomic_fetch_add(&c->next, c->chunk);
+    if (i0 >= c->S) break;
+    const int64_t n = c->S - i0 < c->chunk ? c->S - i0 : c->chunk;
+    const int rc = forward_f64(s, n, c->dense ? c->dense + i0 * s->m.dense_in : NULL,
+                               c->idx ? c->idx + i0 * TL : NULL, c->out + i0 * ow,
+                               c->mag ? c->mag + i0 * ow : NULL,
+                               c->pooled ? c->pooled + i0 * pd : NULL,
+                               c->pmag ? c->pmag + i0 * pd : NULL);
+    if (rc) atomic_store(&c->rc, rc);
+  }
+  return NULL;
+}
+
+int or_forward64_mt(const or_state* s, int64_t S, const float* dense, const int64_t* idx,
+                    double* out, double* mag, double* pooled, double* pooled_mag, int threads) {
+  if (!s || S < 1 || !out) return -1;
+  if (threads < 1) threads = 1;
+  f64_ctx c;
+  c.s = s; c.S = S; c.chunk = 16;
+  c.dense = dense; c.idx = idx; c.out = out; c.mag = mag; c.pooled = pooled; c.pmag = pooled_mag;
+  atomic_init(&c.next, 0);
+  atomic_init(&c.rc, 0);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, f64_worker, &c);
+  for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+  free(th);
+  return atomic_load(&c.rc);
 }
 
 int or_forward32(const or_state* s, int64_t S, const float* dense, const int64_t* idx,
@@ -300,5 +382,81 @@ int or_bench_queries(const or_state* s, int64_t nq, const int64_t* sizes, int th
   *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
   for (int64_t q = 0; q < nq; ++q) { free(c.dense[q]); free(c.idx[q]); }
   free(c.dense); free(c.idx); free(th);
+  return atomic_load(&c.rc);
+}
+
+/* ---- per-request service times on the host cores ------------------------------
+ * `threads` workers each serve `per_thread` requests of `b` items (inputs
+ * pre-generated), all starting together, so each measured time carries the
+ * memory contention of `threads` active cores — the quantity the
+ * reference's cpu_service_time models (proj/src/platform.cpp:71-97, active
+ * cores sampled at dispatch, proj/src/sim.cpp:114-124). times[threads *
+ * per_thread] receives each request's wall seconds. */
+typedef struct {
+  const or_state* s;
+  int64_t b, per_thread;
+  float** dense;
+  int64_t** idx;
+  double* times;
+  atomic_int ready;
+  int threads;
+  atomic_int rc;
+} req_ctx;
+
+typedef struct {
+  req_ctx* c;
+  int id;
+} req_arg;
+
+static double now_s(void) {
+  struct timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return (double)t.tv_sec + 1e-9 * (double)t.tv_nsec;
+}
+
+static void* req_worker(void* p) {
+  req_arg* a = (req_arg*)p;
+  req_ctx* c = a->c;
+  const int64_t ow = or_output_dim(c->s);
+  float* out = (float*)malloc(sizeof(float) * (size_t)(c->b * ow));
+  atomic_fetch_add(&c->ready, 1);
+  while (atomic_load(&c->ready) < c->threads) {
+  }
+  for (int64_t k = 0; k < c->per_thread; ++k) {
+    const int64_t q = (int64_t)a->id * c->per_thread + k;
+    const double t0 = now_s();
+    const int rc = or_forward32(c->s, c->b, c->dense[q], c->idx[q], out);
+    c->times[q] = now_s() - t0;
+    if (rc) atomic_store(&c->rc, rc);
+  }
+  free(out);
+  return NULL;
+}
+
+int or_time_requests(const or_state* s, int64_t b, int threads, int64_t per_thread, uint64_t seed,
+                     double* times) {
+  if (!s || b < 1 || threads < 1 || per_thread < 1 || !times) return -1;
+  const int64_t nq = (int64_t)threads * per_thread;
+  req_ctx c;
+  c.s = s; c.b = b; c.per_thread = per_thread; c.times = times; c.threads = threads;
+  c.dense = (float**)calloc((size_t)nq, sizeof(float*));
+  c.idx = (int64_t**)calloc((size_t)nq, sizeof(int64_t*));
+  for (int64_t q = 0; q < nq; ++q) {
+    c.dense[q] = (float*)malloc(sizeof(float) * (size_t)(b * s->m.dense_in + 1));
+    c.idx[q] = (int64_t*)malloc(sizeof(int64_t) * (size_t)(b * s->m.T * s->m.L + 1));
+    or_fill_query(&s->m, s->rows, seed, (uint64_t)q, b, c.dense[q], c.idx[q]);
+  }
+  atomic_init(&c.ready, 0);
+  atomic_init(&c.rc, 0);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  req_arg* args = (req_arg*)malloc(sizeof(req_arg) * (size_t)threads);
+  for (int i = 0; i < threads; ++i) {
+    args[i].c = &c;
+    args[i].id = i;
+    pthread_create(&th[i], NULL, req_worker, &args[i]);
+  }
+  for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+  for (int64_t q = 0; q < nq; ++q) { free(c.dense[q]); free(c.idx[q]); }
+  free(c.dense); free(c.idx); free(th); free(args);
   return atomic_load(&c.rc);
 }

@@ -70,6 +70,20 @@ SizeDistribution make_dist(int kind, double p0, double p1, double p2, double p3,
   return d;
 }
 
+// "measured": the box's own cores, priced by the measured per-request table of
+// oracle/ref_cpu_adapter.cpp (linked only into librecsim_ref_cpu.so; weak here).
+extern "C" __attribute__((weak)) int64_t ref_measured_cores(void);
+
+CpuPlatformSpec shim_cpu(const char* name) {
+  if (std::strcmp(name, "measured") == 0 && ref_measured_cores) {
+    CpuPlatformSpec p = builtin_cpu("skylake");  // fields other than cores unused
+    p.name = "measured";
+    p.cores = ref_measured_cores();
+    return p;
+  }
+  return builtin_cpu(name);
+}
+
 // 0 ok, -1 invalid_argument, -2 UnknownModel, -3 ConfigError, -4 InvalidDistribution
 template <class F>
 int guard(F&& f) {
@@ -149,7 +163,7 @@ int ref_simulate_decisions(const or_model* m, const char* cpu, uint64_t seed, do
     SchedulerConfig cfg;
     cfg.batch_size = batch;
     cfg.model = to_spec(*m);
-    cfg.cpu = builtin_cpu(cpu);
+    cfg.cpu = shim_cpu(cpu);
     cfg.warmup_fraction = 0.0;
     if (threshold > 0) {
       cfg.offload_threshold = threshold;
@@ -181,7 +195,7 @@ int ref_max_qps(const or_model* m, const char* cpu, double sla, uint64_t seed, i
     SchedulerConfig cfg;
     cfg.batch_size = batch;
     cfg.model = to_spec(*m);
-    cfg.cpu = builtin_cpu(cpu);
+    cfg.cpu = shim_cpu(cpu);
     if (threshold > 0) {
       cfg.offload_threshold = threshold;
       cfg.accel = builtin_accel("default");
@@ -214,7 +228,7 @@ int ref_max_qps_accel(const or_model* m, const char* cpu, const char* accel, dou
     SchedulerConfig cfg;
     cfg.batch_size = batch;
     cfg.model = to_spec(*m);
-    cfg.cpu = builtin_cpu(cpu);
+    cfg.cpu = shim_cpu(cpu);
     if (threshold > 0) {
       cfg.offload_threshold = threshold;
       cfg.accel = named_accel(accel);
@@ -243,7 +257,7 @@ int ref_tune(const or_model* m, const char* cpu, const char* accel, double sla, 
     tp.seeds_to_average = seeds;
     std::optional<AcceleratorSpec> a;
     if (accel && accel[0]) a = named_accel(accel);
-    TunedConfig t = tune(to_spec(*m), builtin_cpu(cpu), a, sla, tp);
+    TunedConfig t = tune(to_spec(*m), shim_cpu(cpu), a, sla, tp);
     *batch = t.batch_size;
     *threshold = t.offload_threshold ? *t.offload_threshold : 0;
     *qps = t.qps;

@@ -103,6 +103,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 INDEX_I64, INDEX_I32 = 0, 1  # rs_query.index_type (I32: labelled input variant)
 DENSE_BF16 = 2               # rs_query.index_type flag: bf16 dense (labelled variant)
 OPT_MERGE_QUERIES = 1        # rs_accel_set_option (labelled scheduler extension)
+OPT_STAGE_TIMING = 2         # rs_accel_set_option: per-stage event timing of rs_forward
 
 
 class CLayerStack(C.Structure):
@@ -147,7 +148,7 @@ class CQuery(C.Structure):
 
 class CTiming(C.Structure):
     _fields_ = [("h2d_ms", C.c_double), ("compute_ms", C.c_double), ("d2h_ms", C.c_double),
-                ("total_ms", C.c_double), ("embed_ms", C.c_double)]
+                ("total_ms", C.c_double), ("embed_ms", C.c_double), ("fc_ms", C.c_double)]
 
 
 class CAccelInfo(C.Structure):
@@ -191,6 +192,8 @@ _sig("rs_forward", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_void_p, P(CTi
 _sig("rs_pooled", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_void_p, P(CTiming))
 _sig("rs_forward_many", C.c_int, C.c_void_p, C.c_int64, P(CQuery), P(C.c_void_p), C.c_void_p,
      P(C.c_double), P(C.c_double))
+_sig("rs_forward_many_ev", C.c_int, C.c_void_p, C.c_int64, P(CQuery), P(C.c_void_p), C.c_void_p,
+     P(C.c_double), P(C.c_double), C.c_void_p)
 _sig("rs_sync", C.c_int, C.c_void_p, C.c_void_p)
 _sig("rs_accel_set_option", C.c_int, C.c_void_p, C.c_int32, C.c_int64)
 _sig("rs_serve", C.c_int, P(C.c_void_p), C.c_int32, C.c_int64, P(CQuery), P(C.c_double),
@@ -213,7 +216,7 @@ EXPORTED_SYMBOLS = [
     "rs_abi_version", "rs_last_error", "rs_model_builtin", "rs_zoo_names", "rs_model_validate",
     "rs_work", "rs_predict_input_dim", "rs_accel_input_bytes", "rs_sla_target", "rs_route",
     "rs_dist_production", "rs_gen_trace", "rs_qps_under_sla", "rs_accel_create",
-    "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_sync",
+    "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_forward_many_ev", "rs_sync",
     "rs_pooled", "rs_service_time", "rs_host_sls", "rs_host_fc",
     "rs_fill_query", "rs_fill_query_zipf", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
     "rs_device_count", "rs_accel_set_option", "rs_serve"]
@@ -510,6 +513,7 @@ class Timing:
     d2h_ms: float
     total_ms: float
     embed_ms: float = 0.0
+    fc_ms: float = 0.0
 
 
 class Accelerator:
@@ -557,7 +561,7 @@ class Accelerator:
         t = CTiming()
         _check(_lib.rs_forward(self._h, C.byref(q), out_ptr, stream or None,
                                C.byref(t) if timed else None))
-        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms, t.embed_ms) if timed else None
+        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms, t.embed_ms, t.fc_ms) if timed else None
 
     def pooled_ptr(self, size: int, idx_ptr: int, out_ptr: int, location: int,
                    stream: int = 0, timed: bool = False, dense_ptr: int = 0,
@@ -566,7 +570,7 @@ class Accelerator:
         t = CTiming()
         _check(_lib.rs_pooled(self._h, C.byref(q), out_ptr, stream or None,
                               C.byref(t) if timed else None))
-        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms, t.embed_ms) if timed else None
+        return Timing(t.h2d_ms, t.compute_ms, t.d2h_ms, t.total_ms, t.embed_ms, t.fc_ms) if timed else None
 
     @staticmethod
     def batch(sizes, dense_ptrs, idx_ptrs, out_ptrs, location: int, index_type: int = 0):
@@ -582,17 +586,17 @@ class Accelerator:
 
     def forward_many(self, sizes, dense_ptrs=None, idx_ptrs=None, out_ptrs=None,
                      location: int = MEM_DEVICE, stream: int = 0, timed: bool = True,
-                     residence: bool = False, prepared=None):
+                     residence: bool = False, prepared=None, done_event: int = 0):
         """rs_forward_many: n whole queries, FIFO-dispatched over the handle's
         lanes. Returns per-query service times in ms when timed (else None);
         with residence=True returns (service_ms, residence_ms)."""
         n, qs, outs = prepared or self.batch(sizes, dense_ptrs, idx_ptrs, out_ptrs, location)
         svc = np.zeros(n, dtype=np.float64) if timed else None
         lat = np.zeros(n, dtype=np.float64) if (timed and residence) else None
-        _check(_lib.rs_forward_many(self._h, n, qs, outs, stream or None,
-                                    svc.ctypes.data_as(P(C.c_double)) if timed else None,
-                                    lat.ctypes.data_as(P(C.c_double)) if lat is not None
-                                    else None))
+        _check(_lib.rs_forward_many_ev(self._h, n, qs, outs, stream or None,
+                                       svc.ctypes.data_as(P(C.c_double)) if timed else None,
+                                       lat.ctypes.data_as(P(C.c_double)) if lat is not None
+                                       else None, done_event or None))
         return (svc, lat) if residence else svc
 
     def set_option(self, option: int, value: int) -> None:

@@ -19,6 +19,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -91,12 +92,13 @@ struct Slot {
   float* X = nullptr;
   float* pact[2] = {nullptr, nullptr};
   float* out = nullptr;
-  cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};  // GraphKind
+  cudaGraphExec_t graph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // GraphKind
   int kernels[3] = {0, 0, 0};
   int tc_layers = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  // event-record nodes around the embedding kernel in the pool graph
-  cudaEvent_t kev[2] = {nullptr, nullptr};
+  // event-record nodes around the embedding kernel (pool graph and the
+  // stage-timed forward graph) and around the predict stack (stage-timed)
+  cudaEvent_t kev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ready = nullptr, free = nullptr;  // pipelined queue hand-off
   cudaStream_t cap2 = nullptr;                  // capture: parallel graph branch
   // SM-partitioned slots (rs_forward_many lanes when the device is split):
@@ -141,6 +143,7 @@ struct rs_accel {
   static constexpr int kMaxLanes = 16;
   int depth = 2;
   int64_t merge_queries = 1;  // RS_OPT_MERGE_QUERIES (1 = one query per launch)
+  int stage_timing = 0;       // RS_OPT_STAGE_TIMING
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t lane_join[kMaxLanes] = {};
@@ -479,7 +482,8 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
 // kGraphPoolTimed: the pool graph with event-record nodes around the
 // embedding kernel (rs_pooled with timing; the untimed graph stays lean)
 enum GraphKind {
-  kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kGraphPoolTimed = 3, kNumGraphs = 4
+  kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kGraphPoolTimed = 3, kGraphStageTimed = 4,
+  kNumGraphs = 5
 };
 static_assert(kNumGraphs == sizeof(Slot::graph) / sizeof(Slot::graph[0]), "Slot::graph size");
 
@@ -497,7 +501,12 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   const rs_model_desc& m = a->m;
   const int64_t maxS = a->init.max_query_size;
-  const bool tc = kind == kGraphLarge;
+  // kGraphStageTimed: the forward graph of the handle's FC path with
+  // event-record nodes around the embedding stage and around the predict
+  // stack (RS_OPT_STAGE_TIMING; rs_timing.embed_ms / fc_ms)
+  const bool stage_stamp = kind == kGraphStageTimed;
+  const bool tc = kind == kGraphLarge ||
+                  (stage_stamp && a->init.fc_mode != RS_FC_FP32 && tc_available());
   int ntc = 0;
   if (kind == kGraphPool || kind == kGraphPoolTimed) {
     // timestamps of the embedding kernel alone (rs_timing.embed_ms): external
@@ -550,12 +559,14 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
       }
     }
     if (fork && !part) RS_CUDA(cudaEventRecord(s->join, bs));
+    if (stage_stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[0], es, cudaEventRecordExternal));
     if (skip & 8) {
     } else if (m.pooling == RS_POOL_SUM) {
       if (a->T > 0) enqueue_pooling(a, s, s->pooled, a->T * a->D, 0, tc, es);
     } else {
       enqueue_pooling(a, s, s->X, a->ld_x, a->dense_out, tc, es);
     }
+    if (stage_stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[1], es, cudaEventRecordExternal));
     if (fork && part) RS_CUDA(cudaEventRecord(s->join, es));
     if (fork) RS_CUDA(cudaStreamWaitEvent(st, s->join, 0));
     if (m.pooling == RS_POOL_SUM && a->T > 0 && !(skip & 2))
@@ -566,9 +577,11 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
       const char* dc = getenv("RS_DIAG_EMPTY_CTAS");
       launch_diag_empty(atoi(de), dc ? atoi(dc) : 1, st);
     }
+    if (stage_stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[2], st, cudaEventRecordExternal));
     if (!(skip & 4))
       ntc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w,
                            s->out, a->out_w, a->out_dim, tc, st, /*final_to_desc=*/true);
+    if (stage_stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[3], st, cudaEventRecordExternal));
   }
   cudaError_t le = cudaGetLastError();
   cudaError_t ce = cudaStreamEndCapture(st, &g);
@@ -962,6 +975,11 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
 
 cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full, bool timed = false) {
   if (!full) return s->graph[timed ? kGraphPoolTimed : kGraphPool];
+  if (timed && a->stage_timing) {
+    if (!s->graph[kGraphStageTimed])
+      s->graph[kGraphStageTimed] = capture(a, s, kGraphStageTimed, nullptr, nullptr);
+    return s->graph[kGraphStageTimed];
+  }
   cudaGraphExec_t small = s->graph[kGraphSmall], large = s->graph[kGraphLarge];
   (void)S;
   return large ? large : small;
@@ -1019,7 +1037,9 @@ int run(rs_accel* a, const rs_query* q, float* out, void* stream, rs_timing* tim
       timing->compute_ms = elapsed(s->ev[1], s->ev[2]);
       timing->d2h_ms = elapsed(s->ev[2], s->ev[3]);
       timing->total_ms = elapsed(s->ev[0], s->ev[3]);
-      timing->embed_ms = full || a->T == 0 ? 0.0 : elapsed(s->kev[0], s->kev[1]);
+      const bool staged = full && a->stage_timing;
+      timing->embed_ms = a->T == 0 || (full && !staged) ? 0.0 : elapsed(s->kev[0], s->kev[1]);
+      timing->fc_ms = staged ? elapsed(s->kev[2], s->kev[3]) : 0.0;
       collect_errors(s, st);
     }
   });
@@ -1085,7 +1105,7 @@ int64_t stage_group(rs_accel* a, Slot* s, const rs_query* qs, int64_t m, cudaStr
 }
 
 int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, void* stream,
-             double* service_ms, double* latency_ms) {
+             double* service_ms, double* latency_ms, void* done_event = nullptr) {
   return guarded([&] {
     if (!a || !qs || !outs) raise(RS_E_INVALID, "null argument");
     if (n < 1) raise(RS_E_INVALID, "n < 1");
@@ -1209,6 +1229,9 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
       RS_CUDA(cudaEventRecord(a->lane_join[d], a->lane[d]));
       RS_CUDA(cudaStreamWaitEvent(st, a->lane_join[d], 0));
     }
+    // the caller's completion stamp: recorded once every query finished, so
+    // it excludes the host's timestamp harvest below
+    if (done_event) RS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(done_event), st));
     if (const char* tr = getenv("RS_TRACE_ENQUEUE")) {
       if (atoi(tr))
         fprintf(stderr, "rs_forward_many: n=%lld enqueue %.3f ms (%.2f us/query)\n",
@@ -1249,6 +1272,10 @@ extern "C" int rs_accel_set_option(rs_accel* a, int32_t option, int64_t value) {
         if (value < 1 || value > kMaxGroup)
           raise(RS_E_INVALID, "merge_queries must be in [1, 64]");
         a->merge_queries = value;
+        break;
+      case RS_OPT_STAGE_TIMING:
+        if (value != 0 && value != 1) raise(RS_E_INVALID, "stage_timing must be 0 or 1");
+        a->stage_timing = (int)value;
         break;
       default:
         raise(RS_E_INVALID, "unknown option");
@@ -1390,12 +1417,44 @@ extern "C" int rs_forward_many(rs_accel* a, int64_t n, const rs_query* queries,
   return run_many(a, n, queries, outs, stream, service_ms, latency_ms);
 }
 
-// Real-time executor: queries are released at their arrival
-// times (host clock), each to the replica with the least outstanding items
-// (ties to the lowest index — the K-server pool of §8e), and served on that
-// replica's lanes exactly as in rs_forward_many. latency = completion (CUDA
-// event on the replica, relative to a start event recorded at t0) minus the
-// arrival offset: queueing + service as a client would see it.
+extern "C" int rs_forward_many_ev(rs_accel* a, int64_t n, const rs_query* queries,
+                                  float* const* outs, void* stream, double* service_ms,
+                                  double* latency_ms, void* done_event) {
+  return run_many(a, n, queries, outs, stream, service_ms, latency_ms, done_event);
+}
+
+// Real-time executor: the reference's single FIFO accelerator
+// server (accel_busy + accel_fifo, proj/src/sim.cpp:95-97, 126-136)
+// generalised to a K-replica pool. The calling thread releases query i at
+// t0 + arrival_s[i] (host clock) and routes it to the replica with the least
+// outstanding items (ties to the lowest index); one dispatcher
+// thread per replica stages, launches and retires that replica's queries on
+// its lanes exactly as rs_forward_many does, so host dispatch cost scales
+// with the replica count instead of serialising on one thread. Outstanding
+// item counts are atomics: the releaser adds on assignment, the replica's
+// dispatcher subtracts when the query's completion event has fired.
+// latency = completion (CUDA event on the replica, relative to a start event
+// recorded at t0) minus the arrival offset: queueing + service.
+namespace rs {
+namespace {
+
+struct ServeRep {
+  rs_accel* a = nullptr;
+  Slot* p[rs_accel::kMaxLanes] = {};
+  std::atomic<int64_t> outstanding{0};
+  // assignment ring (releaser -> dispatcher), single producer/consumer
+  std::vector<int64_t> queue;
+  std::atomic<int64_t> head{0}, tail{0};
+  std::deque<std::pair<int64_t, int64_t>> inflight;  // (query, replica-local seq)
+  int64_t issued = 0;
+  int64_t dispatched = 0;
+};
+
+constexpr int64_t kServeRing = 4096;
+
+}  // namespace
+}  // namespace rs
+
 extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_query* qs,
                         const double* arrival_s, float* const* outs, double* latency_ms) {
   std::vector<std::unique_lock<std::mutex>> locks;
@@ -1412,62 +1471,114 @@ extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_qu
       if (!(arrival_s[i] >= 0) || (i && arrival_s[i] < arrival_s[i - 1]))
         raise(RS_E_INVALID, "arrival times must be non-negative and non-decreasing");
     }
-    constexpr int64_t kRing = 4096;
-    struct Rep {
-      rs_accel* a;
-      Slot* p[rs_accel::kMaxLanes];
-      int64_t issued = 0, outstanding = 0;
-      std::deque<std::pair<int64_t, int64_t>> inflight;  // (query, replica-local seq)
-      std::vector<int64_t> who;                            // ring slot -> query
-    };
     // queue locks in address order (two concurrent callers can never deadlock)
     std::vector<rs_accel*> order(reps, reps + k);
     std::sort(order.begin(), order.end());
     order.erase(std::unique(order.begin(), order.end()), order.end());
     if ((int)order.size() != k) raise(RS_E_INVALID, "a replica appears twice");
     for (rs_accel* a : order) locks.emplace_back(a->many_mu);
-    std::vector<Rep> R((size_t)k);
+    std::vector<std::unique_ptr<ServeRep>> R;
     for (int r = 0; r < k; ++r) {
+      auto rp = std::make_unique<ServeRep>();
       rs_accel* a = reps[r];
       RS_CUDA(cudaSetDevice(a->device));
-      R[r].a = a;
-      for (int d = 0; d < a->depth; ++d) R[r].p[d] = get_pipe_slot(a, d);
-      while ((int64_t)a->evpool.size() < kRing + 1) {
+      rp->a = a;
+      for (int d = 0; d < a->depth; ++d) rp->p[d] = get_pipe_slot(a, d);
+      while ((int64_t)a->evpool.size() < kServeRing + 1) {
         cudaEvent_t e;
         RS_CUDA(cudaEventCreate(&e));
         a->evpool.push_back(e);
       }
-      R[r].who.assign(kRing, -1);
+      rp->queue.assign((size_t)n, -1);
+      R.push_back(std::move(rp));
     }
     std::vector<double> done_ms((size_t)n, -1.0);
-    std::vector<int> rep_of((size_t)n, 0);
-    auto retire = [&](Rep& rp, bool block) {
-      while (!rp.inflight.empty()) {
-        const auto [qi, seq] = rp.inflight.front();
-        cudaEvent_t e = rp.a->evpool[1 + seq % kRing];
-        if (block) {
-          RS_CUDA(cudaEventSynchronize(e));
-        } else {
-          const cudaError_t st = cudaEventQuery(e);
-          if (st == cudaErrorNotReady) break;
-          if (st != cudaSuccess) RS_CUDA(st);
-        }
-        done_ms[(size_t)qi] = elapsed(rp.a->evpool[0], e);
-        rp.outstanding -= qs[qi].size;
-        rp.inflight.pop_front();
-      }
-    };
     // t0: a start event on every replica, then release queries on the clock
     for (auto& rp : R) {
-      RS_CUDA(cudaSetDevice(rp.a->device));
-      RS_CUDA(cudaEventRecord(rp.a->evpool[0], rp.a->own));
-      RS_CUDA(cudaEventRecord(rp.a->copy_gate, rp.a->own));
-      for (int d = 0; d < rp.a->depth; ++d)
-        RS_CUDA(cudaStreamWaitEvent(rp.a->lane[d], rp.a->copy_gate, 0));
-      RS_CUDA(cudaStreamWaitEvent(rp.a->copy, rp.a->copy_gate, 0));
+      rs_accel* a = rp->a;
+      RS_CUDA(cudaSetDevice(a->device));
+      RS_CUDA(cudaEventRecord(a->evpool[0], a->own));
+      RS_CUDA(cudaEventRecord(a->copy_gate, a->own));
+      for (int d = 0; d < a->depth; ++d) RS_CUDA(cudaStreamWaitEvent(a->lane[d], a->copy_gate, 0));
+      RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
+      RS_CUDA(cudaStreamSynchronize(a->own));
     }
+    std::atomic<bool> released_all{false};
+    std::atomic<int> failed{0};
+    std::mutex err_mu;
+    Error first_err{RS_OK, ""};
+    auto record_error = [&](const Error& e) {
+      std::lock_guard<std::mutex> g(err_mu);
+      if (!failed.exchange(1)) first_err = e;
+    };
+    // one dispatcher per replica
+    auto dispatcher = [&](ServeRep* rp) {
+      try {
+        rs_accel* a = rp->a;
+        RS_CUDA(cudaSetDevice(a->device));
+        auto retire = [&](bool block) {
+          while (!rp->inflight.empty()) {
+            const auto [qi, seq] = rp->inflight.front();
+            cudaEvent_t e = a->evpool[1 + seq % kServeRing];
+            if (block) {
+              RS_CUDA(cudaEventSynchronize(e));
+            } else {
+              const cudaError_t st = cudaEventQuery(e);
+              if (st == cudaErrorNotReady) break;
+              if (st != cudaSuccess) RS_CUDA(st);
+            }
+            done_ms[(size_t)qi] = elapsed(a->evpool[0], e);
+            rp->outstanding.fetch_sub(qs[qi].size, std::memory_order_relaxed);
+            rp->inflight.pop_front();
+          }
+        };
+        for (;;) {
+          if (failed.load(std::memory_order_relaxed)) return;
+          const int64_t h = rp->head.load(std::memory_order_acquire);
+          if (rp->dispatched == h) {
+            retire(false);
+            if (released_all.load(std::memory_order_acquire) &&
+                rp->dispatched == rp->head.load(std::memory_order_acquire))
+              break;
+            std::this_thread::yield();
+            continue;
+          }
+          const int64_t i = rp->queue[(size_t)rp->dispatched++];
+          const int64_t seq = rp->issued++;
+          if (seq >= kServeRing)  // event-ring reuse: that query must have retired
+            while (!rp->inflight.empty() && rp->inflight.front().second <= seq - kServeRing)
+              retire(true);
+          const int d = (int)(seq % a->depth);
+          Slot* sl = rp->p[d];
+          cudaStream_t ls = a->lane[d];
+          if (loc == RS_MEM_HOST) {
+            RS_CUDA(cudaStreamWaitEvent(a->copy, sl->free, 0));
+            stage_inputs(a, sl, &qs[i], true, a->copy, nullptr, /*widen_later=*/true);
+            RS_CUDA(cudaEventRecord(sl->ready, a->copy));
+            RS_CUDA(cudaStreamWaitEvent(ls, sl->ready, 0));
+            widen_indices(a, sl, &qs[i], ls);
+          } else {
+            stage_inputs(a, sl, &qs[i], true, ls, outs[i]);
+          }
+          launch_stage(a, sl, &qs[i], outs[i], true, ls);
+          RS_CUDA(cudaEventRecord(sl->free, ls));
+          RS_CUDA(cudaEventRecord(a->evpool[1 + seq % kServeRing], ls));
+          rp->inflight.emplace_back(i, seq);
+          retire(false);
+        }
+        retire(true);
+        for (int d = 0; d < a->depth; ++d) collect_errors(rp->p[d], a->lane[d]);
+      } catch (const Error& e) {
+        record_error(e);
+      } catch (const std::exception& e) {
+        record_error(Error{RS_E_INVALID, e.what()});
+      }
+    };
+    std::vector<std::thread> th;
+    th.reserve((size_t)k);
+    for (auto& rp : R) th.emplace_back(dispatcher, rp.get());
     const auto t0 = std::chrono::steady_clock::now();
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = 0; i < n && !failed.load(std::memory_order_relaxed); ++i) {
       const auto due = t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
                                 std::chrono::duration<double>(arrival_s[i]));
       for (;;) {
@@ -1477,41 +1588,21 @@ extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_qu
           std::this_thread::sleep_for(std::chrono::microseconds(50));
       }
       int best = 0;
-      for (int r = 0; r < k; ++r) {
-        retire(R[r], false);
-        if (R[r].outstanding < R[best].outstanding) best = r;
+      int64_t best_out = R[0]->outstanding.load(std::memory_order_relaxed);
+      for (int r = 1; r < k; ++r) {
+        const int64_t o = R[r]->outstanding.load(std::memory_order_relaxed);
+        if (o < best_out) { best = r; best_out = o; }
       }
-      Rep& rp = R[best];
-      rs_accel* a = rp.a;
-      RS_CUDA(cudaSetDevice(a->device));
-      const int64_t seq = rp.issued++;
-      if (seq >= kRing) {  // ring slot reuse: its query must have retired
-        while (!rp.inflight.empty() && rp.inflight.front().second <= seq - kRing) retire(rp, true);
-      }
-      const int d = (int)(seq % a->depth);
-      Slot* sl = rp.p[d];
-      cudaStream_t ls = a->lane[d];
-      if (loc == RS_MEM_HOST) {
-        RS_CUDA(cudaStreamWaitEvent(a->copy, sl->free, 0));
-        stage_inputs(a, sl, &qs[i], true, a->copy, nullptr, /*widen_later=*/true);
-        RS_CUDA(cudaEventRecord(sl->ready, a->copy));
-        RS_CUDA(cudaStreamWaitEvent(ls, sl->ready, 0));
-        widen_indices(a, sl, &qs[i], ls);
-      } else {
-        stage_inputs(a, sl, &qs[i], true, ls, outs[i]);
-      }
-      launch_stage(a, sl, &qs[i], outs[i], true, ls);
-      RS_CUDA(cudaEventRecord(sl->free, ls));
-      RS_CUDA(cudaEventRecord(a->evpool[1 + seq % kRing], ls));
-      rp.inflight.emplace_back(i, seq);
-      rp.outstanding += qs[i].size;
-      rep_of[(size_t)i] = best;
+      ServeRep* rp = R[best].get();
+      rp->outstanding.fetch_add(qs[i].size, std::memory_order_relaxed);
+      const int64_t t = rp->tail.load(std::memory_order_relaxed);
+      rp->queue[(size_t)t] = i;
+      rp->tail.store(t + 1, std::memory_order_relaxed);
+      rp->head.store(t + 1, std::memory_order_release);
     }
-    for (auto& rp : R) {
-      RS_CUDA(cudaSetDevice(rp.a->device));
-      retire(rp, true);
-      for (int d = 0; d < rp.a->depth; ++d) collect_errors(rp.p[d], rp.a->lane[d]);
-    }
+    released_all.store(true, std::memory_order_release);
+    for (auto& t : th) t.join();
+    if (failed.load()) raise(first_err.code, first_err.msg);
     for (int64_t i = 0; i < n; ++i) latency_ms[i] = done_ms[(size_t)i] - arrival_s[i] * 1e3;
   });
 }

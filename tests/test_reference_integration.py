@@ -12,9 +12,9 @@ import paper_2001_02772_b200 as rs
 
 
 def _libs(orc):
-    if orc.ref is None or orc.ref_b200 is None:
+    if orc.ref is None or orc.load_ref_b200() is None:
         pytest.skip("oracle/_ref libraries not built (no /root/reference here)")
-    return orc.ref, orc.ref_b200
+    return orc.ref, orc.load_ref_b200()
 
 
 def test_wrapped_library_keeps_reference_behaviour_for_other_specs(orc):

@@ -36,24 +36,24 @@ def main():
            "n": args.n, "batch": 64, "models": []}
     for name in args.models.split(","):
         spec = rs.builtin_model(name)
-        if orc.ref_b200 is None:
+        if orc.load_ref_b200() is None:
             print(json.dumps({"error": "oracle/_ref/librecsim_ref_b200.so not built"}))
             return
         sla = rs.sla_target(name, "medium")
         row = {"model": name, "sla_s": sla, "sweep": []}
         for T in [int(x) for x in args.thresholds.split(",")]:
             cpu_only = T == 0
-            b200 = orc.ref_max_qps(orc.ref_b200, spec, "b200", args.cpu, sla, dist, args.n, 64,
+            b200 = orc.ref_max_qps(orc.load_ref_b200(), spec, "b200", args.cpu, sla, dist, args.n, 64,
                                    0 if cpu_only else T)
-            modeled = orc.ref_max_qps(orc.ref_b200, spec, "default", args.cpu, sla, dist, args.n,
+            modeled = orc.ref_max_qps(orc.load_ref_b200(), spec, "default", args.cpu, sla, dist, args.n,
                                       64, 0 if cpu_only else T)
             row["sweep"].append({"threshold": T, "qps_b200": b200[0], "p95_b200": b200[1],
                                  "accel_work_fraction_b200": b200[2], "qps_modeled_gpu": modeled[0],
                                  "accel_work_fraction_modeled": modeled[2]})
-        row["tune_cpu_only"] = orc.ref_tune(orc.ref_b200, spec, "", args.cpu, sla, dist, args.n)
-        row["tune_modeled_gpu"] = orc.ref_tune(orc.ref_b200, spec, "default", args.cpu, sla, dist,
+        row["tune_cpu_only"] = orc.ref_tune(orc.load_ref_b200(), spec, "", args.cpu, sla, dist, args.n)
+        row["tune_modeled_gpu"] = orc.ref_tune(orc.load_ref_b200(), spec, "default", args.cpu, sla, dist,
                                                args.n)
-        row["tune_b200"] = orc.ref_tune(orc.ref_b200, spec, "b200", args.cpu, sla, dist, args.n)
+        row["tune_b200"] = orc.ref_tune(orc.load_ref_b200(), spec, "b200", args.cpu, sla, dist, args.n)
         res["models"].append(row)
         print(json.dumps({"model": name, "tune_cpu_only_qps": row["tune_cpu_only"]["qps"],
                           "tune_modeled_gpu_qps": row["tune_modeled_gpu"]["qps"],
