@@ -327,6 +327,16 @@ int rs_pooled(rs_accel* a, const rs_query* q, float* out, void* stream,
  * host-staged synthetic inputs, H2D + forward + D2H, median of 5 runs.     */
 int rs_service_time(rs_accel* a, int64_t query_size, double* seconds);
 
+/* Measured counterpart of the whole recsim::ServiceTime (platform.hpp:60-68)
+ * for S items: *total (seconds, median of 5 timed host-staged queries),
+ * *transfer (H2D + D2H of those queries) and per_category[RS_NUM_OP_CATEGORIES]
+ * (the compute time total - transfer, split from measured stage times —
+ * embedding stage, predict stack, remaining dense work — and within a stage
+ * by the categories' B200 roofline weights from work(); sums to the compute
+ * time, as the reference's apportioning does, platform.cpp:121-134).        */
+int rs_service_breakdown(rs_accel* a, int64_t query_size, double* total,
+                         double* transfer, double* per_category);
+
 /* Synthetic query inputs: dense U(-1,1), indices uniform in
  * [0, rows_per_table), a pure function of (seed, query_id).                */
 int rs_fill_query(const rs_model_desc* m, int64_t rows_per_table,

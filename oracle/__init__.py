@@ -210,6 +210,19 @@ _TUNE_ARGTYPES = [
 def _bind_accel(lib_):
     lib_.ref_max_qps_accel.argtypes = _ACCEL_ARGTYPES
     lib_.ref_tune.argtypes = _TUNE_ARGTYPES
+    lib_.ref_accel_service_time_named.argtypes = [P(OrModel), C.c_char_p, C.c_int64,
+                                                  P(C.c_double), P(C.c_double), P(C.c_double)]
+
+
+def ref_accel_service_time(lib_, spec, accel: str, S: int):
+    """The reference accel_service_time on a named accelerator: (rc, total,
+    transfer, per_category[7]); rc = the shim's exception code (0 ok, -1
+    std::invalid_argument, -2 UnknownModel, -3 ConfigError, -99 other)."""
+    t, x = C.c_double(), C.c_double()
+    pc = (C.c_double * 7)()
+    rc = lib_.ref_accel_service_time_named(C.byref(model_to_or(spec)), accel.encode(), S,
+                                           C.byref(t), C.byref(x), pc)
+    return rc, t.value, x.value, list(pc)
 
 
 if ref is not None:

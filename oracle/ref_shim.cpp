@@ -219,6 +219,19 @@ static AcceleratorSpec named_accel(const char* name) {
   return a;
 }
 
+// accel_service_time (platform.cpp:113-136) on a named accelerator: the whole
+// ServiceTime (total, transfer, per-category) — through the B200 adapter for
+// "b200" in librecsim_ref_b200.so. Exceptions map to the guard() codes.
+int ref_accel_service_time_named(const or_model* m, const char* accel, int64_t S, double* total,
+                                 double* transfer, double* per_category) {
+  return guard([&] {
+    ServiceTime st = accel_service_time(to_spec(*m), S, named_accel(accel));
+    *total = st.total;
+    *transfer = st.transfer;
+    for (int c = 0; c < kNumOpCategories; ++c) per_category[c] = st.per_category[c];
+  });
+}
+
 // max_qps_under_sla (sim.cpp:246-290) with a named accelerator at threshold T.
 int ref_max_qps_accel(const or_model* m, const char* cpu, const char* accel, double sla,
                       uint64_t seed, int kind, double p0, double p1, double p2, double p3,

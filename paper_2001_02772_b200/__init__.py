@@ -199,6 +199,8 @@ _sig("rs_accel_set_option", C.c_int, C.c_void_p, C.c_int32, C.c_int64)
 _sig("rs_serve", C.c_int, P(C.c_void_p), C.c_int32, C.c_int64, P(CQuery), P(C.c_double),
      P(C.c_void_p), P(C.c_double))
 _sig("rs_service_time", C.c_int, C.c_void_p, C.c_int64, P(C.c_double))
+_sig("rs_service_breakdown", C.c_int, C.c_void_p, C.c_int64, P(C.c_double), P(C.c_double),
+     P(C.c_double))
 _sig("rs_host_sls", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
      C.c_int64, C.c_void_p, C.c_void_p, C.c_int32)
 _sig("rs_host_fc", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
@@ -217,7 +219,7 @@ EXPORTED_SYMBOLS = [
     "rs_work", "rs_predict_input_dim", "rs_accel_input_bytes", "rs_sla_target", "rs_route",
     "rs_dist_production", "rs_gen_trace", "rs_qps_under_sla", "rs_accel_create",
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_forward_many_ev", "rs_sync",
-    "rs_pooled", "rs_service_time", "rs_host_sls", "rs_host_fc",
+    "rs_pooled", "rs_service_time", "rs_service_breakdown", "rs_host_sls", "rs_host_fc",
     "rs_fill_query", "rs_fill_query_zipf", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
     "rs_device_count", "rs_accel_set_option", "rs_serve"]
 
@@ -630,6 +632,15 @@ class Accelerator:
         self.pooled_ptr(S, idx.ctypes.data, out.ctypes.data, MEM_HOST, timed=True,
                         index_type=INDEX_I32 if i32 else INDEX_I64)
         return out
+
+    def service_breakdown(self, query_size: int) -> dict:
+        """rs_service_breakdown: the measured recsim::ServiceTime (seconds):
+        total, transfer and the per-category split of the compute time."""
+        tot, tr = C.c_double(), C.c_double()
+        pc = (C.c_double * NUM_OP_CATEGORIES)()
+        _check(_lib.rs_service_breakdown(self._h, query_size, C.byref(tot), C.byref(tr), pc))
+        return {"total": tot.value, "transfer": tr.value,
+                "per_category": dict(zip(OP_CATEGORIES, list(pc)))}
 
     def service_time(self, query_size: int) -> float:
         """Measured whole-query seconds, memoised per size (sim.cpp:81-88)."""

@@ -1665,3 +1665,78 @@ extern "C" int rs_service_time(rs_accel* a, int64_t query_size, double* seconds)
     *seconds = med;
   });
 }
+
+// Measured ServiceTime breakdown (recsim::ServiceTime, platform.hpp:60-68):
+// total and transfer (H2D + D2H) from the timed whole-query call, and the
+// compute part split over the operator categories the way the reference
+// apportions its roofline (platform.cpp:121-134) — but from MEASURED stage
+// times: the embedding stage (EmbeddingLookup / Pooling / Attention /
+// Recurrent), the predict stack (PredictFC), and the rest of the compute
+// (DenseFC / Interaction, what is not hidden under the gather); inside a
+// stage by the categories' B200 roofline weights from work().
+extern "C" int rs_service_breakdown(rs_accel* a, int64_t query_size, double* total,
+                                    double* transfer, double* per_category) {
+  return guarded([&] {
+    if (!a || !total || !transfer || !per_category) raise(RS_E_INVALID, "null argument");
+    if (query_size < 1) raise(RS_E_INVALID, "query_size < 1");
+    const int64_t S = query_size;
+    const size_t dense_b = (size_t)(S * a->dense_in * 4 + 15) / 16 * 16;
+    const size_t idx_b = (size_t)(S * a->T * a->L * 8);
+    void *in = nullptr, *out = nullptr;
+    RS_CUDA(cudaHostAlloc(&in, std::max<size_t>(dense_b + idx_b, 16), 0));
+    RS_CUDA(cudaHostAlloc(&out, (size_t)(S * a->out_w * 4), 0));
+    void* dense = in;
+    void* idx = static_cast<uint8_t*>(in) + dense_b;
+    std::vector<double> tt, tx, te, tf;
+    int rc = rs_fill_query(&a->m, a->init.rows_per_table, a->init.seed ^ 0x5E41CEull, 0, S,
+                           static_cast<float*>(dense), static_cast<int64_t*>(idx));
+    const int saved = a->stage_timing;
+    for (int pass = 0; rc == RS_OK && pass < 2; ++pass) {
+      // pass 0: the lean graph (total, transfer); pass 1: the stage-timed copy
+      a->stage_timing = pass;
+      for (int i = 0; rc == RS_OK && i < 6; ++i) {
+        rs_query q{S, static_cast<float*>(dense), static_cast<int64_t*>(idx), RS_MEM_HOST, 0};
+        rs_timing tm{};
+        rc = rs_forward(a, &q, static_cast<float*>(out), nullptr, &tm);
+        if (i == 0) continue;
+        if (pass == 0) {
+          tt.push_back(tm.total_ms * 1e-3);
+          tx.push_back((tm.h2d_ms + tm.d2h_ms) * 1e-3);
+        } else {
+          te.push_back(tm.embed_ms * 1e-3);
+          tf.push_back(tm.fc_ms * 1e-3);
+        }
+      }
+    }
+    a->stage_timing = saved;
+    cudaFreeHost(in);
+    cudaFreeHost(out);
+    if (rc != RS_OK) raise(rc, rs_last_error());
+    auto med = [](std::vector<double> v) {
+      std::sort(v.begin(), v.end());
+      return v[v.size() / 2];
+    };
+    const double T = med(tt), X = std::min(med(tx), T), E = med(te), F = med(tf);
+    const double compute = T - X;
+    const rs_work_breakdown wb = work(a->m, S);
+    // B200 roofline weight of a category: max(flops / tf32 rate, bytes / HBM)
+    auto weight = [&](int c) { return std::max(wb.flops[c] / 854e12, wb.bytes[c] / 6.5e12); };
+    double stage[3] = {E, F, std::max(0.0, compute - E - F)};
+    const int cats[3][4] = {{RS_OP_EMBEDDING_LOOKUP, RS_OP_POOLING, RS_OP_ATTENTION, RS_OP_RECURRENT},
+                            {RS_OP_PREDICT_FC, -1, -1, -1},
+                            {RS_OP_DENSE_FC, RS_OP_INTERACTION, -1, -1}};
+    double pc[RS_NUM_OP_CATEGORIES] = {};
+    double sum = 0;
+    for (int g = 0; g < 3; ++g) {
+      double wsum = 0;
+      for (int c : cats[g]) if (c >= 0) wsum += weight(c);
+      for (int c : cats[g])
+        if (c >= 0 && wsum > 0) pc[c] = stage[g] * weight(c) / wsum;
+    }
+    for (double v : pc) sum += v;
+    for (int c = 0; c < RS_NUM_OP_CATEGORIES; ++c)
+      per_category[c] = sum > 0 ? pc[c] * compute / sum : 0.0;  // sums to the compute time
+    *total = T;
+    *transfer = X;
+  });
+}

@@ -591,3 +591,19 @@ def test_embed_kernel_timing():
                         timed=True)
     assert f.embed_ms == 0.0 and f.compute_ms > 0
     acc.close()
+
+
+def test_service_breakdown_is_a_measured_service_time():
+    """rs_service_breakdown: the whole recsim::ServiceTime measured — total,
+    transfer (H2D + D2H) and per-category compute summing to total - transfer,
+    with the embedding categories carrying the SLS-bound model's time."""
+    spec = rs.builtin_model("DLRM-RMC2")
+    acc = rs.Accelerator(spec, 200_000, seed=2, max_query_size=512, fc_mode=rs.FC_AUTO)
+    b = acc.service_breakdown(300)
+    pc = b["per_category"]
+    assert 0 < b["transfer"] < b["total"] < 0.1
+    assert abs(sum(pc.values()) - (b["total"] - b["transfer"])) <= 1e-9 + 1e-6 * b["total"]
+    assert all(v >= 0 for v in pc.values())
+    assert pc["EmbeddingLookup"] > pc["DenseFC"] and pc["PredictFC"] > 0
+    assert pc["Attention"] == 0 and pc["Recurrent"] == 0
+    acc.close()

@@ -52,3 +52,29 @@ def test_deeprecsched_tunes_b200_thresholds(orc):
     assert cpu["threshold"] == 0
     assert b200["threshold"] > 0 and b200["qps"] >= cpu["qps"]
     assert math.isfinite(b200["p95"]) and b200["p95"] <= 0.1
+
+
+@pytest.mark.gpu
+def test_adapter_returns_whole_service_time_and_reference_exceptions(orc):
+    """The adapter answers the reference's accel_service_time with the whole
+    measured ServiceTime (total, transfer, per-category compute summing to
+    total - transfer) and maps RS_E_* failures to the reference's exception
+    types: a query above the handle's 1000-item capacity (RS_E_CAPACITY) is a
+    std::invalid_argument (shim code -1), as S < 1 is in the reference
+    (platform.cpp:115). Two inline specs with the same name but different
+    shapes get different handles (keyed by shape)."""
+    _, ref_b200 = _libs(orc)
+    spec = rs.builtin_model("DLRM-RMC3")
+    rc, total, transfer, pc = orc.ref_accel_service_time(ref_b200, spec, "b200", 200)
+    assert rc == 0 and 0 < transfer < total < 0.1
+    assert abs(sum(pc) - (total - transfer)) <= 1e-9 + 1e-6 * total
+    assert orc.ref_accel_service_time(ref_b200, spec, "b200", 1001)[0] == -1
+    assert orc.ref_accel_service_time(ref_b200, spec, "b200", 0)[0] == -1
+    # the modeled accelerator still takes the reference's own path
+    rc, total_d, transfer_d, _ = orc.ref_accel_service_time(ref_b200, spec, "default", 200)
+    assert rc == 0 and transfer_d > 0
+    other = rs.ModelSpec("DLRM-RMC3", dense_fc=rs.LayerStack([64, 32]),
+                         predict_fc=rs.LayerStack([64, 1]),
+                         embeddings=rs.EmbeddingConfig(4, 5, 32, "Sum"), dense_input_dim=16)
+    rc2, total2, _, _ = orc.ref_accel_service_time(ref_b200, other, "b200", 200)
+    assert rc2 == 0 and total2 != total  # a different shape, its own handle
