@@ -104,6 +104,14 @@ def sla_for(args, zoo_name, sla_target):
     return 0.100 if args.workload.startswith("cfg5") else sla_target(zoo_name, "medium")
 
 
+def size_dist(args):
+    """(p0, p1, kind) of the query-size distribution for the reference's
+    tune(): LogNormal(ln m, 0.5), or Fixed(N) with --size-fixed."""
+    if args.size_fixed:
+        return float(args.size_fixed), 0.0, 0
+    return math.log(args.size_median), 0.5, 2
+
+
 def window(k, Q):
     base = (k % 2) * Q
     return range(base, base + Q)
@@ -121,8 +129,10 @@ def make_config(args, name, shape, rows, sizes, world, sla):
         "workload": args.workload, "model": name, "rows_per_table": rows,
         "tables": T, "lookups": L, "dim": D, "queries_per_step": Q,
         "items_per_step": items_step, "sla_s": sla,
-        "size_distribution": f"LogNormal(ln {args.size_median:g}, 0.5) clamped to "
-                             f"[1, {args.max_query}] (SURVEY 8d (i))",
+        "size_distribution": (f"Fixed({args.size_fixed}) (configs[3] batch sweep)"
+                              if args.size_fixed else
+                              f"LogNormal(ln {args.size_median:g}, 0.5) clamped to "
+                              f"[1, {args.max_query}] (SURVEY 8d (i))"),
         "fc_path": args.fc, "parallelism": f"replicas{world}",
         "input_format": ("LABELLED variant (SURVEY 8f-2), not the reference byte model: " +
                          " + ".join((["int32 indices"] if i32 else []) +
@@ -308,7 +318,7 @@ def cpu_deeprecsched(args, workload, sla, rounds, budget_s, threads=0, rank=0):
     arm = cpu_arm.CpuDeepRecSched(m, rows, threads=threads)
     walls = [arm.sample(budget_s) for _ in range(rounds)]
     t0 = time.time()
-    res = arm.tune(sla, math.log(args.size_median), 0.5, n=50_000, seed=rank_seed(rank),
+    res = arm.tune(sla, *size_dist(args)[:2], kind=size_dist(args)[2], n=50_000, seed=rank_seed(rank),
                    max_size=args.max_query)
     res["tune_s"] = time.time() - t0
     res["fill_s"] = arm.fill_s
@@ -340,9 +350,12 @@ def run_reference(args, rank, world):
     from oracle import cpu_arm
     m, rows, zoo_name = workload_or_model(args.workload)
     sla = sla_for(args, zoo_name, cpu_arm.sla_target)
-    sizes = np.minimum(cpu_arm.gen_trace_sizes(rank_seed(0), math.log(args.size_median), 0.5,
-                                               2 * args.queries_per_step, args.max_query),
-                       args.max_query)
+    if args.size_fixed:
+        sizes = np.full(2 * args.queries_per_step, args.size_fixed, dtype=np.int64)
+    else:
+        sizes = cpu_arm.gen_trace_sizes(rank_seed(0), math.log(args.size_median), 0.5,
+                                        2 * args.queries_per_step, args.max_query)
+    sizes = np.minimum(sizes, args.max_query)
     name = m.name.decode()
     cfg = make_config(args, name, (m.T, m.L, m.D, m.dense_in), rows, sizes, world, sla)
     # every round is a bounded sample; warm-up rounds are discarded
@@ -352,7 +365,7 @@ def run_reference(args, rank, world):
         arm.sample(budget)
     arm.samples = {b: ([], []) for b in cpu_arm.REQUEST_SIZES}
     walls = [arm.sample(budget) for _ in range(args.steps)]
-    res = arm.tune(sla, math.log(args.size_median), 0.5, n=50_000, seed=rank_seed(0),
+    res = arm.tune(sla, *size_dist(args)[:2], kind=size_dist(args)[2], n=50_000, seed=rank_seed(0),
                    max_size=args.max_query)
     bs, t1, tc = arm.table()
     res.update(fill_s=arm.fill_s, threads=arm.threads, rows=rows,
@@ -393,8 +406,11 @@ def run_ours(args, rank, world, local):
     sla = sla_for(args, zoo_name, rs.sla_target)
     Q, K, W = args.queries_per_step, args.steps, args.warmup
     seed = rank_seed(rank)
-    _, sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(math.log(args.size_median), 0.5),
-                            2 * Q)
+    if args.size_fixed:
+        sizes = np.full(2 * Q, args.size_fixed, dtype=np.int64)
+    else:
+        _, sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
+            math.log(args.size_median), 0.5), 2 * Q)
     sizes = np.minimum(sizes, args.max_query)
     acc = rs.Accelerator(spec, rows, seed=1, device=local, max_query_size=args.max_query,
                          fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc],
@@ -677,20 +693,36 @@ def run_serve(args):
     _, pool_sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
         math.log(args.size_median), 0.5), P)
     pool_sizes = np.minimum(pool_sizes, args.max_query)
-    bufs = []
+    device_inputs = args.serve_inputs == "device"
+    if device_inputs and K > 1:
+        raise SystemExit("--serve-inputs device needs --gpus 1 (a query may go to any replica)")
+    bufs, dbufs = [], []
     for q in range(P):
         dn, ix = rs.fill_query(spec, rows, seed, q, int(pool_sizes[q]))
+        if device_inputs:
+            import torch
+            dbufs.append((torch.from_numpy(dn).cuda(0), torch.from_numpy(ix).cuda(0)))
+            continue
         hb = rs.PinnedBuffer(dn.nbytes + ix.nbytes)
         raw = hb.view(np.uint8, (dn.nbytes + ix.nbytes,))
         raw[:dn.nbytes] = dn.reshape(-1).view(np.uint8)
         raw[dn.nbytes:] = ix.reshape(-1).view(np.uint8)
         bufs.append((hb, dn.nbytes))
+    if device_inputs:
+        import torch
+        douts = [torch.empty((args.max_query, reps[0].output_dim), device="cuda:0")
+                 for _ in range(16)]
     outs = [rs.PinnedBuffer(args.max_query * reps[0].output_dim * 4) for _ in range(16)]
     n = args.serve_n
     dist = rs.SizeDistribution.log_normal(math.log(args.size_median), 0.5)
 
     def batch_for(sizes_idx):
         sizes = [int(pool_sizes[j]) for j in sizes_idx]
+        if device_inputs:
+            return reps[0].batch(sizes, [dbufs[j][0].data_ptr() for j in sizes_idx],
+                                 [dbufs[j][1].data_ptr() for j in sizes_idx],
+                                 [douts[i % 16].data_ptr() for i in range(len(sizes_idx))],
+                                 rs.MEM_DEVICE)
         return reps[0].batch(sizes, [bufs[j][0].ptr for j in sizes_idx],
                              [bufs[j][0].ptr + bufs[j][1] for j in sizes_idx],
                              [outs[i % 16].ptr for i in range(len(sizes_idx))], rs.MEM_HOST)
@@ -744,8 +776,10 @@ def run_serve(args):
             "fp32" if args.fc == "fp32" else "fp32 SLS / tf32 FC",
             "config": {"workload": args.workload, "model": spec.name, "rows_per_table": rows,
                        "sla_s": sla, "replicas": K, "queries_per_evaluation": n,
-                       "distinct_queries": P, "inputs": "host pinned, packed [dense | int64 "
-                       "indices] (reference byte model)", "fc_path": args.fc,
+                       "distinct_queries": P,
+                       "inputs": "device-resident (read in place)" if device_inputs else
+                       "host pinned, packed [dense | int64 indices] (reference byte model)",
+                       "fc_path": args.fc,
                        "lanes_per_replica": args.depth},
             "qps_at_sla": {"qps": best["achieved_qps"] if best else 0.0,
                            "at_lambda": best["lambda"] if best else 0.0,
@@ -777,6 +811,8 @@ def main():
                     help="1: each host query in one pinned buffer [dense | indices]")
     ap.add_argument("--size-median", type=float, default=300.0,
                     help="LogNormal(ln m, 0.5) query sizes (SURVEY 8d: 300; 30 = small-query regime)")
+    ap.add_argument("--size-fixed", type=int, default=0,
+                    help=">0: every query has this many items (BASELINE configs[3] batch sweep)")
     ap.add_argument("--merge", type=int, default=1,
                     help=">1 = labelled query-merging variant (SURVEY 8f-3)")
     ap.add_argument("--dense-bits", type=int, choices=[32, 16], default=32,
@@ -796,6 +832,8 @@ def main():
                          "mt-wnd/wnd, else the embedding kernel)")
     ap.add_argument("--serve", action="store_true",
                     help="real-time serving over --gpus replicas in one process (rs_serve)")
+    ap.add_argument("--serve-inputs", choices=["host", "device"], default="host",
+                    help="--serve: host pinned inputs (e2e) or device-resident (--gpus 1)")
     ap.add_argument("--serve-n", type=int, default=50_000,
                     help="--serve: queries per evaluation (reference n = 50,000)")
     args = ap.parse_args()

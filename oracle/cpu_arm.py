@@ -147,21 +147,27 @@ class CpuDeepRecSched:
         tc = np.array([np.median(self.samples[b][1]) for b in REQUEST_SIZES])
         return bs, t1, tc
 
-    def install(self):
+    def install(self, lib_=None):
+        """Put the measured table into `lib_` (default: librecsim_ref_cpu.so;
+        any reference build that links oracle/ref_cpu_adapter.cpp)."""
         bs, t1, tc = self.table()
-        rc = ref_cpu.ref_cpu_set_table(len(bs), bs.ctypes.data_as(P(C.c_int64)),
+        lib_ = lib_ or ref_cpu
+        lib_.ref_cpu_set_table.argtypes = ref_cpu.ref_cpu_set_table.argtypes
+        rc = lib_.ref_cpu_set_table(len(bs), bs.ctypes.data_as(P(C.c_int64)),
                                        t1.ctypes.data_as(P(C.c_double)),
                                        tc.ctypes.data_as(P(C.c_double)), self.threads)
         if rc:
             raise RuntimeError("ref_cpu_set_table failed")
 
     def tune(self, sla: float, mu: float, sigma: float, n: int = 50_000, seed: int = 42,
-             max_size: int = 1000) -> dict:
-        """Reference tune() CPU-only on the measured table: (B, QPS@p95)."""
+             max_size: int = 1000, kind: int = 2) -> dict:
+        """Reference tune() CPU-only on the measured table: (B, QPS@p95).
+        kind/mu/sigma: the SizeDistribution (LogNormal(mu, sigma), or kind 0 =
+        Fixed(mu))."""
         self.install()
         b, t, steps = C.c_int64(), C.c_int64(), C.c_int64()
         q, p, f = C.c_double(), C.c_double(), C.c_double()
-        rc = ref_cpu.ref_tune(C.byref(self.model), b"measured", b"", sla, seed, LOGNORMAL, mu,
+        rc = ref_cpu.ref_tune(C.byref(self.model), b"measured", b"", sla, seed, kind, mu,
                               sigma, 0.0, 0.0, max_size, n, 1, C.byref(b), C.byref(t),
                               C.byref(q), C.byref(p), C.byref(f), C.byref(steps))
         if rc:

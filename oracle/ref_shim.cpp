@@ -257,6 +257,35 @@ int ref_max_qps_accel(const or_model* m, const char* cpu, const char* accel, dou
   });
 }
 
+// tune() phase 2's inner loop made explicit (autotune.cpp:159-212): QPS@p95
+// of max_qps_under_sla at a fixed batch B for each offload threshold T in
+// thresholds[0..n) (T <= 0: CPU only). Out: qps[i], p95[i], accel_fraction[i].
+int ref_sweep_threshold(const or_model* m, const char* cpu, const char* accel, double sla,
+                        uint64_t seed, int kind, double p0, double p1, double p2, double p3,
+                        int64_t max_size, int64_t n, int64_t batch, const int64_t* thresholds,
+                        int64_t n_t, double* qps, double* p95, double* frac) {
+  return guard([&] {
+    for (int64_t i = 0; i < n_t; ++i) {
+      SchedulerConfig cfg;
+      cfg.batch_size = batch;
+      cfg.model = to_spec(*m);
+      cfg.cpu = shim_cpu(cpu);
+      if (thresholds[i] > 0) {
+        cfg.offload_threshold = thresholds[i];
+        cfg.accel = named_accel(accel);
+      }
+      TraceGenParams gen;
+      gen.base_seed = seed;
+      gen.dist = make_dist(kind, p0, p1, p2, p3, max_size);
+      gen.n = n;
+      QpsResult r = max_qps_under_sla(cfg, sla, gen);
+      qps[i] = r.qps;
+      p95[i] = r.p95;
+      frac[i] = r.accel_work_fraction;
+    }
+  });
+}
+
 // DeepRecSched tune() (autotune.cpp:90-217) with a named accelerator ("" = CPU only).
 int ref_tune(const or_model* m, const char* cpu, const char* accel, double sla, uint64_t seed,
              int kind, double p0, double p1, double p2, double p3, int64_t max_size, int64_t n,
