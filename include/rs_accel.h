@@ -373,6 +373,41 @@ int rs_host_fc(const float* x, int64_t rows, int32_t in_dim, const float* weight
                const float* bias, int32_t out_dim, int32_t relu, float* y,
                int32_t threads);
 
+/* ---- the CPU side of the split: whole model on the host cores ------------
+ * DeepRecSched sends every query of size <= T to the CPU as floor(S/B)
+ * requests of B items plus one of S mod B (proj/src/sim.cpp:184-188), each
+ * served whole by one core (sim.cpp:114-124) and priced by cpu_service_time
+ * (proj/src/platform.cpp:71-97). rs_host_model holds the same model as an
+ * rs_accel (tables + weights from the same seeded init) in host
+ * memory; rs_host_forward executes one request on the host cores: the same
+ * operator order and widths as the device graph, logits within the fp32
+ * tolerance rule of the oracle, SLS sums bit-identical to the device.       */
+typedef struct rs_host_model rs_host_model;
+/* threads <= 0: every core this process may run on (sched_getaffinity) for
+ * the table fill at create.                                                  */
+int rs_host_model_create(const rs_model_desc* model, const rs_init_desc* init,
+                         int32_t threads, rs_host_model** out);
+int rs_host_model_destroy(rs_host_model* h);
+/* One request (host memory, index_type 0): logits f32[S * stacks * out_dim].
+ * threads <= 1: the calling thread alone (the reference's one core per
+ * request); > 1: the request's items dealt to that many threads.
+ * RS_E_INDEX for an index outside [0, rows_per_table).                     */
+int rs_host_forward(rs_host_model* h, const rs_query* q, float* out, int32_t threads);
+
+/* Real-time DeepRecSched over this host's cores AND K accelerator replicas:
+ * query i is released at t0 + arrival_s[i]; if threshold > 0 and S >
+ * threshold it is offloaded whole to the least-loaded replica (as rs_serve),
+ * else split into floor(S/B) requests of `batch` items plus one of S mod B
+ * pushed to a FIFO served by `cores` worker threads, each request run by
+ * rs_host_forward on one thread (proj/src/sim.cpp:173-191). latency_ms[i]:
+ * completion (all of a query's requests, or its CUDA event) minus arrival;
+ * offloaded[i] (may be NULL): 1 if the query went to a replica. Queries are
+ * host memory; k = 0 serves CPU only (threshold ignored).                   */
+int rs_serve_hybrid(rs_host_model* cpu, int32_t cores, int64_t batch, int64_t threshold,
+                    rs_accel* const* replicas, int32_t k, int64_t n, const rs_query* queries,
+                    const double* arrival_s, float* const* outs, double* latency_ms,
+                    int32_t* offloaded);
+
 /* Pinned host memory for rs_query buffers. rs_alloc_pinned_flags accepts
  * RS_PINNED_WRITE_COMBINED for input buffers the host only writes (faster
  * H2D over PCIe; host reads from it are very slow).                         */
@@ -382,6 +417,12 @@ int rs_alloc_pinned_flags(size_t bytes, uint32_t flags, void** out);
 int rs_free_pinned(void* p);
 
 int rs_device_count(int* out);
+/* Build flags of the loaded library: RS_BUILD_EXPERIMENTS = the measured-
+ * slower alternatives (SLS variants 1/3/4, RS_FC_CHAIN, RS_SPLITK,
+ * RS_DENSE_SMS, RS_DESC_MEMOP) are compiled in (make EXPERIMENTS=1); the
+ * product build leaves them out and ignores those environment knobs.        */
+enum { RS_BUILD_EXPERIMENTS = 1 };
+int rs_build_flags(void);
 const char* rs_last_error(void);
 int rs_abi_version(void);
 

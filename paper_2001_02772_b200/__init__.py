@@ -23,7 +23,10 @@ import numpy as np
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librecsys_b200.so")
+# RS_LIB_VARIANT=exp loads the experiments build (make EXPERIMENTS=1 OUT=
+# ../librecsys_b200_exp.so): the measured-slower alternatives, for tools only.
+LIB_PATH = os.path.join(_HERE, "librecsys_b200_exp.so" if os.environ.get("RS_LIB_VARIANT") == "exp"
+                        else "librecsys_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -213,6 +216,13 @@ _sig("rs_alloc_pinned", C.c_int, C.c_size_t, P(C.c_void_p))
 _sig("rs_alloc_pinned_flags", C.c_int, C.c_size_t, C.c_uint32, P(C.c_void_p))
 _sig("rs_free_pinned", C.c_int, C.c_void_p)
 _sig("rs_device_count", C.c_int, P(C.c_int))
+_sig("rs_host_model_create", C.c_int, P(CModelDesc), P(CInitDesc), C.c_int32, P(C.c_void_p))
+_sig("rs_host_model_destroy", C.c_int, C.c_void_p)
+_sig("rs_host_forward", C.c_int, C.c_void_p, P(CQuery), C.c_void_p, C.c_int32)
+_sig("rs_serve_hybrid", C.c_int, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, P(C.c_void_p),
+     C.c_int32, C.c_int64, P(CQuery), P(C.c_double), P(C.c_void_p), P(C.c_double),
+     P(C.c_int32))
+_sig("rs_build_flags", C.c_int)
 
 EXPORTED_SYMBOLS = [
     "rs_abi_version", "rs_last_error", "rs_model_builtin", "rs_zoo_names", "rs_model_validate",
@@ -221,7 +231,8 @@ EXPORTED_SYMBOLS = [
     "rs_accel_destroy", "rs_accel_info_get", "rs_forward", "rs_forward_many", "rs_forward_many_ev", "rs_sync",
     "rs_pooled", "rs_service_time", "rs_service_breakdown", "rs_host_sls", "rs_host_fc",
     "rs_fill_query", "rs_fill_query_zipf", "rs_alloc_pinned", "rs_alloc_pinned_flags", "rs_free_pinned",
-    "rs_device_count", "rs_accel_set_option", "rs_serve"]
+    "rs_device_count", "rs_accel_set_option", "rs_serve", "rs_build_flags",
+    "rs_host_model_create", "rs_host_model_destroy", "rs_host_forward", "rs_serve_hybrid"]
 
 
 # ---- operator API (model_zoo.hpp mirror) ------------------------------------
@@ -448,6 +459,12 @@ def qps_under_sla(service_s: Sequence[float], sla: float, servers: int = 1,
     return QpsResult(r.qps, r.at_lambda, r.p95, r.p50, r.evaluations)
 
 
+def experiments_built() -> bool:
+    """True if the library was built with the measured-slower alternatives
+    (make EXPERIMENTS=1; rs_build_flags)."""
+    return bool(_lib.rs_build_flags() & 1)
+
+
 def device_count() -> int:
     n = C.c_int()
     _check(_lib.rs_device_count(C.byref(n)))
@@ -662,6 +679,61 @@ def serve(replicas: Sequence["Accelerator"], prepared, arrival_s) -> np.ndarray:
     _check(_lib.rs_serve(hs, len(replicas), n, qs, arr.ctypes.data_as(P(C.c_double)), outs,
                          lat.ctypes.data_as(P(C.c_double))))
     return lat
+
+
+class HostModel:
+    """The same model on the host cores (rs_host_model): the CPU side of
+    DeepRecSched's split, executed (proj/src/sim.cpp:114-124, 184-188)."""
+
+    def __init__(self, model: ModelSpec, rows_per_table: int, seed: int = 1,
+                 rnn_cell: int = RNN_GRU, threads: int = 0):
+        self.model = model
+        self._desc = model.to_c()
+        init = CInitDesc(seed, rows_per_table, 1, FC_FP32, rnn_cell, 0, 0)
+        h = C.c_void_p()
+        _check(_lib.rs_host_model_create(C.byref(self._desc), C.byref(init), int(threads),
+                                         C.byref(h)))
+        self._h = h
+        self.output_dim = model.num_parallel_predict_stacks * model.predict_fc.dims[-1]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _check(_lib.rs_host_model_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, dense: np.ndarray, idx: np.ndarray, threads: int = 1) -> np.ndarray:
+        """One request on the host cores: logits f32[S, stacks*out]."""
+        S = int(idx.shape[0]) if idx.size else int(dense.shape[0])
+        dense = np.ascontiguousarray(dense, dtype=np.float32)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.empty((S, self.output_dim), dtype=np.float32)
+        q = CQuery(S, dense.ctypes.data or None, idx.ctypes.data or None, MEM_HOST, 0)
+        _check(_lib.rs_host_forward(self._h, C.byref(q), out.ctypes.data, int(threads)))
+        return out
+
+
+def serve_hybrid(cpu: HostModel, cores: int, batch: int, threshold: int,
+                 replicas: Sequence["Accelerator"], prepared, arrival_s):
+    """rs_serve_hybrid: real-time DeepRecSched over `cores` host threads and
+    the replicas; returns (latency_ms, offloaded) per query."""
+    n, qs, outs = prepared
+    arr = np.ascontiguousarray(arrival_s, dtype=np.float64)
+    if arr.shape[0] != n:
+        raise InvalidArgument("arrival_s must have one entry per query")
+    hs = (C.c_void_p * max(1, len(replicas)))(*[r._h for r in replicas])
+    lat = np.zeros(n, dtype=np.float64)
+    off = np.zeros(n, dtype=np.int32)
+    _check(_lib.rs_serve_hybrid(cpu._h, int(cores), int(batch), int(threshold), hs,
+                                len(replicas), n, qs, arr.ctypes.data_as(P(C.c_double)), outs,
+                                lat.ctypes.data_as(P(C.c_double)),
+                                off.ctypes.data_as(P(C.c_int32))))
+    return lat, off
 
 
 class PinnedBuffer:

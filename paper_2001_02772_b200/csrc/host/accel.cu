@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -52,6 +53,7 @@ constexpr int kDescRing = 256;
 
 using BatchMemOpFn = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 
+#if RS_EXPERIMENTS
 BatchMemOpFn batch_memop_fn() {
   static BatchMemOpFn fn = [] {
     void* p = nullptr;
@@ -63,6 +65,7 @@ BatchMemOpFn batch_memop_fn() {
   }();
   return fn;
 }
+#endif
 
 struct FcLayer {
   int64_t in = 0, out = 0, ldk = 0;
@@ -618,6 +621,7 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   return exec;
 }
 
+#if RS_EXPERIMENTS  // green-context SM partitions: measured slower
 // Green-context entry points (driver API, fetched at run time: no -lcuda).
 struct GreenApi {
   CUresult (*get_res)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
@@ -681,12 +685,15 @@ bool make_partition(rs_accel* a, int dense_sms) {
   return true;
 }
 
+#endif  // RS_EXPERIMENTS
+
 std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   RS_CUDA(cudaSetDevice(a->device));
   auto s = std::make_unique<Slot>();
   const int64_t maxS = a->init.max_query_size;
   RS_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
   s->emb_sms = s->dense_sms = a->sm_count;
+#if RS_EXPERIMENTS
   if (partitioned && a->g_dense) {
     const GreenApi& ga = green_api();
     CUstream sd = nullptr, se = nullptr;
@@ -698,6 +705,9 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
     s->emb_sms = a->part_emb_sms;
     s->dense_sms = a->part_dense_sms;
   }
+#else
+  (void)partitioned;
+#endif
   s->d_q = static_cast<QDesc*>(dmalloc(a, s->allocs, sizeof(QDesc)));
   RS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_q), sizeof(QDesc) * kDescRing,
                         cudaHostAllocPortable));
@@ -861,6 +871,7 @@ void write_desc(rs_accel* a, Slot* s, const QDesc& v, cudaStream_t st) {
   RS_CUDA(cudaEventRecord(s->q_ev[r], st));
 }
 
+#if RS_EXPERIMENTS  // stream-memop descriptors: measured slower
 // Descriptor writes: a copy from the slot's event-guarded pinned ring
 // (default; measured faster for a lone query, equal in the pipelined queue),
 // or with RS_DESC_MEMOP=1 stream memory writes, used only if a test write lands.
@@ -885,6 +896,8 @@ BatchMemOpFn probe_memops(rs_accel* a) {
   (void)cudaGetLastError();
   return ok ? fn : nullptr;
 }
+
+#endif  // RS_EXPERIMENTS
 
 // Inputs of one query onto the slot: host buffers are copied (one contiguous
 // H2D each) into the slot's landing zones; device buffers are used in place.
@@ -1344,8 +1357,10 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     RS_CUDA(cudaStreamCreateWithFlags(&a->own, cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&a->copy_gate, cudaEventDisableTiming));
     build_model(a);
+#if RS_EXPERIMENTS
     a->memops = probe_memops(a);
     if (const char* ds = getenv("RS_DENSE_SMS")) make_partition(a, atoi(ds));
+#endif
     *out = a;
   });
   if (rc != RS_OK && a) {
@@ -1378,8 +1393,10 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
     if (a->hot) cudaCtxResetPersistingL2Cache();
     for (void* p : a->allocs) cudaFree(p);
     if (a->own) cudaStreamDestroy(a->own);
+#if RS_EXPERIMENTS
     if (a->g_dense) green_api().destroy(a->g_dense);
     if (a->g_emb) green_api().destroy(a->g_emb);
+#endif
     delete a;
   });
 }
@@ -1423,18 +1440,17 @@ extern "C" int rs_forward_many_ev(rs_accel* a, int64_t n, const rs_query* querie
   return run_many(a, n, queries, outs, stream, service_ms, latency_ms, done_event);
 }
 
-// Real-time executor: the reference's single FIFO accelerator
-// server (accel_busy + accel_fifo, proj/src/sim.cpp:95-97, 126-136)
-// generalised to a K-replica pool. The calling thread releases query i at
-// t0 + arrival_s[i] (host clock) and routes it to the replica with the least
-// outstanding items (ties to the lowest index); one dispatcher
-// thread per replica stages, launches and retires that replica's queries on
-// its lanes exactly as rs_forward_many does, so host dispatch cost scales
-// with the replica count instead of serialising on one thread. Outstanding
-// item counts are atomics: the releaser adds on assignment, the replica's
-// dispatcher subtracts when the query's completion event has fired.
-// latency = completion (CUDA event on the replica, relative to a start event
-// recorded at t0) minus the arrival offset: queueing + service.
+// Real-time executors. The reference's single FIFO accelerator
+// server (accel_busy + accel_fifo, proj/src/sim.cpp:95-97, 126-136) becomes a
+// K-replica pool: the releasing thread routes each offloaded query to the
+// replica with the least outstanding items (ties to the lowest index, SURVEY
+// §8e); one dispatcher thread per replica stages, launches and retires that
+// replica's queries on its lanes exactly as rs_forward_many does, so host
+// dispatch cost scales with the replica count. Outstanding item counts are
+// atomics: the releaser adds on assignment, the replica's dispatcher subtracts
+// when the query's completion event has fired. GPU completion times are CUDA
+// events relative to a start event recorded (and waited for) just before the
+// host clock's t0.
 namespace rs {
 namespace {
 
@@ -1444,7 +1460,8 @@ struct ServeRep {
   std::atomic<int64_t> outstanding{0};
   // assignment ring (releaser -> dispatcher), single producer/consumer
   std::vector<int64_t> queue;
-  std::atomic<int64_t> head{0}, tail{0};
+  std::atomic<int64_t> head{0};
+  int64_t tail = 0;
   std::deque<std::pair<int64_t, int64_t>> inflight;  // (query, replica-local seq)
   int64_t issued = 0;
   int64_t dispatched = 0;
@@ -1452,32 +1469,27 @@ struct ServeRep {
 
 constexpr int64_t kServeRing = 4096;
 
-}  // namespace
-}  // namespace rs
+struct ServeShared {
+  const rs_query* qs = nullptr;
+  float* const* outs = nullptr;
+  int loc = RS_MEM_HOST;
+  std::vector<double> done_ms;          // per query, device clock since t0
+  std::atomic<bool> released_all{false};
+  std::atomic<int> failed{0};
+  std::mutex err_mu;
+  Error first_err{RS_OK, ""};
+  void record(const Error& e) {
+    std::lock_guard<std::mutex> g(err_mu);
+    if (!failed.exchange(1)) first_err = e;
+  }
+};
 
-extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_query* qs,
-                        const double* arrival_s, float* const* outs, double* latency_ms) {
-  std::vector<std::unique_lock<std::mutex>> locks;
-  return guarded([&] {
-    if (!reps || !qs || !arrival_s || !outs || !latency_ms) raise(RS_E_INVALID, "null argument");
-    if (k < 1 || n < 1) raise(RS_E_INVALID, "k < 1 or n < 1");
-    const int loc = qs[0].location;
-    for (int r = 0; r < k; ++r)
-      if (!reps[r]) raise(RS_E_INVALID, "null replica");
-    for (int64_t i = 0; i < n; ++i) {
-      for (int r = 0; r < k; ++r) check_query(reps[r], &qs[i]);
-      if (qs[i].location != loc) raise(RS_E_INVALID, "mixed memory locations");
-      if (!outs[i]) raise(RS_E_INVALID, "null output");
-      if (!(arrival_s[i] >= 0) || (i && arrival_s[i] < arrival_s[i - 1]))
-        raise(RS_E_INVALID, "arrival times must be non-negative and non-decreasing");
-    }
-    // queue locks in address order (two concurrent callers can never deadlock)
-    std::vector<rs_accel*> order(reps, reps + k);
-    std::sort(order.begin(), order.end());
-    order.erase(std::unique(order.begin(), order.end()), order.end());
-    if ((int)order.size() != k) raise(RS_E_INVALID, "a replica appears twice");
-    for (rs_accel* a : order) locks.emplace_back(a->many_mu);
-    std::vector<std::unique_ptr<ServeRep>> R;
+// Replica pool of one serving call: lanes, event rings, t0 events.
+struct ServePool {
+  std::vector<std::unique_ptr<ServeRep>> R;
+  std::vector<std::thread> th;
+
+  void setup(rs_accel* const* reps, int32_t k, int64_t n) {
     for (int r = 0; r < k; ++r) {
       auto rp = std::make_unique<ServeRep>();
       rs_accel* a = reps[r];
@@ -1492,8 +1504,10 @@ extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_qu
       rp->queue.assign((size_t)n, -1);
       R.push_back(std::move(rp));
     }
-    std::vector<double> done_ms((size_t)n, -1.0);
-    // t0: a start event on every replica, then release queries on the clock
+  }
+  // t0 on every replica (a start event each; the lanes and copy stream wait
+  // for it), returned only once the events have fired
+  void start_clock() {
     for (auto& rp : R) {
       rs_accel* a = rp->a;
       RS_CUDA(cudaSetDevice(a->device));
@@ -1503,107 +1517,258 @@ extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_qu
       RS_CUDA(cudaStreamWaitEvent(a->copy, a->copy_gate, 0));
       RS_CUDA(cudaStreamSynchronize(a->own));
     }
-    std::atomic<bool> released_all{false};
-    std::atomic<int> failed{0};
-    std::mutex err_mu;
-    Error first_err{RS_OK, ""};
-    auto record_error = [&](const Error& e) {
-      std::lock_guard<std::mutex> g(err_mu);
-      if (!failed.exchange(1)) first_err = e;
-    };
-    // one dispatcher per replica
-    auto dispatcher = [&](ServeRep* rp) {
-      try {
-        rs_accel* a = rp->a;
-        RS_CUDA(cudaSetDevice(a->device));
-        auto retire = [&](bool block) {
-          while (!rp->inflight.empty()) {
-            const auto [qi, seq] = rp->inflight.front();
-            cudaEvent_t e = a->evpool[1 + seq % kServeRing];
-            if (block) {
-              RS_CUDA(cudaEventSynchronize(e));
-            } else {
-              const cudaError_t st = cudaEventQuery(e);
-              if (st == cudaErrorNotReady) break;
-              if (st != cudaSuccess) RS_CUDA(st);
-            }
-            done_ms[(size_t)qi] = elapsed(a->evpool[0], e);
-            rp->outstanding.fetch_sub(qs[qi].size, std::memory_order_relaxed);
-            rp->inflight.pop_front();
-          }
-        };
-        for (;;) {
-          if (failed.load(std::memory_order_relaxed)) return;
-          const int64_t h = rp->head.load(std::memory_order_acquire);
-          if (rp->dispatched == h) {
-            retire(false);
-            if (released_all.load(std::memory_order_acquire) &&
-                rp->dispatched == rp->head.load(std::memory_order_acquire))
-              break;
-            std::this_thread::yield();
-            continue;
-          }
-          const int64_t i = rp->queue[(size_t)rp->dispatched++];
-          const int64_t seq = rp->issued++;
-          if (seq >= kServeRing)  // event-ring reuse: that query must have retired
-            while (!rp->inflight.empty() && rp->inflight.front().second <= seq - kServeRing)
-              retire(true);
-          const int d = (int)(seq % a->depth);
-          Slot* sl = rp->p[d];
-          cudaStream_t ls = a->lane[d];
-          if (loc == RS_MEM_HOST) {
-            RS_CUDA(cudaStreamWaitEvent(a->copy, sl->free, 0));
-            stage_inputs(a, sl, &qs[i], true, a->copy, nullptr, /*widen_later=*/true);
-            RS_CUDA(cudaEventRecord(sl->ready, a->copy));
-            RS_CUDA(cudaStreamWaitEvent(ls, sl->ready, 0));
-            widen_indices(a, sl, &qs[i], ls);
-          } else {
-            stage_inputs(a, sl, &qs[i], true, ls, outs[i]);
-          }
-          launch_stage(a, sl, &qs[i], outs[i], true, ls);
-          RS_CUDA(cudaEventRecord(sl->free, ls));
-          RS_CUDA(cudaEventRecord(a->evpool[1 + seq % kServeRing], ls));
-          rp->inflight.emplace_back(i, seq);
-          retire(false);
-        }
-        retire(true);
-        for (int d = 0; d < a->depth; ++d) collect_errors(rp->p[d], a->lane[d]);
-      } catch (const Error& e) {
-        record_error(e);
-      } catch (const std::exception& e) {
-        record_error(Error{RS_E_INVALID, e.what()});
-      }
-    };
-    std::vector<std::thread> th;
-    th.reserve((size_t)k);
-    for (auto& rp : R) th.emplace_back(dispatcher, rp.get());
-    const auto t0 = std::chrono::steady_clock::now();
-    for (int64_t i = 0; i < n && !failed.load(std::memory_order_relaxed); ++i) {
-      const auto due = t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
-                                std::chrono::duration<double>(arrival_s[i]));
-      for (;;) {
-        const auto now = std::chrono::steady_clock::now();
-        if (now >= due) break;
-        if (due - now > std::chrono::microseconds(200))
-          std::this_thread::sleep_for(std::chrono::microseconds(50));
-      }
-      int best = 0;
-      int64_t best_out = R[0]->outstanding.load(std::memory_order_relaxed);
-      for (int r = 1; r < k; ++r) {
-        const int64_t o = R[r]->outstanding.load(std::memory_order_relaxed);
-        if (o < best_out) { best = r; best_out = o; }
-      }
-      ServeRep* rp = R[best].get();
-      rp->outstanding.fetch_add(qs[i].size, std::memory_order_relaxed);
-      const int64_t t = rp->tail.load(std::memory_order_relaxed);
-      rp->queue[(size_t)t] = i;
-      rp->tail.store(t + 1, std::memory_order_relaxed);
-      rp->head.store(t + 1, std::memory_order_release);
+  }
+  void launch(ServeShared& sh) {
+    th.reserve(R.size());
+    for (auto& rp : R) th.emplace_back([&sh, p = rp.get()] { dispatch_loop(p, sh); });
+  }
+  // least outstanding items, ties to the lowest index
+  void route(int64_t i, const ServeShared& sh) {
+    int best = 0;
+    int64_t best_out = R[0]->outstanding.load(std::memory_order_relaxed);
+    for (int r = 1; r < (int)R.size(); ++r) {
+      const int64_t o = R[r]->outstanding.load(std::memory_order_relaxed);
+      if (o < best_out) { best = r; best_out = o; }
     }
-    released_all.store(true, std::memory_order_release);
+    ServeRep* rp = R[best].get();
+    rp->outstanding.fetch_add(sh.qs[i].size, std::memory_order_relaxed);
+    rp->queue[(size_t)rp->tail++] = i;
+    rp->head.store(rp->tail, std::memory_order_release);
+  }
+  void join() {
     for (auto& t : th) t.join();
-    if (failed.load()) raise(first_err.code, first_err.msg);
-    for (int64_t i = 0; i < n; ++i) latency_ms[i] = done_ms[(size_t)i] - arrival_s[i] * 1e3;
+    th.clear();
+  }
+
+  static void dispatch_loop(ServeRep* rp, ServeShared& sh) {
+    try {
+      rs_accel* a = rp->a;
+      RS_CUDA(cudaSetDevice(a->device));
+      auto retire = [&](bool block) {
+        while (!rp->inflight.empty()) {
+          const auto [qi, seq] = rp->inflight.front();
+          cudaEvent_t e = a->evpool[1 + seq % kServeRing];
+          if (block) {
+            RS_CUDA(cudaEventSynchronize(e));
+          } else {
+            const cudaError_t st = cudaEventQuery(e);
+            if (st == cudaErrorNotReady) break;
+            if (st != cudaSuccess) RS_CUDA(st);
+          }
+          sh.done_ms[(size_t)qi] = elapsed(a->evpool[0], e);
+          rp->outstanding.fetch_sub(sh.qs[qi].size, std::memory_order_relaxed);
+          rp->inflight.pop_front();
+        }
+      };
+      for (;;) {
+        if (sh.failed.load(std::memory_order_relaxed)) return;
+        const int64_t h = rp->head.load(std::memory_order_acquire);
+        if (rp->dispatched == h) {
+          retire(false);
+          if (sh.released_all.load(std::memory_order_acquire) &&
+              rp->dispatched == rp->head.load(std::memory_order_acquire))
+            break;
+          std::this_thread::yield();
+          continue;
+        }
+        const int64_t i = rp->queue[(size_t)rp->dispatched++];
+        const int64_t seq = rp->issued++;
+        if (seq >= kServeRing)  // event-ring reuse: that query must have retired
+          while (!rp->inflight.empty() && rp->inflight.front().second <= seq - kServeRing)
+            retire(true);
+        const int d = (int)(seq % a->depth);
+        Slot* sl = rp->p[d];
+        cudaStream_t ls = a->lane[d];
+        if (sh.loc == RS_MEM_HOST) {
+          RS_CUDA(cudaStreamWaitEvent(a->copy, sl->free, 0));
+          stage_inputs(a, sl, &sh.qs[i], true, a->copy, nullptr, /*widen_later=*/true);
+          RS_CUDA(cudaEventRecord(sl->ready, a->copy));
+          RS_CUDA(cudaStreamWaitEvent(ls, sl->ready, 0));
+          widen_indices(a, sl, &sh.qs[i], ls);
+        } else {
+          stage_inputs(a, sl, &sh.qs[i], true, ls, sh.outs[i]);
+        }
+        launch_stage(a, sl, &sh.qs[i], sh.outs[i], true, ls);
+        RS_CUDA(cudaEventRecord(sl->free, ls));
+        RS_CUDA(cudaEventRecord(a->evpool[1 + seq % kServeRing], ls));
+        rp->inflight.emplace_back(i, seq);
+        retire(false);
+      }
+      retire(true);
+      for (int d = 0; d < a->depth; ++d) collect_errors(rp->p[d], a->lane[d]);
+    } catch (const Error& e) {
+      sh.record(e);
+    } catch (const std::exception& e) {
+      sh.record(Error{RS_E_INVALID, e.what()});
+    }
+  }
+};
+
+// host-clock wait until t0 + seconds
+void wait_until(std::chrono::steady_clock::time_point t0, double seconds) {
+  const auto due = t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                            std::chrono::duration<double>(seconds));
+  for (;;) {
+    const auto now = std::chrono::steady_clock::now();
+    if (now >= due) break;
+    if (due - now > std::chrono::microseconds(200))
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+void check_serve_args(rs_accel* const* reps, int32_t k, int64_t n, const rs_query* qs,
+                      const double* arrival_s, float* const* outs, double* latency_ms,
+                      std::vector<std::unique_lock<std::mutex>>& locks) {
+  if (!qs || !arrival_s || !outs || !latency_ms) raise(RS_E_INVALID, "null argument");
+  if (k < 0 || n < 1 || (k > 0 && !reps)) raise(RS_E_INVALID, "k < 0 or n < 1");
+  const int loc = qs[0].location;
+  for (int r = 0; r < k; ++r)
+    if (!reps[r]) raise(RS_E_INVALID, "null replica");
+  for (int64_t i = 0; i < n; ++i) {
+    for (int r = 0; r < k; ++r) check_query(reps[r], &qs[i]);
+    if (qs[i].location != loc) raise(RS_E_INVALID, "mixed memory locations");
+    if (!outs[i]) raise(RS_E_INVALID, "null output");
+    if (!(arrival_s[i] >= 0) || (i && arrival_s[i] < arrival_s[i - 1]))
+      raise(RS_E_INVALID, "arrival times must be non-negative and non-decreasing");
+  }
+  // queue locks in address order (two concurrent callers can never deadlock)
+  std::vector<rs_accel*> order(reps, reps + k);
+  std::sort(order.begin(), order.end());
+  order.erase(std::unique(order.begin(), order.end()), order.end());
+  if ((int)order.size() != k) raise(RS_E_INVALID, "a replica appears twice");
+  for (rs_accel* a : order) locks.emplace_back(a->many_mu);
+}
+
+}  // namespace
+}  // namespace rs
+
+extern "C" int rs_serve(rs_accel* const* reps, int32_t k, int64_t n, const rs_query* qs,
+                        const double* arrival_s, float* const* outs, double* latency_ms) {
+  std::vector<std::unique_lock<std::mutex>> locks;
+  return guarded([&] {
+    if (k < 1) raise(RS_E_INVALID, "k < 1");
+    check_serve_args(reps, k, n, qs, arrival_s, outs, latency_ms, locks);
+    ServeShared sh;
+    sh.qs = qs;
+    sh.outs = outs;
+    sh.loc = qs[0].location;
+    sh.done_ms.assign((size_t)n, -1.0);
+    ServePool pool;
+    pool.setup(reps, k, n);
+    pool.start_clock();
+    pool.launch(sh);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < n && !sh.failed.load(std::memory_order_relaxed); ++i) {
+      wait_until(t0, arrival_s[i]);
+      pool.route(i, sh);
+    }
+    sh.released_all.store(true, std::memory_order_release);
+    pool.join();
+    if (sh.failed.load()) raise(sh.first_err.code, sh.first_err.msg);
+    for (int64_t i = 0; i < n; ++i) latency_ms[i] = sh.done_ms[(size_t)i] - arrival_s[i] * 1e3;
+  });
+}
+
+// DeepRecSched in real time: the routing decision of
+// simulate() (proj/src/sim.cpp:173-191) executed — offloaded queries to the
+// replica pool above, the rest split into requests of `batch` items on a FIFO
+// served by `cores` host worker threads (the C-core pool, sim.cpp:114-124),
+// each request run whole by rs_host_forward on its thread. A query completes
+// when its last request (or its offloaded run) does.
+extern "C" int rs_serve_hybrid(rs_host_model* cpu, int32_t cores, int64_t batch,
+                               int64_t threshold, rs_accel* const* reps, int32_t k, int64_t n,
+                               const rs_query* qs, const double* arrival_s, float* const* outs,
+                               double* latency_ms, int32_t* offloaded) {
+  std::vector<std::unique_lock<std::mutex>> locks;
+  return guarded([&] {
+    if (!cpu) raise(RS_E_INVALID, "null host model");
+    if (cores < 1 || batch < 1) raise(RS_E_INVALID, "cores < 1 or batch < 1");
+    check_serve_args(reps, k, n, qs, arrival_s, outs, latency_ms, locks);
+    for (int64_t i = 0; i < n; ++i)
+      if (qs[i].location != RS_MEM_HOST || qs[i].index_type != 0)
+        raise(RS_E_INVALID, "hybrid serving takes host queries in the reference byte model");
+    const bool use_gpu = k > 0 && threshold > 0;
+    ServeShared sh;
+    sh.qs = qs;
+    sh.outs = outs;
+    sh.loc = RS_MEM_HOST;
+    sh.done_ms.assign((size_t)n, -1.0);
+    ServePool pool;
+    if (use_gpu) {
+      pool.setup(reps, k, n);
+      pool.start_clock();
+      pool.launch(sh);
+    }
+    // CPU side: request FIFO + worker pool
+    struct Req { int64_t q, off, cnt; };
+    std::deque<Req> fifo;
+    std::mutex fmu;
+    std::condition_variable fcv;
+    bool closed = false;
+    std::vector<std::atomic<int64_t>> remaining((size_t)n);
+    std::vector<double> cpu_done((size_t)n, -1.0);
+    std::chrono::steady_clock::time_point t0;
+    auto worker = [&] {
+      try {
+        for (;;) {
+          Req r;
+          {
+            std::unique_lock<std::mutex> g(fmu);
+            fcv.wait(g, [&] { return closed || !fifo.empty(); });
+            if (fifo.empty()) return;
+            r = fifo.front();
+            fifo.pop_front();
+          }
+          if (sh.failed.load(std::memory_order_relaxed)) continue;
+          const rs_query& q = qs[r.q];
+          const int64_t bad = host_forward_rows(cpu, q.dense, q.indices, outs[r.q], r.off,
+                                                r.off + r.cnt);
+          if (bad >= 0) raise(RS_E_INDEX, "embedding index outside [0, rows_per_table)");
+          if (remaining[(size_t)r.q].fetch_sub(1) == 1)
+            cpu_done[(size_t)r.q] =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count();
+        }
+      } catch (const Error& e) {
+        sh.record(e);
+      } catch (const std::exception& e) {
+        sh.record(Error{RS_E_INVALID, e.what()});
+      }
+    };
+    t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> workers;
+    for (int c = 0; c < cores; ++c) workers.emplace_back(worker);
+    for (int64_t i = 0; i < n && !sh.failed.load(std::memory_order_relaxed); ++i) {
+      wait_until(t0, arrival_s[i]);
+      const int64_t S = qs[i].size;
+      const bool off = use_gpu && S > threshold;  // strictly greater (sim.cpp:178)
+      if (offloaded) offloaded[i] = off ? 1 : 0;
+      if (off) {
+        pool.route(i, sh);
+        continue;
+      }
+      const int64_t full = S / batch, rem = S % batch;
+      remaining[(size_t)i].store(full + (rem > 0 ? 1 : 0));
+      {
+        std::lock_guard<std::mutex> g(fmu);
+        for (int64_t j = 0; j < full; ++j) fifo.push_back({i, j * batch, batch});
+        if (rem > 0) fifo.push_back({i, full * batch, rem});
+      }
+      fcv.notify_all();
+    }
+    {
+      std::lock_guard<std::mutex> g(fmu);
+      closed = true;
+    }
+    fcv.notify_all();
+    sh.released_all.store(true, std::memory_order_release);
+    for (auto& w : workers) w.join();
+    if (use_gpu) pool.join();
+    if (sh.failed.load()) raise(sh.first_err.code, sh.first_err.msg);
+    for (int64_t i = 0; i < n; ++i) {
+      const bool off = use_gpu && qs[i].size > threshold;
+      latency_ms[i] = (off ? sh.done_ms[(size_t)i] : cpu_done[(size_t)i]) - arrival_s[i] * 1e3;
+    }
   });
 }
 
@@ -1740,3 +1905,5 @@ extern "C" int rs_service_breakdown(rs_accel* a, int64_t query_size, double* tot
     *transfer = X;
   });
 }
+
+extern "C" int rs_build_flags(void) { return RS_EXPERIMENTS ? RS_BUILD_EXPERIMENTS : 0; }

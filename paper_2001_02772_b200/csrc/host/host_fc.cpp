@@ -104,6 +104,12 @@ void fc_rows(const float* __restrict__ x, int64_t m0, int64_t m1, int K, int N,
 }
 
 }  // namespace
+
+void host_fc_rows(const float* x, int64_t m0, int64_t m1, int K, int N, const float* wt,
+                  const float* b, int relu, float* y) {
+  fc_rows(x, m0, m1, K, N, wt, b, relu, y);
+}
+
 }  // namespace rs
 
 extern "C" int rs_host_fc(const float* x, int64_t rows, int32_t in_dim, const float* weight,

@@ -73,6 +73,12 @@ int64_t pool_range(const float* __restrict__ tables, int64_t rows, int T, int L,
 }
 
 }  // namespace
+
+int64_t host_pool_bags(const float* tables, int64_t rows, int T, int L, int D,
+                       const int64_t* idx, float* pooled, int64_t b0, int64_t b1) {
+  return pool_range(tables, rows, T, L, D, canonical_r(D), idx, pooled, b0, b1, 8);
+}
+
 }  // namespace rs
 
 extern "C" int rs_host_sls(const float* tables, int64_t rows_per_table, int32_t num_tables,

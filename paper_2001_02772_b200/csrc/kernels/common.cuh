@@ -10,6 +10,13 @@
 
 #include "../spec.h"
 
+// Measured-slower alternatives (SLS variants 1/3/4, the whole-stack FC chain
+// kernel, split-K, green-context partitions, stream-memop descriptors) are
+// compiled only into an experiments build: make EXPERIMENTS=1.
+#ifndef RS_EXPERIMENTS
+#define RS_EXPERIMENTS 0
+#endif
+
 namespace rs {
 
 // Device-resident query descriptor. Every kernel of the forward graph reads
@@ -114,16 +121,31 @@ inline int high_priority() {
 // preferred L1/shared split. Measured off by default: the gathers lose L1
 // capacity for in-flight loads (pipelined queue 34.2 -> 39.0 us/query, one
 // launch 5.43 -> 4.99 TB/s at 323 items).
+// Function attributes belong to the current device's context: a process that
+// drives several GPUs (rs_serve over K replicas) sets them once PER DEVICE.
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+inline void smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.insert({current_device(), fn}).second)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 inline void max_carveout(const void* fn) {
   static std::mutex mu;
-  static std::set<const void*> done;
+  static std::set<std::pair<int, const void*>> done;
   static const bool on = [] {
     const char* v = getenv("RS_CARVEOUT");
     return v && atoi(v) != 0;
   }();
   if (!on) return;
   std::lock_guard<std::mutex> g(mu);
-  if (done.insert(fn).second)
+  if (done.insert({current_device(), fn}).second)
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
 }

@@ -111,6 +111,7 @@ sls_sum_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, i
   }
 }
 
+#if RS_EXPERIMENTS  // measured-slower SLS variant 1
 // Variant 1 (RS_SLS_VARIANT=1): TMA tile::gather4. One warp per CTA; the warp walks its bags
 // in sub-chunks of up to LB rows. For each sub-chunk, lane i loads lookups
 // 4i..4i+3, turns them into rows of the stacked [T*rows, D] tensor and issues
@@ -247,6 +248,8 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
   }
 }
 
+#endif  // RS_EXPERIMENTS
+
 // Variant 2 (RS_SLS_VARIANT=2): warp-per-bag with the two serial latencies of
 // a bag hidden — the NEXT bag's index list is loaded into registers while this
 // bag's rows stream, and row batch j+1 is in flight while batch j accumulates.
@@ -343,6 +346,7 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
   }
 }
 
+#if RS_EXPERIMENTS  // measured-slower SLS variants 4 and 3
 // Variant 4 (RS_SLS_VARIANT=4): variant 2 without the bubble between bags.
 // A warp's bags are one continuous stream of row batches: batch t+1 is issued
 // before batch t is summed even when t+1 is the first batch of the warp's
@@ -571,6 +575,8 @@ sls_stage_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables,
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
+
+#endif  // RS_EXPERIMENTS
 
 // Any D (not a power of two in [8,256]): lane-per-column, sequential in l.
 __global__ void __launch_bounds__(kWarps * 32)
@@ -983,6 +989,7 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
   kern<<<grid, wpc * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err, hot, hot_rows);
 }
 
+#if RS_EXPERIMENTS  // variant 4 launcher
 template <int LPR, int VPL, int U, int IPL>
 void launch_sls_stream(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                        float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
@@ -1018,6 +1025,8 @@ bool try_sls_stream(const QDesc* qd, const float* tables, int64_t rows, int T, i
   return true;
 }
 
+#endif  // RS_EXPERIMENTS
+
 template <int LPR, int VPL>
 bool try_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L, float* out,
                   int64_t ld_out, int* err, int64_t max_items, int sm_count, cudaStream_t s,
@@ -1040,6 +1049,7 @@ bool try_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int
   return true;
 }
 
+#if RS_EXPERIMENTS  // variant 3 launcher
 // Variant 3 geometry: one CTA per SM, each warp owning nbuf bag stages
 // (RS_SLS_NBUF, 2..4, default 2) of L*D*4 bytes; as many warps as fit in
 // RS_SLS_SMEM_KB (default 200) of shared memory, at most 16 (RS_SLS_WARPS caps).
@@ -1055,12 +1065,7 @@ bool launch_sls_stage(const QDesc* qd, const float* tables, int64_t rows, int T,
   nw = std::min(nw, env_int("RS_SLS_WARPS", 16));
   if (nw < 1) return false;
   const size_t smem = per_warp * nw;
-  static bool attr = [] {
-    return cudaFuncSetAttribute(sls_stage_kernel<LPR, VPL, IPL>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
-           cudaSuccess;
-  }();
-  if (!attr) return false;
+  smem_attr(reinterpret_cast<const void*>(sls_stage_kernel<LPR, VPL, IPL>), 227 * 1024);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sls_stage_kernel<LPR, VPL, IPL>, nw * 32,
                                                 smem);
@@ -1083,6 +1088,8 @@ bool try_sls_stage(const QDesc* qd, const float* tables, int64_t rows, int T, in
                                        sm_count, s);
 }
 
+#endif  // RS_EXPERIMENTS
+
 template <int LPR, int VPL, int U>
 void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                     float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
@@ -1098,6 +1105,7 @@ void launch_sls_bag(const QDesc* qd, const float* tables, int64_t rows, int T, i
                                                            err, 0);
 }
 
+#if RS_EXPERIMENTS  // variant 1 launcher
 template <int LPR, int VPL, int NBUF>
 bool launch_sls_tma(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                     float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
@@ -1120,24 +1128,40 @@ bool launch_sls_tma(const QDesc* qd, const float* tables, int64_t rows, int T, i
   return true;
 }
 
+#endif  // RS_EXPERIMENTS
+
+// Measured-slower SLS variants (RS_SLS_VARIANT = 1 TMA gather4, 3 cp.async
+// staged, 4 continuous stream) exist only in an experiments
+// build (make EXPERIMENTS=1); the product build serves 2 (default) and 0.
+template <int LPR, int VPL>
+bool try_sls_experimental(int v, const QDesc* qd, const float* tables, int64_t rows, int T, int L,
+                          float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
+                          cudaStream_t s) {
+#if RS_EXPERIMENTS
+  if (v == 1) return launch_sls_tma<LPR, VPL, 2>(qd, tables, rows, T, L, out, ld_out, err,
+                                                 max_items, sm_count, s);
+  if (v == 3) return try_sls_stage<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, err, max_items,
+                                             sm_count, s);
+  if (v == 4) return try_sls_stream<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, err,
+                                              max_items, sm_count, s);
+#else
+  (void)v; (void)qd; (void)tables; (void)rows; (void)T; (void)L; (void)out; (void)ld_out;
+  (void)err; (void)max_items; (void)sm_count; (void)s;
+#endif
+  return false;
+}
+
 void launch_sls_sum(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
                     float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
                     cudaStream_t s, const float* hot, int64_t hot_rows) {
 #define RS_SLS(LPR, VPL)                                                                    \
   do {                                                                                      \
-    if (sls_variant() == 1 && launch_sls_tma<LPR, VPL, 2>(qd, tables, rows, T, L, out,      \
-                                                          ld_out, err, max_items, sm_count, \
-                                                          s))                               \
+    if (try_sls_experimental<LPR, VPL>(sls_variant(), qd, tables, rows, T, L, out, ld_out,  \
+                                       err, max_items, sm_count, s))                        \
       break;                                                                                \
     if (sls_variant() == 2 && try_sls_pipe<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,   \
                                                      err, max_items, sm_count, s, hot,      \
                                                      hot_rows))                             \
-      break;                                                                                \
-    if (sls_variant() == 3 && try_sls_stage<LPR, VPL>(qd, tables, rows, T, L, out, ld_out,  \
-                                                      err, max_items, sm_count, s))         \
-      break;                                                                                \
-    if (sls_variant() == 4 && try_sls_stream<LPR, VPL>(qd, tables, rows, T, L, out, ld_out, \
-                                                       err, max_items, sm_count, s))        \
       break;                                                                                \
     launch_sls_bag<LPR, VPL, (VPL == 2 ? 4 : 8)>(qd, tables, rows, T, L, out, ld_out, err,  \
                                                  max_items, sm_count, s);                   \
@@ -1198,10 +1222,7 @@ void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled,
   const int64_t pair_work = (int64_t)(T + 1) * T / 2 * D;
   if (D % 4 == 0 && D <= 64 && T + 1 <= 33 && per_item * kInterWarps <= 200 * 1024 &&
       pair_work <= 8192 && env_int("RS_INTER_WARP", 1)) {
-    static bool attr = cudaFuncSetAttribute(interaction_warp_kernel,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            200 * 1024) == cudaSuccess;
-    (void)attr;
+    smem_attr(reinterpret_cast<const void*>(interaction_warp_kernel), 200 * 1024);
     const int grid = grid_for(max_items, kInterWarps, sm_count, 2);
     launch_pdl(interaction_warp_kernel, dim3(grid), dim3(kInterWarps * 32),
                per_item * kInterWarps, s, qd, pooled, ld_pooled, T, D, X, ld_x, sum_off,

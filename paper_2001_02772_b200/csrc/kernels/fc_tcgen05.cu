@@ -112,7 +112,11 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   // split-K: grid.z = batch x splits; this CTA accumulates k-blocks
   // [kb0, kb0 + nk) of the tile and the last of its splits to arrive sums the
   // partials in split order (deterministic) and runs the epilogue
+#if RS_EXPERIMENTS
   const int splits = a.splits > 1 ? a.splits : 1;
+#else
+  constexpr int splits = 1;
+#endif
   const int z = blockIdx.z / splits, sp = blockIdx.z - (blockIdx.z / splits) * splits;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   if (m0 >= M) return;
@@ -213,6 +217,7 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
     pdl_trigger();
     const int quad = warp;
     const int64_t m = m0 + quad * 32 + lane;
+#if RS_EXPERIMENTS
     if (splits > 1) {
       // partial tile -> workspace; the last split to arrive reduces
       const int64_t tile = ((int64_t)z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -295,7 +300,9 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
             if (nb + i < a.N) C[nb + i] = y[i];
         }
       }
-    } else {
+    } else
+#endif  // RS_EXPERIMENTS
+    {
     float* __restrict__ Cb = (a.c_desc && qd->out) ? qd->out : a.C;
     float* __restrict__ C = Cb + (int64_t)z * a.sCz + m * a.ldc;
     const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
@@ -413,14 +420,12 @@ size_t tc_smem_bytes() {
 }
 
 template <int BN, int STAGES>
-void set_attr_once() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(fc_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)tc_smem_bytes<BN, STAGES>());
-  });
+void set_attr_once() {  // once per device (common.cuh smem_attr)
+  smem_attr(reinterpret_cast<const void*>(fc_tc_kernel<BN, STAGES>),
+            (int)tc_smem_bytes<BN, STAGES>());
 }
 
+#if RS_EXPERIMENTS  // measured slower (DESIGN.md Appendix RS_FC_CHAIN)
 // ---------------------------------------------------------------------------
 // fc_chain_kernel: a whole FC stack per 128-row tile (see TcChainPlan).
 // Warps 0-3: epilogue (TMEM lanes 32w..32w+31 = tile rows) and, between
@@ -654,6 +659,7 @@ fc_chain_kernel(const QDesc* __restrict__ qd, const __grid_constant__ TcChainPla
                  : "memory");
   }
 }
+#endif  // RS_EXPERIMENTS
 
 }  // namespace
 
@@ -744,6 +750,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   p->splits = 1;
   p->ws = nullptr;
   p->cnt = nullptr;
+#if RS_EXPERIMENTS
   const char* sk = getenv("RS_SPLITK");
   const int nk = (a.K + BK - 1) / BK;
   if (pool && a.N2 == 0 && nk >= 32 && sk && atoi(sk) > 1) {
@@ -759,6 +766,9 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
       pool->cnt_used += tiles;
     }
   }
+#else
+  (void)pool;
+#endif
   return true;
 }
 
@@ -768,6 +778,10 @@ bool tc_chain_plan(TcChainPlan* p, const FcArgs* ly, int L, int64_t m_cap, int64
   // 52 -> 67 us alone): a chain CTA must own whole rows, so a 256-wide layer
   // runs on half the CTAs the per-layer kernels use, and the launches saved
   // do not pay for the lost parallelism.
+#if !RS_EXPERIMENTS
+  (void)p; (void)ly; (void)L; (void)m_cap; (void)a_rows;
+  return false;
+#else
   if (!tc_available() || L < 1) return false;
   const char* e = getenv("RS_FC_CHAIN");
   if (!e || !atoi(e)) return false;
@@ -821,17 +835,18 @@ bool tc_chain_plan(TcChainPlan* p, const FcArgs* ly, int L, int64_t m_cap, int64
   p->stages = std::min(kChainMaxStages, kChainRingBytes / p->slot);
   if (p->stages < 2) return false;
   p->m_tiles = (int)((m_cap + BM - 1) / BM);
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(fc_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(ChainSmem) + 1024));
-  });
+  smem_attr(reinterpret_cast<const void*>(fc_chain_kernel), (int)(sizeof(ChainSmem) + 1024));
   return true;
+#endif  // RS_EXPERIMENTS
 }
 
 void launch_fc_chain(const QDesc* qd, const TcChainPlan& p, cudaStream_t s) {
+#if RS_EXPERIMENTS
   launch_pdl(fc_chain_kernel, dim3(p.m_tiles), dim3(kChainThreads), sizeof(ChainSmem) + 1024, s,
              qd, p);
+#else
+  (void)qd; (void)p; (void)s;
+#endif
 }
 
 void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a0, cudaStream_t s) {

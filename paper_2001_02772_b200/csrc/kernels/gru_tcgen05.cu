@@ -380,11 +380,7 @@ gru_tc_kernel(const QDesc* __restrict__ qd, GruArgs g) {
 template <int D, int H>
 void launch_typed(const QDesc* qd, const GruArgs& g, int64_t max_items, cudaStream_t s) {
   const size_t smem = sizeof(GruTcSmem<D, H>) + 1024;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    cudaFuncSetAttribute(gru_tc_kernel<D, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  });
+  smem_attr(reinterpret_cast<const void*>(gru_tc_kernel<D, H>), (int)smem);
   const dim3 grid((unsigned)((max_items + kSeq - 1) / kSeq), g.T);
   max_carveout(reinterpret_cast<const void*>(gru_tc_kernel<D, H>));
   gru_tc_kernel<D, H><<<grid, GruThreads<H>::N, smem, s>>>(qd, g);

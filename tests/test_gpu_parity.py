@@ -15,6 +15,10 @@ from parity_rule import FP32, TF32, assert_attention_pooled, assert_close, asser
 
 pytestmark = pytest.mark.gpu
 
+# measured-slower alternatives exist only in an experiments build (make EXPERIMENTS=1)
+needs_experiments = pytest.mark.skipif(not rs.experiments_built(),
+                                       reason="library built without EXPERIMENTS=1")
+
 # path labels kept as the tolerance argument of check_forward
 FP32_TOL = FP32
 TF32_TOL = TF32
@@ -224,7 +228,7 @@ def test_dien_tensor_core_recurrence(augru, L):
                       max_q=256)
 
 
-@pytest.mark.parametrize("desc_memop", ["0", "1"])
+@pytest.mark.parametrize("desc_memop", ["0", pytest.param("1", marks=needs_experiments)])
 def test_forward_many_long_batch_host_runs_ahead(desc_memop, monkeypatch):
     """2000 small queries over 2 lanes: the host enqueues far ahead of the GPU,
     so every query must carry its own descriptor (item count, pointers) by
@@ -257,7 +261,9 @@ def test_forward_many_long_batch_host_runs_ahead(desc_memop, monkeypatch):
     acc.close()
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
+@pytest.mark.parametrize("variant", ["0", pytest.param("1", marks=needs_experiments), "2",
+                                     pytest.param("3", marks=needs_experiments),
+                                     pytest.param("4", marks=needs_experiments)])
 @pytest.mark.parametrize("D,L", [(32, 80), (64, 80), (64, 20), (128, 33), (256, 7)])
 def test_sls_kernel_variants_bit_exact(variant, D, L, monkeypatch):
     """Every SLS kernel variant (RS_SLS_VARIANT) reproduces the oracle's
@@ -447,6 +453,7 @@ def test_bf16_dense_variant_matches_rounded_fp32(name):
     acc.close()
 
 
+@needs_experiments
 @pytest.mark.parametrize("name", ["DLRM-RMC1", "DIN", "NCF"])
 def test_fc_chain_kernel_parity(name, monkeypatch):
     """The whole-stack tcgen05 kernel (RS_FC_CHAIN=1, off by default — measured
@@ -512,6 +519,7 @@ def test_queue_edge_cases():
     acc.close()
 
 
+@needs_experiments
 @pytest.mark.parametrize("splits", ["2", "4"])
 def test_split_k_parity(splits, monkeypatch):
     """Split-K tcgen05 layers (RS_SPLITK=n, off by default — measured slower):
@@ -606,4 +614,43 @@ def test_service_breakdown_is_a_measured_service_time():
     assert all(v >= 0 for v in pc.values())
     assert pc["EmbeddingLookup"] > pc["DenseFC"] and pc["PredictFC"] > 0
     assert pc["Attention"] == 0 and pc["Recurrent"] == 0
+    acc.close()
+
+
+def test_serve_hybrid_cpu_and_gpu():
+    """rs_serve_hybrid: DeepRecSched in real time — queries above T go whole to
+    the B200 replica (the tf32 rule of the oracle, bit-identical to rs_forward),
+    the rest run as B-item requests on host worker threads (bit-identical to
+    the host forward); the offload flags follow the strict S > T rule."""
+    spec = rs.builtin_model("DLRM-RMC1")
+    rows = 5000
+    acc = rs.Accelerator(spec, rows, seed=6, max_query_size=400, fc_mode=rs.FC_AUTO)
+    host = rs.HostModel(spec, rows, seed=6)
+    orc = Oracle(spec, rows, seed=6)
+    sizes = [5, 300, 64, 65, 200, 1, 399, 120]
+    T, B = 100, 32
+    qs = [rs.fill_query(spec, rows, 2, k, S) for k, S in enumerate(sizes)]
+    hb = []
+    for d, i in qs:
+        b = rs.PinnedBuffer(d.nbytes + i.nbytes)
+        raw = b.view(np.uint8, (d.nbytes + i.nbytes,))
+        raw[:d.nbytes] = d.reshape(-1).view(np.uint8)
+        raw[d.nbytes:] = i.reshape(-1).view(np.uint8)
+        hb.append((b, d.nbytes))
+    outs = [rs.PinnedBuffer(S * acc.output_dim * 4) for S in sizes]
+    batch = acc.batch(sizes, [b.ptr for b, _ in hb], [b.ptr + n for b, n in hb],
+                      [o.ptr for o in outs], rs.MEM_HOST)
+    lat, off = rs.serve_hybrid(host, 4, B, T, [acc], batch, np.arange(len(sizes)) * 5e-4)
+    assert list(off) == [int(S > T) for S in sizes]
+    assert (lat > 0).all()
+    for k, ((d, i), S) in enumerate(zip(qs, sizes)):
+        got = outs[k].view(np.float32, (S, acc.output_dim)).copy()
+        ref, mag, _, _ = orc.forward64(d, i)
+        if off[k]:
+            assert_close(got, ref, mag, TF32, f"hybrid gpu query {k}")
+            assert np.array_equal(got, acc.forward(d, i))
+        else:
+            assert_close(got, ref, mag, FP32, f"hybrid cpu query {k}")
+            assert np.array_equal(got, host.forward(d, i))
+    host.close()
     acc.close()
