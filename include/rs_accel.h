@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 2
+#define RS_ABI_VERSION 3
 
 /* ---- error codes -------------------------------------------------------- */
 enum {
@@ -366,10 +366,12 @@ int rs_host_sls(const float* tables, int64_t rows_per_table, int32_t num_tables,
 /* Fully connected layer on the host cores (the GEMM half of
  * the CPU side of the split; replaces the costed DenseFC/PredictFC flops of
  * cpu_service_time, proj/src/platform.cpp:71-103):
- * y[rows][out] = act(bias + x[rows][in] * weight^T), weight f32[out][in]
- * (the device layout), bias may be NULL, relu != 0 applies ReLU. fp32 with
- * FMA; DESIGN.md §4 tolerance, not bit identity. threads <= 0: all.       */
-int rs_host_fc(const float* x, int64_t rows, int32_t in_dim, const float* weight,
+ * y[rows][out] = act(bias + x[rows][in] * weight^T), weight f32[out][ldw]
+ * (row stride ldw >= in; 0 = in — the device layout pads rows to
+ * round4(in), so device-layout weights pass as is), bias may be
+ * NULL, relu != 0 applies ReLU. fp32 with FMA; DESIGN.md §4 tolerance, not
+ * bit identity. threads <= 0: every core this process may run on.          */
+int rs_host_fc(const float* x, int64_t rows, int32_t in_dim, const float* weight, int64_t ldw,
                const float* bias, int32_t out_dim, int32_t relu, float* y,
                int32_t threads);
 

@@ -206,8 +206,8 @@ _sig("rs_service_breakdown", C.c_int, C.c_void_p, C.c_int64, P(C.c_double), P(C.
      P(C.c_double))
 _sig("rs_host_sls", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
      C.c_int64, C.c_void_p, C.c_void_p, C.c_int32)
-_sig("rs_host_fc", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
-     C.c_int32, C.c_int32, C.c_void_p, C.c_int32)
+_sig("rs_host_fc", C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
+     C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32)
 _sig("rs_fill_query", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
      C.c_void_p, C.c_void_p)
 _sig("rs_fill_query_zipf", C.c_int, P(CModelDesc), C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
@@ -505,20 +505,24 @@ def host_sls(tables: np.ndarray, idx: np.ndarray, threads: int = 0) -> np.ndarra
 
 
 def host_fc(x: np.ndarray, weight: np.ndarray, bias: Optional[np.ndarray] = None,
-            relu: bool = True, threads: int = 0) -> np.ndarray:
+            relu: bool = True, threads: int = 0, in_dim: Optional[int] = None) -> np.ndarray:
     """Fully connected layer on the host cores: x f32[M, in],
-    weight f32[out, in] (device layout), bias f32[out] or None -> f32[M, out]."""
+    weight f32[out, ldw] with ldw >= in (the device layout pads rows to
+    round4(in); pass in_dim when the weight rows are padded), bias f32[out] or
+    None -> f32[M, out]."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     weight = np.ascontiguousarray(weight, dtype=np.float32)
     M, K = x.shape
-    N, Kw = weight.shape
-    if Kw != K:
-        raise InvalidArgument(f"weight is [{N}, {Kw}], x has {K} features")
+    N, ldw = weight.shape
+    if in_dim is not None and in_dim != K:
+        raise InvalidArgument(f"in_dim {in_dim} but x has {K} features")
+    if ldw < K or (in_dim is None and ldw != K):
+        raise InvalidArgument(f"weight is [{N}, {ldw}], x has {K} features")
     b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
     if b is not None and b.shape != (N,):
         raise InvalidArgument(f"bias shape {b.shape}, expected ({N},)")
     y = np.empty((M, N), dtype=np.float32)
-    _check(_lib.rs_host_fc(x.ctypes.data, M, K, weight.ctypes.data,
+    _check(_lib.rs_host_fc(x.ctypes.data, M, K, weight.ctypes.data, ldw,
                            None if b is None else b.ctypes.data, N, int(relu),
                            y.ctypes.data, int(threads)))
     return y

@@ -223,6 +223,19 @@ std::vector<float> fill_param(uint64_t seed, uint64_t id, int64_t n, float bound
 // access-policy window keeps in the persisting L2 set-aside, so hot rows stay
 // resident while the cold gathers stream past them. A pure copy — the SLS
 // result does not depend on which of the two copies a row is read from.
+struct HotDevice {
+  int users = 0;
+  size_t saved_limit = 0;
+};
+std::mutex& hot_mu() {
+  static std::mutex m;
+  return m;
+}
+std::map<int, HotDevice>& hot_devices() {
+  static std::map<int, HotDevice> d;
+  return d;
+}
+
 void setup_hot(rs_accel* a) {
   cudaDeviceProp prop;
   RS_CUDA(cudaGetDeviceProperties(&prop, a->device));
@@ -240,7 +253,20 @@ void setup_hot(rs_accel* a) {
                             w, (size_t)a->T, cudaMemcpyDeviceToDevice, a->own));
   size_t cur = 0;
   RS_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  std::lock_guard<std::mutex> g(hot_mu());
+  HotDevice& hd = hot_devices()[a->device];
+  if (hd.users++ == 0) hd.saved_limit = cur;  // the first hot handle remembers the limit
   if (cur < a->hot_bytes) RS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, a->hot_bytes));
+}
+
+// The last hot-block handle of a device drops the persisting lines and puts
+// the set-aside limit back; earlier ones leave other handles' blocks alone.
+void release_hot(rs_accel* a) {
+  std::lock_guard<std::mutex> g(hot_mu());
+  HotDevice& hd = hot_devices()[a->device];
+  if (--hd.users > 0) return;
+  cudaCtxResetPersistingL2Cache();
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, hd.saved_limit);
 }
 
 
@@ -575,7 +601,7 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
     if (m.pooling == RS_POOL_SUM && a->T > 0 && !(skip & 2))
       launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
                          a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
-                         s->dense_sms, st);
+                         s->dense_sms, st, tc);
     if (const char* de = getenv("RS_DIAG_EMPTY")) {
       const char* dc = getenv("RS_DIAG_EMPTY_CTAS");
       launch_diag_empty(atoi(de), dc ? atoi(dc) : 1, st);
@@ -1390,7 +1416,7 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
       if (a->lane[d]) cudaStreamDestroy(a->lane[d]);
       if (a->lane_join[d]) cudaEventDestroy(a->lane_join[d]);
     }
-    if (a->hot) cudaCtxResetPersistingL2Cache();
+    if (a->hot) release_hot(a);
     for (void* p : a->allocs) cudaFree(p);
     if (a->own) cudaStreamDestroy(a->own);
 #if RS_EXPERIMENTS

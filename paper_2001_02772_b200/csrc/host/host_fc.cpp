@@ -113,32 +113,35 @@ void host_fc_rows(const float* x, int64_t m0, int64_t m1, int K, int N, const fl
 }  // namespace rs
 
 extern "C" int rs_host_fc(const float* x, int64_t rows, int32_t in_dim, const float* weight,
-                          const float* bias, int32_t out_dim, int32_t relu, float* y,
-                          int32_t threads) {
+                          int64_t ldw, const float* bias, int32_t out_dim, int32_t relu,
+                          float* y, int32_t threads) {
   using namespace rs;
-  clear_error();
-  if (rows < 0 || in_dim < 0 || out_dim < 1)
-    return fail(RS_E_INVALID, "rs_host_fc: bad shape");
-  if (rows == 0) return RS_OK;
-  if (!y || (in_dim > 0 && (!x || !weight))) return fail(RS_E_INVALID, "rs_host_fc: null buffer");
-  std::vector<float> wt((size_t)in_dim * out_dim);
-  for (int n = 0; n < out_dim; ++n)
-    for (int k = 0; k < in_dim; ++k) wt[(size_t)k * out_dim + n] = weight[(size_t)n * in_dim + k];
-  int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
-  nt = (int)std::min<int64_t>(nt, (rows + kRows - 1) / kRows);
-  auto run = [&](int i) {
-    const int64_t blocks = (rows + kRows - 1) / kRows;
-    const int64_t m0 = std::min(rows, blocks * i / nt * kRows);
-    const int64_t m1 = std::min(rows, blocks * (i + 1) / nt * kRows);
-    fc_rows(x, m0, m1, in_dim, out_dim, wt.data(), bias, relu, y);
-  };
-  if (nt == 1) {
-    run(0);
-  } else {
-    std::vector<std::thread> pool;
-    pool.reserve(nt);
-    for (int i = 0; i < nt; ++i) pool.emplace_back(run, i);
-    for (auto& th : pool) th.join();
-  }
-  return RS_OK;
+  return guarded([&] {
+    if (rows < 0 || in_dim < 0 || out_dim < 1) raise(RS_E_INVALID, "rs_host_fc: bad shape");
+    if (ldw == 0) ldw = in_dim;
+    if (ldw < in_dim) raise(RS_E_INVALID, "rs_host_fc: ldw < in_dim");
+    if (rows == 0) return;
+    if (!y || (in_dim > 0 && (!x || !weight))) raise(RS_E_INVALID, "rs_host_fc: null buffer");
+    // W^T [in][out] (row stride ldw of the caller's [out][ldw] weight: the
+    // device layout pads rows to round4(in))
+    std::vector<float> wt((size_t)in_dim * out_dim);
+    for (int n = 0; n < out_dim; ++n)
+      for (int k = 0; k < in_dim; ++k) wt[(size_t)k * out_dim + n] = weight[(size_t)n * ldw + k];
+    int nt = threads > 0 ? threads : host_cores();
+    nt = (int)std::min<int64_t>(nt, (rows + kRows - 1) / kRows);
+    auto run = [&](int i) {
+      const int64_t blocks = (rows + kRows - 1) / kRows;
+      const int64_t m0 = std::min(rows, blocks * i / nt * kRows);
+      const int64_t m1 = std::min(rows, blocks * (i + 1) / nt * kRows);
+      fc_rows(x, m0, m1, in_dim, out_dim, wt.data(), bias, relu, y);
+    };
+    if (nt == 1) {
+      run(0);
+    } else {
+      std::vector<std::thread> pool;
+      pool.reserve(nt);
+      for (int i = 0; i < nt; ++i) pool.emplace_back(run, i);
+      for (auto& th : pool) th.join();
+    }
+  });
 }

@@ -85,20 +85,20 @@ extern "C" int rs_host_sls(const float* tables, int64_t rows_per_table, int32_t 
                            int32_t lookups, int32_t dim, int64_t query_size,
                            const int64_t* indices, float* pooled, int32_t threads) {
   using namespace rs;
-  clear_error();
+  return guarded([&] {
   if (query_size < 0 || rows_per_table < 1 || num_tables < 1 || lookups < 0 || dim < 1 ||
       dim > 4096)
-    return fail(RS_E_INVALID, "rs_host_sls: bad shape");
+    raise(RS_E_INVALID, "rs_host_sls: bad shape");
   const int64_t bags = query_size * num_tables;
-  if (bags == 0) return RS_OK;
+  if (bags == 0) return;
   if (!tables || !pooled || (lookups > 0 && !indices))
-    return fail(RS_E_INVALID, "rs_host_sls: null buffer");
+    raise(RS_E_INVALID, "rs_host_sls: null buffer");
   const int R = canonical_r(dim);
   static const int pf = [] {  // lookups prefetched ahead (RS_HOST_PREFETCH)
     const char* v = getenv("RS_HOST_PREFETCH");
     return v ? std::max(1, atoi(v)) : 8;
   }();
-  int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  int nt = threads > 0 ? threads : host_cores();
   nt = (int)std::min<int64_t>(nt, bags);
   std::vector<int64_t> bad(nt, -1);
   auto run = [&](int i) {
@@ -117,11 +117,10 @@ extern "C" int rs_host_sls(const float* tables, int64_t rows_per_table, int32_t 
   for (int i = 0; i < nt; ++i)
     if (bad[i] >= 0) {
       const int64_t bag = bad[i] / std::max(lookups, 1), l = bad[i] % std::max(lookups, 1);
-      return fail(RS_E_INDEX, "rs_host_sls: index " + std::to_string(indices[bad[i]]) +
-                                  " outside [0, " + std::to_string(rows_per_table) +
-                                  ") at item " + std::to_string(bag / num_tables) + ", table " +
-                                  std::to_string(bag % num_tables) + ", lookup " +
-                                  std::to_string(l));
+      raise(RS_E_INDEX, "rs_host_sls: index " + std::to_string(indices[bad[i]]) +
+                            " outside [0, " + std::to_string(rows_per_table) + ") at item " +
+                            std::to_string(bag / num_tables) + ", table " +
+                            std::to_string(bag % num_tables) + ", lookup " + std::to_string(l));
     }
-  return RS_OK;
+  });
 }

@@ -1211,9 +1211,132 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// interaction_tc_kernel: the DLRM dot interaction (model_zoo.cpp:231-238) on the
+// tensor cores, for the tcgen05 (tf32) forward graph. One WARP per item: the
+// item's R = T+1 vectors (v0 = dense_out, v_t = pooled_t, D floats each) are
+// staged in shared memory by cp.async, the Gram matrix G = V V^T is formed by
+// mma.sync.m16n8k8 tf32 tiles covering the strict lower triangle (j < i), and
+// G[i][j] lands in X[item][dot_off + i(i-1)/2 + j]; lanes also write the summed
+// embedding X[item][sum_off + c] = sum_t pooled_t[c] (fp32, t in order).
+// Per item ~80 MMAs + ~180 shared loads for cfg3 (33 x 64) instead of 33.8K
+// dependent FMAs: the stage's SM time in the pipelined queue is what it costs
+// the concurrent gathers (tools/pipe_diag.py). tf32 operands (rounded, cvt.rna)
+// -> the tf32 tolerance of the graph's FC layers (tests/parity_rule.py).
+constexpr int kInterTcWarps = 4;
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kInterTcWarps * 32)
+interaction_tc_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
+                      int64_t ld_pooled, int T, float* __restrict__ X, int64_t ld_x,
+                      int64_t sum_off, int64_t dot_off) {
+  constexpr int LDV = D + 4;  // row stride: conflict-free fragment loads
+  extern __shared__ float smem_v[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = T + 1;
+  float* __restrict__ V = smem_v + (size_t)warp * R * LDV;
+  const int g = lane >> 2, tig = lane & 3;
+  const int mtiles = (R + 15) / 16, ntiles = (R - 1 + 7) / 8;
+  pdl_wait();  // pooled (SLS) and X[:, 0:D] (bottom MLP) are predecessors' outputs
+  const int64_t S = qd->S;
+  for (int64_t item = (int64_t)blockIdx.x * kInterTcWarps + warp; item < S;
+       item += (int64_t)gridDim.x * kInterTcWarps) {
+    __syncwarp();
+    // stage the R vectors: 16-byte cp.async per lane, all in flight at once
+    constexpr int D4 = D / 4;
+    for (int u = lane; u < R * D4; u += 32) {
+      const int v = u / D4, c4 = u - v * D4;
+      const float* src = v == 0 ? X + item * ld_x + c4 * 4
+                                : pooled + item * ld_pooled + (int64_t)(v - 1) * D + c4 * 4;
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(V + v * LDV + c4 * 4));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    // summed embedding (D9): lanes over columns, tables in order
+    for (int c = lane; c < D; c += 32) {
+      float s = 0.f;
+      for (int t = 1; t <= T; ++t) s += V[t * LDV + c];
+      X[item * ld_x + sum_off + c] = s;
+    }
+    // strict lower triangle of V V^T by m16n8k8 tiles (rows i, cols j < i)
+    for (int mt = 0; mt < mtiles; ++mt) {
+      const int r0 = mt * 16 + g, r1 = r0 + 8;
+      const int nt_end = min(ntiles, (mt * 16 + 15) / 8 + 1);
+      float acc[8][4];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+#pragma unroll 2
+      for (int k0 = 0; k0 < D; k0 += 8) {
+        const uint32_t a0 = r0 < R ? to_tf32(V[r0 * LDV + k0 + tig]) : 0u;
+        const uint32_t a1 = r1 < R ? to_tf32(V[r1 * LDV + k0 + tig]) : 0u;
+        const uint32_t a2 = r0 < R ? to_tf32(V[r0 * LDV + k0 + tig + 4]) : 0u;
+        const uint32_t a3 = r1 < R ? to_tf32(V[r1 * LDV + k0 + tig + 4]) : 0u;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          if (nt >= nt_end) break;
+          const int cj = nt * 8 + g;
+          const uint32_t b0 = cj < R ? to_tf32(V[cj * LDV + k0 + tig]) : 0u;
+          const uint32_t b1 = cj < R ? to_tf32(V[cj * LDV + k0 + tig + 4]) : 0u;
+          asm volatile(
+              "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 "
+              "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+              : "+f"(acc[nt][0]), "+f"(acc[nt][1]), "+f"(acc[nt][2]), "+f"(acc[nt][3])
+              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+        }
+      }
+      float* __restrict__ xo = X + item * ld_x + dot_off;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        if (nt >= nt_end) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = (q < 2) ? r0 : r1;
+          const int j = nt * 8 + 2 * tig + (q & 1);
+          if (i < R && j < i) xo[i * (i - 1) / 2 + j] = acc[nt][q];
+        }
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+bool interaction_tc_supported(int T, int D) {
+  return (D == 32 || D == 64 || D == 128) && T + 1 <= 64 &&
+         (size_t)(T + 1) * (D + 4) * 4 * kInterTcWarps <= 200 * 1024;
+}
+
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
-                        int64_t max_items, int sm_count, cudaStream_t s) {
+                        int64_t max_items, int sm_count, cudaStream_t s, bool tc) {
+  // tcgen05 graph: the tensor-core Gram interaction (tf32 like the FC layers)
+  if (tc && has_dense && interaction_tc_supported(T, D) && env_int("RS_INTER_TC", 1)) {
+    const size_t smem = (size_t)(T + 1) * (D + 4) * sizeof(float) * kInterTcWarps;
+    // one warp per item, items spread over ~half the SMs' worth of CTAs
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
+        (max_items + kInterTcWarps - 1) / kInterTcWarps, (int64_t)sm_count));
+#define RS_ITC(DD)                                                                            \
+  do {                                                                                        \
+    smem_attr(reinterpret_cast<const void*>(interaction_tc_kernel<DD>), (int)smem);           \
+    launch_pdl(interaction_tc_kernel<DD>, dim3(grid), dim3(kInterTcWarps * 32), smem, s, qd,  \
+               pooled, ld_pooled, T, X, ld_x, sum_off, dot_off);                              \
+  } while (0)
+    switch (D) {
+      case 32: RS_ITC(32); break;
+      case 64: RS_ITC(64); break;
+      default: RS_ITC(128); break;
+    }
+#undef RS_ITC
+    return;
+  }
   const size_t per_item = (size_t)(T + 1) * (D + 1) * sizeof(float);
   // warp-per-item only while an item's dot work is short: one warp runs each
   // dot as a dependent FMA chain, so at cfg3's 528 pairs x 64 it lengthens the

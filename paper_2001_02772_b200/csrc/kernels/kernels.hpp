@@ -43,7 +43,7 @@ void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t l
                         int64_t max_items, int sm_count, cudaStream_t s);
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
-                        int64_t max_items, int sm_count, cudaStream_t s);
+                        int64_t max_items, int sm_count, cudaStream_t s, bool tc = false);
 size_t interaction_smem(int T, int D);
 void launch_init_tables(float* tables, int64_t T, int64_t rows, int64_t D, uint64_t seed,
                         int sm_count, cudaStream_t s);

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol(rs):
 
 
 def test_abi_version(rs):
-    assert rs._lib.rs_abi_version() == 2
+    assert rs._lib.rs_abi_version() == 3
 
 
 def test_errors_cross_the_abi_as_codes(rs):

@@ -105,3 +105,21 @@ def test_host_fc_edges():
         rs.host_fc(x, np.ones((2, 5), np.float32))
     with pytest.raises(rs.InvalidArgument):
         rs.host_fc(x, w, np.ones(3, np.float32))
+
+
+def test_host_fc_takes_device_layout_padded_weights():
+    """the device keeps weights [out][round4(in)] zero-padded; an
+    in % 4 != 0 layer (RMC1's 13-input bottom layer) passes them as is with
+    ldw = round4(in) and gives the same y as the unpadded weight."""
+    rng = np.random.default_rng(5)
+    M, K, N = 9, 13, 24
+    x = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    w = rng.uniform(-0.3, 0.3, (N, K)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, N).astype(np.float32)
+    padded = np.zeros((N, 16), np.float32)
+    padded[:, :K] = w
+    padded[:, K:] = 7.0  # the pad columns must never be read
+    y = rs.host_fc(x, padded, b, relu=True, in_dim=K)
+    assert np.array_equal(y, rs.host_fc(x, w, b, relu=True))
+    with pytest.raises(rs.InvalidArgument):
+        rs.host_fc(x, np.ones((N, 12), np.float32), b, in_dim=K)  # ldw < in
