@@ -730,12 +730,29 @@ def run_serve(args):
     pool_of = np.arange(n) % P
     prepared = batch_for(pool_of)
     warm = int(0.1 * n)
+    host = None
+    if args.hybrid_threshold > 0:
+        if device_inputs:
+            raise SystemExit("--hybrid-threshold serves host queries")
+        # DeepRecSched for real: queries <= T as B-item requests on host cores
+        host = rs.HostModel(spec, rows, seed=1)
+        cores = args.cpu_cores or max(1, (os.cpu_count() or 2) - K - 2)
+    offl = {"fraction": None}
+
+    def run_once(arr):
+        if host is None:
+            return rs.serve(reps, prepared, arr)
+        lat, off = rs.serve_hybrid(host, cores, args.cpu_batch, args.hybrid_threshold, reps,
+                                   prepared, arr)
+        offl["fraction"] = float(np.sum(off * np.array(
+            [int(pool_sizes[j]) for j in pool_of])) / np.sum([int(pool_sizes[j]) for j in pool_of]))
+        return lat
 
     def evaluate(lam, eval_idx):
         arr, _ = rs.gen_trace(seed + eval_idx, lam, dist, n)  # Poisson gaps at rate lam
         arr = arr - arr[0]
         t0 = time.time()
-        lat = rs.serve(reps, prepared, arr) * 1e-3
+        lat = run_once(arr) * 1e-3
         wall = time.time() - t0
         post = lat[warm:]
         p95 = float(np.sort(post)[max(int(math.ceil(0.95 * len(post))), 1) - 1])
@@ -747,7 +764,7 @@ def run_serve(args):
     # warm-up, then a burst (all arrivals at t=0): the saturated throughput
     rs.serve(reps, batch_for(pool_of[:min(n, 2000)]), np.zeros(min(n, 2000)))
     t0 = time.time()
-    lat = rs.serve(reps, prepared, np.zeros(n))
+    lat = run_once(np.zeros(n))
     burst_qps = n / (float(lat.max()) * 1e-3)
     evals = []
     lo, hi = 0.5 * burst_qps, 1.5 * burst_qps
@@ -788,12 +805,19 @@ def run_serve(args):
             "burst": {"qps": burst_qps, "queries": n,
                       "method": "all n arrivals at t=0: saturated real throughput"},
             "stable_load": stable, "evaluations": evals,
+            "hybrid": None if host is None else {
+                "threshold": args.hybrid_threshold, "cpu_batch": args.cpu_batch,
+                "cpu_cores": cores, "offloaded_item_fraction": offl["fraction"],
+                "rule": "S > T whole to the least-loaded replica, else floor(S/B) x B + S mod B "
+                        "requests on host worker threads (rs_serve_hybrid, sim.cpp:173-191)"},
             "method": "rs_serve real-time executor: host clock releases, least-outstanding-"
                       "items routing, one dispatcher thread per replica, CUDA-event "
                       "completions; reference search rule (sim.cpp:246-290) over real runs"}
     print(json.dumps(line), flush=True)
     for r in reps:
         r.close()
+    if host is not None:
+        host.close()
 
 
 def main():
@@ -834,6 +858,12 @@ def main():
                     help="real-time serving over --gpus replicas in one process (rs_serve)")
     ap.add_argument("--serve-inputs", choices=["host", "device"], default="host",
                     help="--serve: host pinned inputs (e2e) or device-resident (--gpus 1)")
+    ap.add_argument("--hybrid-threshold", type=int, default=0,
+                    help="--serve: >0 = DeepRecSched hybrid, queries of <= T items on host cores")
+    ap.add_argument("--cpu-batch", type=int, default=4,
+                    help="--serve --hybrid-threshold: CPU request size B")
+    ap.add_argument("--cpu-cores", type=int, default=0,
+                    help="--serve --hybrid-threshold: host worker threads (0: nproc - K - 2)")
     ap.add_argument("--serve-n", type=int, default=50_000,
                     help="--serve: queries per evaluation (reference n = 50,000)")
     args = ap.parse_args()

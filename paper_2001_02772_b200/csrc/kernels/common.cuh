@@ -5,6 +5,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <map>
 #include <set>
 #include <utility>
 
@@ -128,12 +129,18 @@ inline int current_device() {
   cudaGetDevice(&d);
   return d;
 }
+// The attribute is a per-function maximum: raised whenever a launch needs more
+// than any earlier one on this device (kernels whose shared memory depends on
+// the model shape, e.g. the interaction's (T+1) x D staging).
 inline void smem_attr(const void* fn, int bytes) {
   static std::mutex mu;
-  static std::set<std::pair<int, const void*>> done;
+  static std::map<std::pair<int, const void*>, int> done;
   std::lock_guard<std::mutex> g(mu);
-  if (done.insert({current_device(), fn}).second)
+  int& cur = done[{current_device(), fn}];
+  if (bytes > cur) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cur = bytes;
+  }
 }
 
 inline void max_carveout(const void* fn) {

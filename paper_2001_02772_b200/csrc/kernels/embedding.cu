@@ -255,7 +255,7 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
 // bag's rows stream, and row batch j+1 is in flight while batch j accumulates.
 // Same per-lane accumulation order as sls_sum_kernel (bit-identical results).
 // Bags of up to 32*IPL lookups; longer bags use sls_sum_kernel.
-template <int LPR, int VPL, int U, int IPL, bool HOT>
+template <int LPR, int VPL, int U, int IPL, bool HOT, bool EF = false>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                 int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
@@ -270,6 +270,9 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
   const int64_t* __restrict__ idx = qd->idx;
   const int nw = blockDim.x >> 5;  // warps per CTA (<= kWarps; RS_SLS_WPC)
   const int64_t stride = (int64_t)gridDim.x * nw;
+  // EF: table rows marked evict-first in L2, so the once-touched gather stream
+  // does not push the dense stages' reused data (weights, X, pooled) out
+  const uint64_t pol = EF ? l2_evict_first_policy() : 0;
   int64_t nidx[IPL];
   auto fetch_idx = [&](int64_t bag) {
 #pragma unroll
@@ -305,7 +308,8 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
             ok[u] = true;
             const float4* p = (HOT && r < hot_rows ? htab : tab) + r * (D / 4) + c;
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) v[u][k] = ldg_stream(p + k * LPR);
+            for (int k = 0; k < VPL; ++k)
+              v[u][k] = EF ? ldg_stream_hint(p + k * LPR, pol) : ldg_stream(p + k * LPR);
           } else {
             atomicOr(err, kErrIndex);
           }
@@ -979,8 +983,17 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
                      float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
                      cudaStream_t s, const float* hot, int64_t hot_rows) {
   const int wpc = std::min(kWarps, std::max(1, env_int("RS_SLS_WPC", kWarps)));
+#if RS_EXPERIMENTS
+  // RS_SLS_EF=1: gather rows evict-first in L2 (measured +1.3% us/query in the
+  // pipelined queue, i.e. slower: tools/env_sweep.py)
+  const bool ef = env_int("RS_SLS_EF", 0) != 0;
+  auto kern = hot_rows > 0 ? sls_pipe_kernel<LPR, VPL, U, IPL, true>
+                           : (ef ? sls_pipe_kernel<LPR, VPL, U, IPL, false, true>
+                                 : sls_pipe_kernel<LPR, VPL, U, IPL, false>);
+#else
   auto kern = hot_rows > 0 ? sls_pipe_kernel<LPR, VPL, U, IPL, true>
                            : sls_pipe_kernel<LPR, VPL, U, IPL, false>;
+#endif
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, 0);
   per_sm = std::max(per_sm, 1);
@@ -1211,6 +1224,7 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
   }
 }
 
+#if RS_EXPERIMENTS  // measured slower in the pipelined queue
 // ---------------------------------------------------------------------------
 // interaction_tc_kernel: the DLRM dot interaction (model_zoo.cpp:231-238) on the
 // tensor cores, for the tcgen05 (tf32) forward graph. One WARP per item: the
@@ -1237,19 +1251,18 @@ interaction_tc_kernel(const QDesc* __restrict__ qd, const float* __restrict__ po
                       int64_t ld_pooled, int T, float* __restrict__ X, int64_t ld_x,
                       int64_t sum_off, int64_t dot_off) {
   constexpr int LDV = D + 4;  // row stride: conflict-free fragment loads
+  constexpr int D4 = D / 4;
   extern __shared__ float smem_v[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = T + 1;
-  float* __restrict__ V = smem_v + (size_t)warp * R * LDV;
+  // two item buffers per warp: item k+1's vectors land while item k's tiles run
+  float* __restrict__ Vbuf = smem_v + (size_t)warp * 2 * R * LDV;
   const int g = lane >> 2, tig = lane & 3;
   const int mtiles = (R + 15) / 16, ntiles = (R - 1 + 7) / 8;
   pdl_wait();  // pooled (SLS) and X[:, 0:D] (bottom MLP) are predecessors' outputs
   const int64_t S = qd->S;
-  for (int64_t item = (int64_t)blockIdx.x * kInterTcWarps + warp; item < S;
-       item += (int64_t)gridDim.x * kInterTcWarps) {
-    __syncwarp();
-    // stage the R vectors: 16-byte cp.async per lane, all in flight at once
-    constexpr int D4 = D / 4;
+  const int64_t step = (int64_t)gridDim.x * kInterTcWarps;
+  auto stage = [&](int64_t item, float* V) {
     for (int u = lane; u < R * D4; u += 32) {
       const int v = u / D4, c4 = u - v * D4;
       const float* src = v == 0 ? X + item * ld_x + c4 * 4
@@ -1257,7 +1270,19 @@ interaction_tc_kernel(const QDesc* __restrict__ qd, const float* __restrict__ po
       const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(V + v * LDV + c4 * 4));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int64_t item = (int64_t)blockIdx.x * kInterTcWarps + warp;
+  if (item < S) stage(item, Vbuf);
+  for (int buf = 0; item < S; item += step, buf ^= 1) {
+    float* __restrict__ V = Vbuf + buf * R * LDV;
+    const bool more = item + step < S;
+    if (more) {
+      stage(item + step, Vbuf + (buf ^ 1) * R * LDV);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncwarp();
     // summed embedding (D9): lanes over columns, tables in order
     for (int c = lane; c < D; c += 32) {
@@ -1305,24 +1330,35 @@ interaction_tc_kernel(const QDesc* __restrict__ qd, const float* __restrict__ po
         }
       }
     }
+    __syncwarp();  // this buffer is refilled two items from now
   }
   pdl_trigger();
 }
 
 bool interaction_tc_supported(int T, int D) {
   return (D == 32 || D == 64 || D == 128) && T + 1 <= 64 &&
-         (size_t)(T + 1) * (D + 4) * 4 * kInterTcWarps <= 200 * 1024;
+         (size_t)(T + 1) * (D + 4) * 4 * 2 * kInterTcWarps <= 200 * 1024;
 }
+
+#endif  // RS_EXPERIMENTS
 
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
                         int64_t max_items, int sm_count, cudaStream_t s, bool tc) {
-  // tcgen05 graph: the tensor-core Gram interaction (tf32 like the FC layers)
-  if (tc && has_dense && interaction_tc_supported(T, D) && env_int("RS_INTER_TC", 1)) {
-    const size_t smem = (size_t)(T + 1) * (D + 4) * sizeof(float) * kInterTcWarps;
-    // one warp per item, items spread over ~half the SMs' worth of CTAs
+#if RS_EXPERIMENTS
+  // tcgen05 graph, RS_INTER_TC=1: the tensor-core Gram interaction (tf32 like
+  // the FC layers). Measured 1 us/query SLOWER in the pipelined queue than the
+  // FFMA kernel below at every grid size (tools/env_sweep.py)
+  if (tc && has_dense && interaction_tc_supported(T, D) && env_int("RS_INTER_TC", 0)) {
+    const size_t smem = (size_t)(T + 1) * (D + 4) * sizeof(float) * 2 * kInterTcWarps;
+    // FEW CTAs, each warp streaming items with a one-item prefetch: in the
+    // pipelined queue every CTA of this grid displaces a gather CTA for its
+    // lifetime (tools/tl_analyze.py: the 296-CTA FFMA kernel stretched the
+    // concurrent SLS grids by ~8 us per query), so the stage is packed onto
+    // RS_INTER_CTAS (default 16) SMs
+    const int ctas = std::max(1, env_int("RS_INTER_CTAS", 16));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
-        (max_items + kInterTcWarps - 1) / kInterTcWarps, (int64_t)sm_count));
+        (max_items + kInterTcWarps - 1) / kInterTcWarps, (int64_t)ctas));
 #define RS_ITC(DD)                                                                            \
   do {                                                                                        \
     smem_attr(reinterpret_cast<const void*>(interaction_tc_kernel<DD>), (int)smem);           \
@@ -1337,6 +1373,9 @@ void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled,
 #undef RS_ITC
     return;
   }
+#else
+  (void)tc;
+#endif
   const size_t per_item = (size_t)(T + 1) * (D + 1) * sizeof(float);
   // warp-per-item only while an item's dot work is short: one warp runs each
   // dot as a dependent FMA chain, so at cfg3's 528 pairs x 64 it lengthens the
@@ -1405,7 +1444,10 @@ stage_dense_kernel(const QDesc* __restrict__ qd, int64_t dense_in, float* __rest
 void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t ld_dst,
                         int64_t max_items, int sm_count, cudaStream_t s) {
   const int64_t units = max_items * ((dense_in % 4 == 0) ? dense_in / 4 : dense_in);
-  const int grid = grid_for(units, 256, sm_count, 2);
+  // a few hundred KB per query: a small grid-stride grid, so the copy does not
+  // take an SM slot from the concurrent gathers on every SM (RS_STAGE_CTAS)
+  const int grid = (int)std::min<int64_t>(grid_for(units, 256, sm_count, 2),
+                                          std::max(1, env_int("RS_STAGE_CTAS", 32)));
   launch_pdl(stage_dense_kernel, dim3(grid), dim3(256), 0, s, qd, dense_in, dst, ld_dst);
 }
 
