@@ -30,6 +30,9 @@ struct QDesc {
   const float* dense;  // [S, dense_in] fp32 contiguous (device), or null
   float* out;          // final logits [S, out_w] (device) or null: slot buffer
   int64_t flags;       // kDescDenseBf16: `dense` holds bfloat16 values
+  // embedding-stage work counters, zero in every descriptor the host writes
+  // (so each query starts from 0): [0] next bag ticket, [1] warps retired
+  unsigned int work[2];
 };
 constexpr int64_t kDescDenseBf16 = 1;
 

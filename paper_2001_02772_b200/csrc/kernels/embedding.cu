@@ -255,7 +255,13 @@ sls_tma_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap
 // bag's rows stream, and row batch j+1 is in flight while batch j accumulates.
 // Same per-lane accumulation order as sls_sum_kernel (bit-identical results).
 // Bags of up to 32*IPL lookups; longer bags use sls_sum_kernel.
-template <int LPR, int VPL, int U, int IPL, bool HOT, bool EF = false>
+// DYN: bags handed out by a ticket counter in the query descriptor instead of
+// a static stride — a warp that finishes early takes the next bag, so a launch
+// ends when the LAST BAG ends, not when the warp with the most bags does
+// (static striding gives 1.49 bags per warp at 330 items x 32 tables over the
+// 7104-warp grid: half the warps idle for a whole bag at the end). The order
+// inside a bag is untouched (bit-identical).
+template <int LPR, int VPL, int U, int IPL, bool HOT, bool EF = false, bool DYN = false>
 __global__ void __launch_bounds__(kWarps * 32)
 sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, int64_t rows,
                 int T, int L, float* __restrict__ out, int64_t ld_out, int* __restrict__ err,
@@ -281,14 +287,21 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
       nidx[q] = (bag < bags && l < L) ? __ldg(idx + bag * L + l) : 0;
     }
   };
-  int64_t bag = (int64_t)blockIdx.x * nw + warp;
+  unsigned int* work = const_cast<unsigned int*>(qd->work);
+  auto ticket = [&]() -> int64_t {
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(work, 1u);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  int64_t bag = DYN ? ticket() : (int64_t)blockIdx.x * nw + warp;
   fetch_idx(bag);
-  for (; bag < bags; bag += stride) {
+  for (int64_t next; bag < bags; bag = next) {
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < IPL; ++q) sidx[warp][q * 32 + lane] = nidx[q];
     __syncwarp();
-    fetch_idx(bag + stride);  // next bag's indices fly with this bag's rows
+    next = DYN ? ticket() : bag + stride;
+    fetch_idx(next);  // next bag's indices fly with this bag's rows
     const int t = (int)(bag % T);
     const float4* __restrict__ tab =
         reinterpret_cast<const float4*>(tables + (int64_t)t * rows * D);
@@ -346,6 +359,15 @@ sls_pipe_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
       float4* o = reinterpret_cast<float4*>(out + (bag / T) * ld_out + (int64_t)t * D) + c;
 #pragma unroll
       for (int k = 0; k < VPL; ++k) o[k * LPR] = acc[k];
+    }
+  }
+  if (DYN && lane == 0) {
+    // the last warp to retire leaves the counters at zero for the next launch
+    // of this slot's graph (descriptor rewrites zero them too)
+    const unsigned int total = gridDim.x * (unsigned int)nw;
+    if (atomicAdd(work + 1, 1u) == total - 1) {
+      atomicExch(work, 0u);
+      atomicExch(work + 1, 0u);
     }
   }
 }
@@ -978,6 +1000,9 @@ int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
+// RS_SLS_DYN: 1 = dynamic bag tickets in the pipelined SLS kernel
+bool sls_dyn() { return env_int("RS_SLS_DYN", 1) != 0; }
+
 template <int LPR, int VPL, int U, int IPL>
 void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
                      float* out, int64_t ld_out, int* err, int64_t max_items, int sm_count,
@@ -992,12 +1017,15 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
                                  : sls_pipe_kernel<LPR, VPL, U, IPL, false>);
 #else
   auto kern = hot_rows > 0 ? sls_pipe_kernel<LPR, VPL, U, IPL, true>
-                           : sls_pipe_kernel<LPR, VPL, U, IPL, false>;
+                           : (sls_dyn() ? sls_pipe_kernel<LPR, VPL, U, IPL, false, false, true>
+                                        : sls_pipe_kernel<LPR, VPL, U, IPL, false>);
 #endif
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, 0);
   per_sm = std::max(per_sm, 1);
-  const int grid = grid_for(max_items * T, wpc, sm_count, env_int("RS_SLS_WAVES", 2) * per_sm);
+  // dynamic tickets balance the warps by themselves: one resident wave
+  const int waves = env_int("RS_SLS_WAVES", sls_dyn() && hot_rows == 0 ? 1 : 2);
+  const int grid = grid_for(max_items * T, wpc, sm_count, waves * per_sm);
   max_carveout(reinterpret_cast<const void*>(kern));
   kern<<<grid, wpc * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err, hot, hot_rows);
 }
