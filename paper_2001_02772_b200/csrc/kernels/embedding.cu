@@ -1000,8 +1000,8 @@ int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
-// RS_SLS_DYN: 1 = dynamic bag tickets in the pipelined SLS kernel
-bool sls_dyn() { return env_int("RS_SLS_DYN", 1) != 0; }
+// RS_SLS_DYN (experiments build): 1 = dynamic bag tickets in the SLS kernel
+bool sls_dyn() { return RS_EXPERIMENTS && env_int("RS_SLS_DYN", 0) != 0; }
 
 template <int LPR, int VPL, int U, int IPL>
 void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, int L,
@@ -1011,20 +1011,23 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
 #if RS_EXPERIMENTS
   // RS_SLS_EF=1: gather rows evict-first in L2 (measured +1.3% us/query in the
   // pipelined queue, i.e. slower: tools/env_sweep.py)
+  // RS_SLS_DYN=1: bags by ticket (measured slower: one launch 5.16 -> 3.89
+  // TB/s at 330 items, pipelined 38.5 -> 40.5 us/query — the ticket atomic
+  // sits in front of the next bag's index load)
   const bool ef = env_int("RS_SLS_EF", 0) != 0;
   auto kern = hot_rows > 0 ? sls_pipe_kernel<LPR, VPL, U, IPL, true>
                            : (ef ? sls_pipe_kernel<LPR, VPL, U, IPL, false, true>
-                                 : sls_pipe_kernel<LPR, VPL, U, IPL, false>);
+                                 : sls_dyn() ? sls_pipe_kernel<LPR, VPL, U, IPL, false, false, true>
+                                             : sls_pipe_kernel<LPR, VPL, U, IPL, false>);
 #else
   auto kern = hot_rows > 0 ? sls_pipe_kernel<LPR, VPL, U, IPL, true>
-                           : (sls_dyn() ? sls_pipe_kernel<LPR, VPL, U, IPL, false, false, true>
-                                        : sls_pipe_kernel<LPR, VPL, U, IPL, false>);
+                           : sls_pipe_kernel<LPR, VPL, U, IPL, false>;
 #endif
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, 0);
   per_sm = std::max(per_sm, 1);
   // dynamic tickets balance the warps by themselves: one resident wave
-  const int waves = env_int("RS_SLS_WAVES", sls_dyn() && hot_rows == 0 ? 1 : 2);
+  const int waves = env_int("RS_SLS_WAVES", sls_dyn() && hot_rows == 0 ? 1 : 2);  // 2 measured
   const int grid = grid_for(max_items * T, wpc, sm_count, waves * per_sm);
   max_carveout(reinterpret_cast<const void*>(kern));
   kern<<<grid, wpc * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err, hot, hot_rows);
