@@ -288,8 +288,12 @@ def measured_tensor_peak(fc):
     if os.path.exists(p):
         with open(p) as f:
             bf = json.load(f).get("bf16_tflops")
+        if bf and fc == "bf16":
+            return bf, f"measured dense bf16 {bf:.0f} TF/s (MEASURED_PEAKS.json)"
         if bf:
             return 0.5 * bf, f"0.5 x measured bf16 {bf:.0f} TF/s (MEASURED_PEAKS.json): tf32 rate"
+    if fc == "bf16":
+        return 2250.0, "fallback: bf16 dense 2.25 PF/s (B200_PROFILING.md)"
     return 1100.0, "fallback: tf32 dense 1.1 PF/s (B200_PROFILING.md)"
 
 
@@ -413,7 +417,8 @@ def run_ours(args, rank, world, local):
             math.log(args.size_median), 0.5), 2 * Q)
     sizes = np.minimum(sizes, args.max_query)
     acc = rs.Accelerator(spec, rows, seed=1, device=local, max_query_size=args.max_query,
-                         fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc],
+                         fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO,
+                                  "bf16": rs.FC_BF16}[args.fc],
                          queue_depth=args.depth, l2_persist_mb=args.l2_persist_mb)
     if args.merge > 1:
         acc.set_option(rs.OPT_MERGE_QUERIES, args.merge)
@@ -631,7 +636,8 @@ def run_ours(args, rank, world, local):
             "metric": METRIC, "value": agg["value"], "unit": "queries/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": agg["time_s"] * 1e3 / K,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "fp32" if args.fc == "fp32" else "fp32 SLS / tf32 FC",
+            "dtype": {"fp32": "fp32", "bf16": "fp32 SLS / bf16 FC (labelled variant)"}.get(
+                args.fc, "fp32 SLS / tf32 FC"),
             "data": f"synthetic (seeded random-init tables/weights, LogNormal(ln{args.size_median:g},0.5) sizes)",
             "config": cfg,
             "method": "open-loop Poisson replay (n=50,000, sim.hpp:79) of the per-query CUDA-event "
@@ -685,7 +691,7 @@ def run_serve(args):
     K = args.gpus
     if rs.device_count() < K:
         raise SystemExit(f"--serve --gpus {K}: only {rs.device_count()} devices visible")
-    fc = {"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc]
+    fc = {"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO, "bf16": rs.FC_BF16}[args.fc]
     reps = [rs.Accelerator(spec, rows, seed=1, device=r, max_query_size=args.max_query,
                            fc_mode=fc, queue_depth=args.depth) for r in range(K)]
     P = 2 * args.queries_per_step
@@ -848,7 +854,8 @@ def main():
     ap.add_argument("--l2-persist-mb", type=int, default=0,
                     help="hot-row block kept in the L2 persisting set-aside (MiB)")
     ap.add_argument("--max-query", type=int, default=1000)
-    ap.add_argument("--fc", choices=["fp32", "tf32", "auto"], default="auto")
+    ap.add_argument("--fc", choices=["fp32", "tf32", "auto", "bf16"], default="auto",
+                    help="bf16 = labelled lower-precision variant (bf16 weights/activations)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--depth", type=int, default=8, help="queries in flight per GPU (lanes)")
     ap.add_argument("--roofline", choices=["auto", "hbm", "tensor"], default="auto",

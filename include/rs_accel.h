@@ -170,8 +170,11 @@ typedef struct rs_accel rs_accel;
 enum {
   RS_FC_FP32 = 0,  /* FFMA fp32 path (tight parity)                        */
   RS_FC_TF32 = 1,  /* tcgen05 kind::tf32 (fp32 operands, fp32 accumulate)   */
-  RS_FC_AUTO = 2   /* the measured-fastest path: today the tcgen05 graph at
+  RS_FC_AUTO = 2,  /* the measured-fastest path: today the tcgen05 graph at
                       every query size (= RS_FC_TF32)                   */
+  RS_FC_BF16 = 3   /* tcgen05 kind::f16 with bf16 weights and activations,
+                      fp32 accumulate (LABELLED lower-precision variant:
+                      its own tolerance, tests/parity_rule.py)           */
 };
 enum { RS_RNN_GRU = 0, RS_RNN_AUGRU = 1 };
 

@@ -100,7 +100,7 @@ POOLING = {"Sum": 0, "Concat": 1, "AttentionFC": 2, "AttentionRNN": 3}
 POOLING_NAMES = {v: k for k, v in POOLING.items()}
 OP_CATEGORIES = ["DenseFC", "PredictFC", "EmbeddingLookup", "Pooling", "Attention",
                  "Recurrent", "Interaction"]
-FC_FP32, FC_TF32, FC_AUTO = 0, 1, 2
+FC_FP32, FC_TF32, FC_AUTO, FC_BF16 = 0, 1, 2, 3  # FC_BF16: labelled bf16 tcgen05 variant
 RNN_GRU, RNN_AUGRU = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 INDEX_I64, INDEX_I32 = 0, 1  # rs_query.index_type (I32: labelled input variant)

@@ -73,6 +73,10 @@ struct FcLayer {
   int batch = 1;
   float* W = nullptr;  // [batch][out][ldk]
   float* b = nullptr;  // [batch][out]
+  // RS_FC_BF16: the same weights rounded to bfloat16, [batch][out][ldk16],
+  // ldk16 = round8(in) (16-byte rows for TMA)
+  uint16_t* W16 = nullptr;
+  int64_t ldk16 = 0;
 };
 
 struct Slot {
@@ -94,6 +98,11 @@ struct Slot {
   float* pooled = nullptr;
   float* X = nullptr;
   float* pact[2] = {nullptr, nullptr};
+  // RS_FC_BF16 activations: the stacks' inputs and hidden layers as bfloat16
+  uint16_t* X16 = nullptr;
+  uint16_t* dense16 = nullptr;
+  uint16_t* act16[2] = {nullptr, nullptr};
+  uint16_t* pact16[2] = {nullptr, nullptr};
   float* out = nullptr;
   cudaGraphExec_t graph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // GraphKind
   int kernels[3] = {0, 0, 0};
@@ -128,6 +137,7 @@ struct rs_accel {
   int64_t p_in = 0, ld_x = 0, out_dim = 0, out_w = 0;
   int64_t pooled_dim = 0;
   int64_t max_dense_w = 0, max_pred_w = 0;
+  int64_t ld_x16 = 0, ld_dense16 = 0;  // bf16 row strides (round8)
   // device state
   float* tables = nullptr;
   // L2-persisting hot block: rows [0, hot_rows) of every table, [T][hot_rows][D]
@@ -181,6 +191,14 @@ void upload(void* dst, const std::vector<float>& v) {
 
 float fan_bound(int64_t fan_in) { return 1.0f / sqrtf(static_cast<float>(fan_in)); }
 
+// fp32 -> bfloat16 bits, round to nearest even (finite inputs)
+uint16_t to_bf16_bits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
 // Weights and biases of one FC stack layer, [batch][out][ldk] with zero pad.
 FcLayer make_layer(rs_accel* a, int64_t in, int64_t out, int relu, int batch,
                    uint64_t (*wid)(int64_t, int64_t), uint64_t (*bid)(int64_t, int64_t),
@@ -203,6 +221,18 @@ FcLayer make_layer(rs_accel* a, int64_t in, int64_t out, int relu, int batch,
   upload(f.W, w);
   upload(f.b, b);
   a->weight_bytes += (int64_t)((w.size() + b.size()) * sizeof(float));
+  if (a->init.fc_mode == RS_FC_BF16) {
+    f.ldk16 = round_up(in, 8);
+    std::vector<uint16_t> h((size_t)(batch * out * f.ldk16), 0);
+    for (int z = 0; z < batch; ++z)
+      for (int64_t o = 0; o < out; ++o)
+        for (int64_t i = 0; i < in; ++i)
+          h[(size_t)((z * out + o) * f.ldk16 + i)] =
+              to_bf16_bits(w[(size_t)((z * out + o) * f.ldk + i)]);
+    f.W16 = static_cast<uint16_t*>(dmalloc(a, a->allocs, h.size() * 2, false));
+    RS_CUDA(cudaMemcpy(f.W16, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+    a->weight_bytes += (int64_t)(h.size() * 2);
+  }
   return f;
 }
 
@@ -282,6 +312,8 @@ void build_model(rs_accel* a) {
   a->dense_out = dense_out_dim(m);
   a->p_in = predict_input_dim(m);
   a->ld_x = round_up(a->p_in, 4);
+  a->ld_x16 = round_up(a->p_in, 8);
+  a->ld_dense16 = round_up(std::max<int64_t>(a->dense_in, 1), 8);
   a->out_dim = m.predict_fc.dims[m.predict_fc.n - 1];
   a->out_w = a->stacks * a->out_dim;
   switch (m.pooling) {
@@ -505,6 +537,110 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
   return tc_count;
 }
 
+// RS_FC_BF16: the stack on tcgen05 kind::f16 layers with bf16 operands. The
+// fp32 stack input (src, cols wide) is converted once into in16; layer l
+// writes bf16 activations for layer l+1 whenever that layer also plans as a
+// bf16 tcgen05 layer, fp32 otherwise (the logits, a fused narrow last layer's
+// input stays in registers, or an FFMA successor). Returns the number of
+// tcgen05 layers, or -1 (nothing enqueued) when layer 0 cannot run on bf16
+// tcgen05 — the caller then uses the fp32/tf32 stack.
+int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
+                       const float* src, int64_t ld_src, int64_t cols, uint16_t* in16,
+                       int64_t ld_in16, uint16_t* const* tmp16, int64_t ld_tmp16,
+                       float* const* tmp, int64_t ld_tmp, float* final_out, int64_t ld_final,
+                       int64_t final_sCz, cudaStream_t st, bool final_to_desc, int sms) {
+  const int64_t maxS = a->init.max_query_size;
+  if (layers.empty() || !tc_available()) return -1;
+  auto args16 = [&](const FcLayer& f, const uint16_t* A, int64_t lda, int64_t sAz) {
+    FcArgs x{};
+    x.A = reinterpret_cast<const float*>(A); x.lda = lda; x.sAz = sAz;
+    x.W = reinterpret_cast<const float*>(f.W16); x.ldw = f.ldk16; x.sWz = f.out * f.ldk16;
+    x.bias = f.b; x.sbz = f.out;
+    x.N = (int)f.out; x.K = (int)f.in; x.relu = f.relu; x.batch = f.batch;
+    x.ab16 = 1;
+    return x;
+  };
+  // can layer l run as a bf16 tcgen05 layer reading A (dry-run plan)?
+  auto can16 = [&](size_t l, const uint16_t* A, int64_t lda, int64_t sAz, int64_t rows) {
+    if (!layers[l].W16) return false;
+    FcArgs x = args16(layers[l], A, lda, sAz);
+    x.C = tmp[0]; x.ldc = ld_tmp; x.sCz = maxS * ld_tmp;
+    TcPlan p;
+    return tc_plan(&p, x, maxS, rows, nullptr);
+  };
+  if (!can16(0, in16, ld_in16, 0, maxS)) return -1;
+  launch_to_bf16(s->d_q, src, ld_src, in16, ld_in16, cols, maxS, sms, st);
+  int tc_count = 0;
+  const uint16_t* cur16 = in16;
+  const float* cur32 = nullptr;
+  int64_t lda = ld_in16, sAz = 0;
+  for (size_t l = 0; l < layers.size(); ++l) {
+    const FcLayer& f = layers[l];
+    const bool last = l + 1 == layers.size();
+    FcArgs args{};
+    if (cur16) {
+      args = args16(f, cur16, lda, sAz);
+    } else {
+      args.A = cur32; args.lda = lda; args.sAz = sAz;
+      args.W = f.W; args.ldw = f.ldk; args.sWz = f.out * f.ldk;
+      args.bias = f.b; args.sbz = f.out;
+      args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
+    }
+    const bool fuse = l + 2 == layers.size() && layers[l + 1].out <= kFuseMaxN2 &&
+                      f.out <= 128 && fuse_enabled();
+    auto set_output = [&](bool fused) {
+      args.c16 = 0;
+      if (fused) {
+        const FcLayer& g = layers[l + 1];
+        args.single_n_tile = 1;
+        args.W2 = g.W; args.ldw2 = g.ldk; args.sW2z = g.out * g.ldk;
+        args.b2 = g.b; args.sb2z = g.out;
+        args.C2 = final_out; args.ldc2 = ld_final; args.sC2z = final_sCz;
+        args.N2 = (int)g.out; args.relu2 = g.relu; args.c2_desc = final_to_desc ? 1 : 0;
+        args.skip_c = 1;
+        args.C = tmp[l & 1]; args.ldc = ld_tmp; args.sCz = maxS * ld_tmp;
+      } else if (last) {
+        args.C = final_out; args.ldc = ld_final; args.sCz = final_sCz;
+        args.c_desc = final_to_desc ? 1 : 0;
+      } else if (can16(l + 1, tmp16[l & 1], ld_tmp16, maxS * ld_tmp16, maxS)) {
+        args.C = reinterpret_cast<float*>(tmp16[l & 1]); args.ldc = ld_tmp16;
+        args.sCz = maxS * ld_tmp16; args.c16 = 1;
+      } else {
+        args.C = tmp[l & 1]; args.ldc = ld_tmp; args.sCz = maxS * ld_tmp;
+      }
+    };
+    set_output(fuse);
+    TcPlan p;
+    bool ok = tc_plan(&p, args, maxS, cur16 == in16 || cur32 == nullptr ? maxS : maxS,
+                      &s->splitk) && (!fuse || p.n_tiles == 1);
+    bool fused = fuse && ok;
+    if (fuse && !ok) {
+      args.single_n_tile = 0; args.N2 = 0; args.skip_c = 0; args.W2 = nullptr;
+      args.b2 = nullptr; args.C2 = nullptr;
+      set_output(false);
+      ok = tc_plan(&p, args, maxS, maxS, &s->splitk);
+    }
+    if (ok) {
+      launch_fc_tc(s->d_q, p, args, st);
+      tc_count += fused ? 2 : 1;
+    } else {
+      if (cur16) raise(RS_E_CUDA, "bf16 FC layer failed to plan after a bf16 producer");
+      launch_fc_ffma(s->d_q, args, maxS, st);
+    }
+    if (fused) break;
+    if (args.c16) {
+      cur16 = reinterpret_cast<const uint16_t*>(args.C);
+      cur32 = nullptr;
+    } else {
+      cur16 = nullptr;
+      cur32 = args.C;
+    }
+    lda = args.ldc;
+    sAz = args.sCz;
+  }
+  return tc_count;
+}
+
 // Graph kinds per slot: the embedding stage alone (rs_pooled), the whole
 // forward with FFMA FC layers (small batches / fp32 parity) and the whole
 // forward with tcgen05 FC layers wherever the layer shape fills a tile.
@@ -536,6 +672,7 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   const bool stage_stamp = kind == kGraphStageTimed;
   const bool tc = kind == kGraphLarge ||
                   (stage_stamp && a->init.fc_mode != RS_FC_FP32 && tc_available());
+  const bool h16 = tc && a->init.fc_mode == RS_FC_BF16;  // bf16 FC stacks
   int ntc = 0;
   if (kind == kGraphPool || kind == kGraphPoolTimed) {
     // timestamps of the embedding kernel alone (rs_timing.embed_ms): external
@@ -580,9 +717,17 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
       if (m.has_dense_fc) {
         launch_stage_dense(s->d_q, a->dense_in, s->dense_stage, a->ld_dense, maxS, s->dense_sms,
                            bs);
-        if (!(skip & 1))
-          ntc += enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS, s->act,
-                               a->max_dense_w, s->X, a->ld_x, 0, tc, bs);
+        if (!(skip & 1)) {
+          const int u = h16 ? enqueue_stack_bf16(
+                                  a, s, a->dense_layers, s->dense_stage, a->ld_dense, a->dense_in,
+                                  s->dense16, a->ld_dense16, s->act16,
+                                  round_up(std::max<int64_t>(a->max_dense_w, 8), 8), s->act,
+                                  a->max_dense_w, s->X, a->ld_x, 0, bs, false, s->dense_sms)
+                            : -1;
+          ntc += u >= 0 ? u
+                        : enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS,
+                                        s->act, a->max_dense_w, s->X, a->ld_x, 0, tc, bs);
+        }
       } else {
         launch_stage_dense(s->d_q, a->dense_in, s->X, a->ld_x, maxS, s->dense_sms, bs);
       }
@@ -607,9 +752,18 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
       launch_diag_empty(atoi(de), dc ? atoi(dc) : 1, st);
     }
     if (stage_stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[2], st, cudaEventRecordExternal));
-    if (!(skip & 4))
-      ntc += enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact, a->max_pred_w,
-                           s->out, a->out_w, a->out_dim, tc, st, /*final_to_desc=*/true);
+    if (!(skip & 4)) {
+      const int u = h16 ? enqueue_stack_bf16(a, s, a->pred_layers, s->X, a->ld_x, a->p_in, s->X16,
+                                             a->ld_x16, s->pact16,
+                                             round_up(std::max<int64_t>(a->max_pred_w, 8), 8),
+                                             s->pact, a->max_pred_w, s->out, a->out_w, a->out_dim,
+                                             st, true, s->dense_sms)
+                        : -1;
+      ntc += u >= 0 ? u
+                    : enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact,
+                                    a->max_pred_w, s->out, a->out_w, a->out_dim, tc, st,
+                                    /*final_to_desc=*/true);
+    }
     if (stage_stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[3], st, cudaEventRecordExternal));
   }
   cudaError_t le = cudaGetLastError();
@@ -778,6 +932,17 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   s->pooled = static_cast<float*>(
       dmalloc(a, s->allocs, (size_t)(maxS * std::max<int64_t>(a->pooled_dim, 1) * 4)));
   s->X = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_x * 4)));
+  if (a->init.fc_mode == RS_FC_BF16) {
+    const int64_t wd = round_up(std::max<int64_t>(a->max_dense_w, 8), 8);
+    const int64_t wp = round_up(std::max<int64_t>(a->max_pred_w, 8), 8);
+    s->X16 = static_cast<uint16_t*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_x16 * 2)));
+    s->dense16 = static_cast<uint16_t*>(dmalloc(a, s->allocs, (size_t)(maxS * a->ld_dense16 * 2)));
+    for (int i = 0; i < 2; ++i) {
+      s->act16[i] = static_cast<uint16_t*>(dmalloc(a, s->allocs, (size_t)(maxS * wd * 2)));
+      s->pact16[i] =
+          static_cast<uint16_t*>(dmalloc(a, s->allocs, (size_t)(a->stacks * maxS * wp * 2)));
+    }
+  }
   s->out = static_cast<float*>(dmalloc(a, s->allocs, (size_t)(maxS * a->out_w * 4)));
   for (auto& e : s->ev) RS_CUDA(cudaEventCreate(&e));
   for (auto& e : s->kev) RS_CUDA(cudaEventCreate(&e));
@@ -1369,7 +1534,7 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     if (prop.major != 10)
       raise(RS_E_NO_DEVICE, "this library is built for sm_100a (B200) only");
     if (init->max_query_size < 1) raise(RS_E_INVALID, "max_query_size < 1");
-    if (init->fc_mode < RS_FC_FP32 || init->fc_mode > RS_FC_AUTO)
+    if (init->fc_mode < RS_FC_FP32 || init->fc_mode > RS_FC_BF16)
       raise(RS_E_INVALID, "bad fc_mode");
     RS_CUDA(cudaSetDevice(device));
     (void)cudaGetLastError();  // drop a stale non-sticky error from an earlier call

@@ -30,6 +30,8 @@
 // shared-memory capacity caps bytes in flight; 3.8 vs 5.2 TB/s at S=323).
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -1480,6 +1482,30 @@ void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t l
   const int grid = (int)std::min<int64_t>(grid_for(units, 256, sm_count, 2),
                                           std::max(1, env_int("RS_STAGE_CTAS", 32)));
   launch_pdl(stage_dense_kernel, dim3(grid), dim3(256), 0, s, qd, dense_in, dst, ld_dst);
+}
+
+// fp32 -> bf16 rows (round to nearest even) for the RS_FC_BF16 graph: the
+// first layer of a bf16 FC stack reads its activations as bfloat16. Rows are
+// the query's S items; columns [0, cols) of each row (the padding of the
+// destination rows is never read: the tensor map's K extent is cols).
+__global__ void __launch_bounds__(256)
+to_bf16_kernel(const QDesc* __restrict__ qd, const float* __restrict__ src, int64_t lds,
+               __nv_bfloat16* __restrict__ dst, int64_t ldd, int64_t cols) {
+  pdl_wait();  // src is the predecessor's output
+  const int64_t total = qd->S * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+  }
+  pdl_trigger();
+}
+
+void launch_to_bf16(const QDesc* qd, const float* src, int64_t lds, void* dst, int64_t ldd,
+                    int64_t cols, int64_t max_items, int sm_count, cudaStream_t s) {
+  const int grid = grid_for(max_items * cols, 256, sm_count, 2);
+  launch_pdl(to_bf16_kernel, dim3(grid), dim3(256), 0, s, qd, src, lds,
+             static_cast<__nv_bfloat16*>(dst), ldd, cols);
 }
 
 // int32 -> int64 index widening for the RS_INDEX_I32 input variant

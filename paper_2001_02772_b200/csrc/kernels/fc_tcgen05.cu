@@ -87,6 +87,19 @@ __device__ __forceinline__ uint32_t idesc_tf32() {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
          ((uint32_t)(BM >> 4) << 24);
 }
+// kind::f16 with bf16 operands: A bf16 [7,10)=1, B bf16 [10,13)=1, D f32.
+template <int BN>
+__device__ __forceinline__ uint32_t idesc_bf16() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+
+// bf16 pair -> one 32-bit word (round to nearest even)
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 
 template <int BN, int STAGES>
 struct TcSmem {
@@ -101,7 +114,11 @@ struct TcSmem {
 
 constexpr int kTcThreads = 128;
 
-template <int BN, int STAGES>
+// H: bf16 operands (kind::f16, 64 elements = 128 B per k-slab, RS_FC_BF16);
+// otherwise fp32 operands rounded to tf32 by the tensor core (32 per slab).
+// The k-slab is 128 bytes per row either way, so the shared-memory ring, the
+// SW128 descriptors and the 4 MMAs per slab are identical.
+template <int BN, int STAGES, bool H = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap map_a,
              const __grid_constant__ CUtensorMap map_w, FcArgs a, int a_batched) {
@@ -121,7 +138,8 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   if (m0 >= M) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk_all = (a.K + BK - 1) / BK;
+  constexpr int KE = H ? 2 * BK : BK;  // operand elements per k-slab
+  const int nk_all = (a.K + KE - 1) / KE;
   const int per = (nk_all + splits - 1) / splits;
   const int kb0 = sp * per;
   const int nk = max(0, min(nk_all, kb0 + per) - kb0);
@@ -157,7 +175,7 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < pre; ++kb) {
       mbar_expect_tx(&sm.full[kb], kBytes);
-      tma_load_3d(sm.b[kb], &map_w, &sm.full[kb], (kb0 + kb) * BK, n0, z);
+      tma_load_3d(sm.b[kb], &map_w, &sm.full[kb], (kb0 + kb) * KE, n0, z);
     }
   }
   pdl_wait();  // the activations A are the previous layer's output
@@ -170,15 +188,15 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
       if (kb >= pre) {
         mbar_wait(&sm.empty[s], ph ^ 1u);
         mbar_expect_tx(&sm.full[s], kBytes);
-        tma_load_3d(sm.b[s], &map_w, &sm.full[s], (kb0 + kb) * BK, n0, z);
+        tma_load_3d(sm.b[s], &map_w, &sm.full[s], (kb0 + kb) * KE, n0, z);
       }
-      if (a_batched) tma_load_3d(sm.a[s], &map_a, &sm.full[s], (kb0 + kb) * BK, m0, z);
-      else tma_load_2d(sm.a[s], &map_a, &sm.full[s], (kb0 + kb) * BK, m0);
+      if (a_batched) tma_load_3d(sm.a[s], &map_a, &sm.full[s], (kb0 + kb) * KE, m0, z);
+      else tma_load_2d(sm.a[s], &map_a, &sm.full[s], (kb0 + kb) * KE, m0);
     }
     __syncwarp();
   } else if (warp == 1) {
     // ---- MMA issuer (lane 0) ----
-    const uint32_t idesc = idesc_tf32<BN>();
+    const uint32_t idesc = H ? idesc_bf16<BN>() : idesc_tf32<BN>();
     for (int kb = 0; lane == 0 && kb < nk; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
@@ -190,11 +208,18 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
         const uint64_t da = sw128_desc(sa + kk * 32);
         const uint64_t db = sw128_desc(sb + kk * 32);
         const uint32_t acc = (kb | kk) ? 1u : 0u;
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-            "l"(da), "l"(db), "r"(idesc), "r"(acc)
-            : "memory");
+        if constexpr (H)
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc)
+              : "memory");
+        else
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc)
+              : "memory");
       }
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -349,6 +374,23 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
           }
         }
         if (a.skip_c) {
+        } else if (a.c16) {
+          // bf16 activations for the next bf16 layer: 32 values = 64 bytes
+          uint16_t* __restrict__ C16 = reinterpret_cast<uint16_t*>(Cb) + (int64_t)z * a.sCz +
+                                       m * a.ldc + nb;
+          if (vec_ok && nb + 32 <= a.N && (a.ldc % 8 == 0)) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(C16)[i] =
+                  make_uint4(pack_bf16(y[8 * i], y[8 * i + 1]), pack_bf16(y[8 * i + 2], y[8 * i + 3]),
+                             pack_bf16(y[8 * i + 4], y[8 * i + 5]),
+                             pack_bf16(y[8 * i + 6], y[8 * i + 7]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (nb + i < a.N)
+                C16[i] = (uint16_t)(pack_bf16(y[i], 0.f) & 0xFFFFu);
+          }
         } else if (vec_ok && nb + 32 <= a.N) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
@@ -402,26 +444,27 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-bool encode(CUtensorMap* map, const float* base, int rank, const cuuint64_t* dims,
+bool encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims,
             const cuuint64_t* strides_bytes, const cuuint32_t* box,
-            CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
+            CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B,
+            CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, (void*)base, dims,
+  CUresult r = fn(map, dtype, (cuuint32_t)rank, (void*)base, dims,
                   strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool H = false>
 size_t tc_smem_bytes() {
   return sizeof(TcSmem<BN, STAGES>) + 1024;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool H = false>
 void set_attr_once() {  // once per device (common.cuh smem_attr)
-  smem_attr(reinterpret_cast<const void*>(fc_tc_kernel<BN, STAGES>),
+  smem_attr(reinterpret_cast<const void*>(fc_tc_kernel<BN, STAGES, H>),
             (int)tc_smem_bytes<BN, STAGES>());
 }
 
@@ -677,8 +720,11 @@ bool make_row_gather_map(CUtensorMap* map, const float* base, int64_t total_rows
 
 bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch,
              SplitKPool* pool) {
-  if (a.N < 64 || a.K < BK) return false;
-  if (a.lda % 4 || a.ldw % 4 || (a.sAz % 4) || (a.sWz % 4)) return false;
+  const int ke = a.ab16 ? 2 * BK : BK;      // operand elements per 128-byte k-slab
+  const int esz = a.ab16 ? 2 : 4;          // operand bytes
+  const int al = 16 / esz;                 // 16-byte rows for TMA
+  if (a.N < 64 || a.K < ke) return false;
+  if (a.lda % al || a.ldw % al || (a.sAz % al) || (a.sWz % al)) return false;
   if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.W) & 15))
     return false;
   // tile/pipeline configuration: 0 <BN128,3 stages> 1 <64,4> 2 <128,6> 3 <64,8>
@@ -716,30 +762,43 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   p->m_tiles = (int)((m_cap + BM - 1) / BM);
   p->n_tiles = (a.N + p->block_n - 1) / p->block_n;
   // A: [batch][rows][K] (or shared 2D when sAz == 0)
+  const CUtensorMapDataType dt =
+      a.ab16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   if (a.sAz != 0) {
     cuuint64_t dims[3] = {(cuuint64_t)a.K, (cuuint64_t)a_rows_per_batch, (cuuint64_t)a.batch};
-    cuuint64_t str[2] = {(cuuint64_t)a.lda * 4, (cuuint64_t)a.sAz * 4};
-    cuuint32_t box[3] = {BK, BM, 1};
-    if (!encode(&p->map_a, a.A, 3, dims, str, box)) return false;
+    cuuint64_t str[2] = {(cuuint64_t)a.lda * esz, (cuuint64_t)a.sAz * esz};
+    cuuint32_t box[3] = {(cuuint32_t)ke, BM, 1};
+    if (!encode(&p->map_a, a.A, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return false;
   } else {
     cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a_rows_per_batch};
-    cuuint64_t str[1] = {(cuuint64_t)a.lda * 4};
-    cuuint32_t box[2] = {BK, BM};
-    if (!encode(&p->map_a, a.A, 2, dims, str, box)) return false;
+    cuuint64_t str[1] = {(cuuint64_t)a.lda * esz};
+    cuuint32_t box[2] = {(cuuint32_t)ke, BM};
+    if (!encode(&p->map_a, a.A, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return false;
   }
   {
     cuuint64_t dims[3] = {(cuuint64_t)a.K, (cuuint64_t)a.N, (cuuint64_t)a.batch};
-    cuuint64_t str[2] = {(cuuint64_t)a.ldw * 4,
-                         (cuuint64_t)(a.sWz ? a.sWz : (int64_t)a.N * a.ldw) * 4};
-    cuuint32_t box[3] = {BK, (cuuint32_t)p->block_n, 1};
-    if (!encode(&p->map_w, a.W, 3, dims, str, box)) return false;
+    cuuint64_t str[2] = {(cuuint64_t)a.ldw * esz,
+                         (cuuint64_t)(a.sWz ? a.sWz : (int64_t)a.N * a.ldw) * esz};
+    cuuint32_t box[3] = {(cuuint32_t)ke, (cuuint32_t)p->block_n, 1};
+    if (!encode(&p->map_w, a.W, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return false;
   }
-  switch (p->cfg) {
-    case 0: set_attr_once<128, 3>(); break;
-    case 1: set_attr_once<64, 4>(); break;
-    case 2: set_attr_once<128, 6>(); break;
-    case 4: set_attr_once<256, 4>(); break;
-    default: set_attr_once<64, 8>(); break;
+  p->ab16 = a.ab16;
+  if (a.ab16) {
+    switch (p->cfg) {
+      case 0: set_attr_once<128, 3, true>(); break;
+      case 1: set_attr_once<64, 4, true>(); break;
+      case 2: set_attr_once<128, 6, true>(); break;
+      case 4: set_attr_once<256, 4, true>(); break;
+      default: set_attr_once<64, 8, true>(); break;
+    }
+  } else {
+    switch (p->cfg) {
+      case 0: set_attr_once<128, 3>(); break;
+      case 1: set_attr_once<64, 4>(); break;
+      case 2: set_attr_once<128, 6>(); break;
+      case 4: set_attr_once<256, 4>(); break;
+      default: set_attr_once<64, 8>(); break;
+    }
   }
   // Split-K for long reductions (K >= 1024: RMC3's 2560 -> 512, MT-WND/WND's
   // 1640 -> 1024), RS_SPLITK=n (2..4) enables: a tile's k-blocks are spread
@@ -753,7 +812,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
 #if RS_EXPERIMENTS
   const char* sk = getenv("RS_SPLITK");
   const int nk = (a.K + BK - 1) / BK;
-  if (pool && a.N2 == 0 && nk >= 32 && sk && atoi(sk) > 1) {
+  if (pool && !a.ab16 && a.N2 == 0 && nk >= 32 && sk && atoi(sk) > 1) {
     int splits = std::min(std::min(4, atoi(sk)), nk / 16);
     while (splits > 1 && (splits - 1) * ((nk + splits - 1) / splits) >= nk) --splits;
     const size_t tiles = (size_t)a.batch * p->m_tiles * p->n_tiles;
@@ -856,15 +915,25 @@ void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a0, cudaStream
   a.cnt = p.cnt;
   const dim3 grid(p.n_tiles, p.m_tiles, a.batch * std::max(1, p.splits));
   const int a_batched = a.sAz != 0 ? 1 : 0;
-#define RS_TC(BN, ST)                                                                   \
-  launch_pdl(fc_tc_kernel<BN, ST>, grid, dim3(kTcThreads), tc_smem_bytes<BN, ST>(), s, qd, p.map_a, \
-             p.map_w, a, a_batched)
-  switch (p.cfg) {
-    case 0: RS_TC(128, 3); break;
-    case 4: RS_TC(256, 4); break;
-    case 1: RS_TC(64, 4); break;
-    case 2: RS_TC(128, 6); break;
-    default: RS_TC(64, 8); break;
+#define RS_TC(BN, ST, H)                                                                    \
+  launch_pdl(fc_tc_kernel<BN, ST, H>, grid, dim3(kTcThreads), tc_smem_bytes<BN, ST>(), s, qd, \
+             p.map_a, p.map_w, a, a_batched)
+  if (p.ab16) {
+    switch (p.cfg) {
+      case 0: RS_TC(128, 3, true); break;
+      case 4: RS_TC(256, 4, true); break;
+      case 1: RS_TC(64, 4, true); break;
+      case 2: RS_TC(128, 6, true); break;
+      default: RS_TC(64, 8, true); break;
+    }
+  } else {
+    switch (p.cfg) {
+      case 0: RS_TC(128, 3, false); break;
+      case 4: RS_TC(256, 4, false); break;
+      case 1: RS_TC(64, 4, false); break;
+      case 2: RS_TC(128, 6, false); break;
+      default: RS_TC(64, 8, false); break;
+    }
   }
 #undef RS_TC
 }

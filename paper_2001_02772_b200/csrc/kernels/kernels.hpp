@@ -41,6 +41,10 @@ void launch_group_gather(const GroupGather& g, int64_t dense_in, int64_t TL, flo
                          int64_t* idx_dst, int sm_count, cudaStream_t s);
 void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t ld_dst,
                         int64_t max_items, int sm_count, cudaStream_t s);
+// fp32 rows -> bf16 rows (RS_FC_BF16 graphs): dst[r][c] = bf16(src[r][c]),
+// r < QDesc::S, c < cols
+void launch_to_bf16(const QDesc* qd, const float* src, int64_t lds, void* dst, int64_t ldd,
+                    int64_t cols, int64_t max_items, int sm_count, cudaStream_t s);
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
                         int64_t max_items, int sm_count, cudaStream_t s, bool tc = false);
@@ -68,6 +72,9 @@ struct FcArgs {
   int skip_c;          // 1: C itself is not needed (only C2)
   int single_n_tile;   // planning hint: prefer one N tile (BN = 128) when N <= 128
   int splits; float* ws; int* cnt;  // split-K (set by launch_fc_tc from the plan)
+  // RS_FC_BF16: A and W hold bfloat16 (row strides in elements); c16: C is
+  // written as bfloat16 (the next bf16 layer's A). tcgen05 only.
+  int ab16; int c16;
 };
 constexpr int kFuseMaxN2 = 4;
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);
@@ -84,6 +91,7 @@ struct TcPlan {
   int splits;          // split-K factor (1 = none)
   float* ws;           // split-K partial tiles [batch*splits][m_tiles][n_tiles][128*BN]
   int* cnt;            // split-K arrival counters [batch][m_tiles][n_tiles] (self-resetting)
+  int ab16;            // bf16 operands (kind::f16)
 };
 // Device scratch the plans of one graph carve split-K workspaces from.
 struct SplitKPool {

@@ -13,6 +13,11 @@ floating-point error for each output element.
                                     2 * 2^-11 * |w||x|: Σ over a dot is 2^-10 *
                                     Σ|terms|), and normwise
                                     max|d| / max|ref| <= 5e-3
+  bf16 path (RS_FC_BF16, labelled   |gpu - ref| <= 2^-5 * mag elementwise
+  lower-precision variant):         (bf16 operands: unit roundoff 2^-8, so a
+                                    product is within 2^-7 |w||x|; activations
+                                    are re-rounded between layers; up to 4
+                                    layers) and normwise max|d|/max|ref| <= 3e-2
   SLS pooled sums:                  bit-identical to the oracle's canonical
                                     fp32 summation order
   DIN attention-pooled sums         Σ_l a_l e_l over L lookups accumulated in
@@ -30,6 +35,7 @@ import numpy as np
 
 FP32 = "fp32"
 TF32 = "tf32"
+BF16 = "bf16"
 TWO_M10 = 2.0 ** -10
 
 
@@ -38,6 +44,8 @@ def excess(got, ref, mag, path):
     d = np.abs(np.asarray(got, dtype=np.float64) - ref)
     if path == FP32:
         bound = 1e-5 * np.maximum(np.abs(ref), mag * TWO_M10)
+    elif path == BF16:
+        bound = 2.0 ** -5 * mag
     else:
         bound = TWO_M10 * mag
     return float(np.max(d / np.maximum(bound, 1e-300)))
@@ -51,9 +59,10 @@ def normwise(got, ref):
 def assert_close(got, ref, mag, path, what=""):
     x = excess(got, ref, mag, path)
     assert x <= 1.0, f"{what}: {path} rule exceeded by {x:.3g}x"
-    if path == TF32:
+    if path in (TF32, BF16):
         nw = normwise(got, ref)
-        assert nw <= 5e-3, f"{what}: tf32 normwise {nw:.3g} > 5e-3"
+        lim = 5e-3 if path == TF32 else 3e-2
+        assert nw <= lim, f"{what}: {path} normwise {nw:.3g} > {lim}"
     return x
 
 

@@ -138,3 +138,28 @@ def test_e2e_packed_host_queue_matches_oracle(model):
         assert_close(got, ref, mag, TF32, f"e2e {model} query {k} S={S}")
         assert np.array_equal(got, acc.forward(d, i)), k
     acc.close()
+
+
+@pytest.mark.parametrize("name", ["MT-WND", "WND", "NCF", "DLRM-RMC1", "DLRM-RMC2", "DLRM-RMC3",
+                                  "DIN", "DIEN", "cfg3-RMC2", "cfg3-RMC3"])
+def test_bf16_fc_variant(name):
+    """RS_FC_BF16 (labelled lower-precision variant): tcgen05 kind::f16 with
+    bf16 weights and activations, fp32 accumulate — within the stated bf16
+    rule of the fp64 oracle at S in {1, 129, 1000}; the embedding stage is the
+    fp32 one (SLS bit-exact)."""
+    from parity_rule import BF16
+    if name.startswith("cfg3"):
+        spec, rows = cfg3(name[-4:]), 2_000_000
+    else:
+        spec, rows = rs.builtin_model(name), 200_000
+    acc = rs.Accelerator(spec, rows, seed=3, max_query_size=1000, fc_mode=rs.FC_BF16)
+    assert acc.info.fc_layers_tcgen05 > 0
+    orc = Oracle(spec, rows, seed=3)
+    for k, S in enumerate((1, 129, 1000)):
+        dense, idx = rs.fill_query(spec, rows, 51, k, S)
+        out = acc.forward(dense, idx)
+        ref, mag, _, _ = orc.forward64(dense, idx)
+        assert_close(out, ref, mag, BF16, f"bf16 {name} S={S}")
+        if spec.embeddings.pooling == "Sum":
+            assert np.array_equal(acc.pooled(idx), orc.sls_canonical(idx))
+    acc.close()

@@ -4,7 +4,7 @@ forward (fp32 FFMA path and tf32 tcgen05 path) against the fp64 oracle.
 Prints one JSON object: max |gpu-ref|/mag (the tolerance-rule statistic),
 normwise max|gpu-ref|/max|ref|, and whether SLS pooled sums are bit-exact.
 
-  python tools/parity_report.py > profiles/parity_r1.json
+  python tools/parity_report.py > profiles/parity_r2.json
 """
 import json
 import os
@@ -34,13 +34,16 @@ def main():
         dense, idx = rs.fill_query(spec, rows, 103, 0, 200)
         ref, mag, pref, pmag = orc.forward64(dense, idx)
         row = {}
-        for mode, label in ((rs.FC_FP32, "fp32"), (rs.FC_TF32, "tf32")):
+        for mode, label in ((rs.FC_FP32, "fp32"), (rs.FC_TF32, "tf32"), (rs.FC_BF16, "bf16")):
             acc = rs.Accelerator(spec, rows, seed=3, max_query_size=200, fc_mode=mode)
             out = acc.forward(dense, idx).astype(np.float64)
             row[label] = {
                 "max_err_over_mag": float(np.max(np.abs(out - ref) / mag)),
                 "normwise_rel": float(np.max(np.abs(out - ref)) / np.max(np.abs(ref))),
                 "tcgen05_layers": acc.info.fc_layers_tcgen05,
+                # the SURVEY 8c statistic: max |d| / max(|ref|, mag 2^-10)
+                "max_err_over_survey_scale": float(np.max(np.abs(out - ref) / np.maximum(
+                    np.abs(ref), mag * 2.0 ** -10))),
             }
             if label == "fp32" and spec.embeddings.num_tables:
                 pooled = acc.pooled(idx).astype(np.float64)
