@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--L", type=int, default=0, help="override lookups_per_table")
     ap.add_argument("--S", type=int, default=300)
     ap.add_argument("--rows", type=int, default=1_000_000)
-    ap.add_argument("--fc", choices=["fp32", "tf32", "auto"], default="tf32")
+    ap.add_argument("--fc", choices=["fp32", "tf32", "auto", "bf16"], default="tf32")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--pooled", action="store_true", help="embedding stage only (rs_pooled)")
     args = ap.parse_args()
@@ -34,7 +34,7 @@ def main():
         spec, rows = rs.builtin_model(args.model), args.rows
     if args.L:
         spec.embeddings.lookups_per_table = args.L
-    mode = {"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO}[args.fc]
+    mode = {"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO, "bf16": rs.FC_BF16}[args.fc]
     acc = rs.Accelerator(spec, rows, max_query_size=max(args.S, 1), fc_mode=mode)
     dense, idx = rs.fill_query(spec, rows, 5, 0, args.S)
     for r in range(args.reps):

@@ -57,12 +57,15 @@ def layer_flops(workload, S):
     return out
 
 
+FC = os.environ.get("TP_FC", "auto")  # auto (tf32) | bf16
+
+
 def run_case(workload, S):
-    rep = os.path.join(ROOT, "gpurun_out", f"tp_{workload}_{S}.csv")
+    rep = os.path.join(ROOT, "gpurun_out", f"tp_{FC}_{workload}_{S}.csv")
     cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "--csv",
            "-k", "regex:fc_tc|gru_tc", "--log-file", rep,
            sys.executable, os.path.join(ROOT, "tools", "run_once.py"), "--workload", workload,
-           "--S", str(S), "--fc", "auto", "--reps", "2"]
+           "--S", str(S), "--fc", FC, "--reps", "2"]
     subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL)
     rows = list(csv.reader(open(rep)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
@@ -80,8 +83,10 @@ def run_case(workload, S):
 
 def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    tf32 = 0.5 * peaks["bf16_tflops"]
-    out = {"peak_tf32_tflops": tf32, "peak_source": "0.5 x MEASURED_PEAKS bf16_tflops",
+    tf32 = 0.5 * peaks["bf16_tflops"] if FC != "bf16" else peaks["bf16_tflops"]
+    out = {"fc": FC, "peak_tflops": tf32,
+           "peak_source": ("0.5 x MEASURED_PEAKS bf16_tflops (tf32 rate)" if FC != "bf16"
+                           else "MEASURED_PEAKS bf16_tflops"),
            "ncu": "--metrics " + ",".join(METRICS) + " --clock-control none (cold, serialised "
                   "launches; second forward of two)", "cases": []}
     for workload, S in CASES:
@@ -111,7 +116,7 @@ def main():
             inst = rec.get("sm__inst_executed_pipe_tensor_subpipe_hmma.sum")
             if "fc_tc_kernel<" in name and inst:
                 bn = int(name.split("fc_tc_kernel<")[1].split(",")[0])
-                rec["executed_mma_flops"] = inst * 2 * 128 * bn * 8
+                rec["executed_mma_flops"] = inst * 2 * 128 * bn * (16 if FC == "bf16" else 8)
                 rec["executed_over_algorithmic"] = rec["executed_mma_flops"] / fl if fl else None
             res.append(rec)
         tot_f = sum(r["flops"] or 0 for r in res)
