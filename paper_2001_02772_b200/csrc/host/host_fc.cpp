@@ -24,83 +24,96 @@ namespace {
 
 constexpr int kRows = 4;  // rows of x per pass over W^T
 
-typedef float v16 __attribute__((vector_size(64)));
-
-#define LOAD16(dst, p) std::memcpy(&(dst), (p), sizeof(v16))
-
-__attribute__((target_clones("avx512f", "avx2", "default")))
-void fc_rows(const float* __restrict__ x, int64_t m0, int64_t m1, int K, int N,
-             const float* __restrict__ wt, const float* __restrict__ b, int relu,
-             float* __restrict__ y) {
-  const int n32 = N / 32 * 32;
+// The register tile is 4 rows x 2 vectors of y held across the K loop: 8
+// accumulators + 2 W^T vectors. Its width follows the vector ISA so the tile
+// never spills: 2 x 16 floats with AVX-512 (32 zmm), 2 x 8 with AVX2 (16 ymm),
+// 2 x 4 otherwise.
+template <int W>
+__attribute__((always_inline)) inline void fc_rows_body(
+    const float* __restrict__ x, int64_t m0, int64_t m1, int K, int N,
+    const float* __restrict__ wt, const float* __restrict__ b, int relu, float* __restrict__ y) {
+  typedef float vec __attribute__((vector_size(W * 4)));
+  constexpr int TW = 2 * W;  // tile columns
+  const int nt = N / TW * TW;
   for (int64_t m = m0; m < m1; m += kRows) {
     const int nr = (int)std::min<int64_t>(kRows, m1 - m);
-    if (nr == kRows && n32 > 0) {
-      // 4 rows x 32 columns of y in eight vector registers across the K loop
-      for (int n0 = 0; n0 < n32; n0 += 32) {
-        v16 acc[kRows][2];
+    if (nr == kRows && nt > 0) {
+      for (int n0 = 0; n0 < nt; n0 += TW) {
+        vec acc[kRows][2];
         for (int r = 0; r < kRows; ++r) {
-          acc[r][0] = v16{};
-          acc[r][1] = v16{};
+          acc[r][0] = vec{};
+          acc[r][1] = vec{};
           if (b) {
-            LOAD16(acc[r][0], b + n0);
-            LOAD16(acc[r][1], b + n0 + 16);
+            std::memcpy(&acc[r][0], b + n0, sizeof(vec));
+            std::memcpy(&acc[r][1], b + n0 + W, sizeof(vec));
           }
         }
         for (int k = 0; k < K; ++k) {
-          v16 w0, w1;
-          LOAD16(w0, wt + (int64_t)k * N + n0);
-          LOAD16(w1, wt + (int64_t)k * N + n0 + 16);
+          vec w0, w1;
+          std::memcpy(&w0, wt + (int64_t)k * N + n0, sizeof(vec));
+          std::memcpy(&w1, wt + (int64_t)k * N + n0 + W, sizeof(vec));
           for (int r = 0; r < kRows; ++r) {
-            const float a = x[(m + r) * K + k];
-            acc[r][0] += a * w0;
-            acc[r][1] += a * w1;
+            const float av = x[(m + r) * K + k];
+            acc[r][0] += av * w0;
+            acc[r][1] += av * w1;
           }
         }
         for (int r = 0; r < kRows; ++r) {
           if (relu) {
-            acc[r][0] = acc[r][0] > 0.0f ? acc[r][0] : v16{};
-            acc[r][1] = acc[r][1] > 0.0f ? acc[r][1] : v16{};
+            acc[r][0] = acc[r][0] > 0.0f ? acc[r][0] : vec{};
+            acc[r][1] = acc[r][1] > 0.0f ? acc[r][1] : vec{};
           }
-          std::memcpy(y + (m + r) * N + n0, &acc[r][0], sizeof(v16));
-          std::memcpy(y + (m + r) * N + n0 + 16, &acc[r][1], sizeof(v16));
+          std::memcpy(y + (m + r) * N + n0, &acc[r][0], sizeof(vec));
+          std::memcpy(y + (m + r) * N + n0 + W, &acc[r][1], sizeof(vec));
         }
       }
-      if (n32 == N) continue;
+      if (nt == N) continue;
     }
-    const int nb = (nr == kRows) ? n32 : 0;  // columns already written
+    const int nb = (nr == kRows) ? nt : 0;  // columns already written
     float* __restrict__ yr[kRows];
     for (int r = 0; r < kRows; ++r) yr[r] = y + (m + std::min(r, nr - 1)) * N;
     for (int r = 0; r < nr; ++r)
       for (int n = nb; n < N; ++n) yr[r][n] = b ? b[n] : 0.0f;
     for (int k = 0; k < K; ++k) {
       const float* __restrict__ w = wt + (int64_t)k * N;
-      if (nr == kRows) {
-        const float a0 = x[(m + 0) * K + k], a1 = x[(m + 1) * K + k];
-        const float a2 = x[(m + 2) * K + k], a3 = x[(m + 3) * K + k];
-        float* __restrict__ y0 = yr[0];
-        float* __restrict__ y1 = yr[1];
-        float* __restrict__ y2 = yr[2];
-        float* __restrict__ y3 = yr[3];
-        for (int n = nb; n < N; ++n) {
-          const float wn = w[n];
-          y0[n] += a0 * wn;
-          y1[n] += a1 * wn;
-          y2[n] += a2 * wn;
-          y3[n] += a3 * wn;
-        }
-      } else {
-        for (int r = 0; r < nr; ++r) {
-          const float a = x[(m + r) * K + k];
-          float* __restrict__ yy = yr[r];
-          for (int n = nb; n < N; ++n) yy[n] += a * w[n];
-        }
+      for (int r = 0; r < nr; ++r) {
+        const float av = x[(m + r) * K + k];
+        float* __restrict__ yy = yr[r];
+        for (int n = nb; n < N; ++n) yy[n] += av * w[n];
       }
     }
     if (relu)
       for (int r = 0; r < nr; ++r)
         for (int n = nb; n < N; ++n) yr[r][n] = yr[r][n] > 0.0f ? yr[r][n] : 0.0f;
   }
+}
+
+__attribute__((target("avx512f"))) void fc_rows_avx512(const float* x, int64_t m0, int64_t m1,
+                                                       int K, int N, const float* wt,
+                                                       const float* b, int relu, float* y) {
+  fc_rows_body<16>(x, m0, m1, K, N, wt, b, relu, y);
+}
+__attribute__((target("avx2,fma"))) void fc_rows_avx2(const float* x, int64_t m0, int64_t m1,
+                                                      int K, int N, const float* wt,
+                                                      const float* b, int relu, float* y) {
+  fc_rows_body<8>(x, m0, m1, K, N, wt, b, relu, y);
+}
+void fc_rows_sse(const float* x, int64_t m0, int64_t m1, int K, int N, const float* wt,
+                 const float* b, int relu, float* y) {
+  fc_rows_body<4>(x, m0, m1, K, N, wt, b, relu, y);
+}
+
+void fc_rows(const float* x, int64_t m0, int64_t m1, int K, int N, const float* wt,
+             const float* b, int relu, float* y) {
+  static const int isa = [] {
+    __builtin_cpu_init();
+    if (__builtin_cpu_supports("avx512f")) return 2;
+    if (__builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma")) return 1;
+    return 0;
+  }();
+  if (isa == 2) fc_rows_avx512(x, m0, m1, K, N, wt, b, relu, y);
+  else if (isa == 1) fc_rows_avx2(x, m0, m1, K, N, wt, b, relu, y);
+  else fc_rows_sse(x, m0, m1, K, N, wt, b, relu, y);
 }
 
 }  // namespace
