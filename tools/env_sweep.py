@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--pool", type=int, default=256)
     ap.add_argument("--depth", type=int, default=8)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--size-fixed", type=int, default=0)
+    ap.add_argument("--fc", default="auto", choices=["auto", "tf32", "fp32", "bf16"])
     ap.add_argument("settings", nargs="+")
     args = ap.parse_args()
     import torch
@@ -32,6 +34,8 @@ def main():
     _, sizes = rs.gen_trace(42, 1000.0, rs.SizeDistribution.log_normal(math.log(300), 0.5),
                             args.pool)
     sizes = np.minimum(sizes, 1000)
+    if args.size_fixed:
+        sizes = np.full(args.pool, args.size_fixed, dtype=np.int64)
     dq, iq = [], []
     for q in range(args.pool):
         d, i = rs.fill_query(spec, rows, 42, q, int(sizes[q]))
@@ -48,9 +52,11 @@ def main():
                 k, v = kv.split("=")
                 saved[k] = os.environ.get(k)
                 os.environ[k] = v
-            acc = rs.Accelerator(spec, rows, seed=1, max_query_size=1000, fc_mode=rs.FC_AUTO,
-                                 queue_depth=args.depth)
-            o = torch.empty((1000, acc.output_dim), device="cuda")
+            fc = {"auto": rs.FC_AUTO, "tf32": rs.FC_TF32, "fp32": rs.FC_FP32,
+                  "bf16": rs.FC_BF16}[args.fc]
+            acc = rs.Accelerator(spec, rows, seed=1, max_query_size=max(1000, args.size_fixed),
+                                 fc_mode=fc, queue_depth=args.depth)
+            o = torch.empty((max(1000, args.size_fixed), acc.output_dim), device="cuda")
             b = acc.batch([int(sizes[q]) for q in qs], [dq[q].data_ptr() for q in qs],
                           [iq[q].data_ptr() for q in qs], [o.data_ptr()] * len(qs),
                           rs.MEM_DEVICE)
