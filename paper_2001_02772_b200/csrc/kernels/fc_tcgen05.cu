@@ -748,7 +748,10 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
     const char* e = getenv("RS_TC_WIDE_K1");
     return e ? atoi(e) : 2048;
   }();
-  const bool wide = a.K >= (a.batch > 1 ? wide_k : wide_k1) || ctas > 148;
+  // batched stacks (MT-WND's 4 towers) are feed-bound at every layer: the
+  // shallow 2-per-SM tiles also for their narrow last layer (512 -> 256:
+  // 14.2 -> 13.2 us/query pipelined at 256 items, tools/env_sweep.py)
+  const bool wide = a.K >= (a.batch > 1 ? wide_k : wide_k1) || ctas > 148 || a.batch > 1;
   p->cfg = a.N >= 128 ? (wide ? 0 : 2) : (wide ? 1 : 3);
   // cfg 4 <256,4>: one CTA covers 256 output columns (half the CTAs of a
   // 512-wide layer, same k-block round trips per CTA); RS_TC_WIDE=1 selects it
