@@ -857,7 +857,8 @@ def main():
     ap.add_argument("--fc", choices=["fp32", "tf32", "auto", "bf16"], default="auto",
                     help="bf16 = labelled lower-precision variant (bf16 weights/activations)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--depth", type=int, default=8, help="queries in flight per GPU (lanes)")
+    ap.add_argument("--depth", type=int, default=16,
+                    help="queries in flight per GPU (lanes): 16 = 8 within 0.4% on cfg3, 2-26% faster for small queries (DESIGN.md §5a)")
     ap.add_argument("--roofline", choices=["auto", "hbm", "tensor"], default="auto",
                     help="which kernel the roofline object reports (auto: tensor for "
                          "mt-wnd/wnd, else the embedding kernel)")

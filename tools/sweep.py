@@ -21,12 +21,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workloads", default=",".join(ALL))
+    ap.add_argument("--extra", default="", help="extra bench.py flags, e.g. '--fc bf16 --no-cpu'")
     args = ap.parse_args()
     os.makedirs(args.out, exist_ok=True)
     rows = []
     for w in args.workloads.split(","):
         cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", w, "--steps",
-               str(args.steps), "--warmup", str(args.warmup)]
+               str(args.steps), "--warmup", str(args.warmup)] + args.extra.split()
         r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
         line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
         if r.returncode != 0 or not line:
@@ -42,9 +43,10 @@ def main():
             "qps_at_sla": round(d["value"]), "mean_service_us": round(
                 d["sla"]["mean_service_ms"] * 1e3, 1),
             "e2e_qps": round(d["e2e"]["value"]), "h2d_gbs": round(d["e2e"]["h2d_gbs"], 1),
-            "gather_gbs": round(d["roofline"]["achieved"]), "gather_frac": round(
-                d["roofline"]["frac"], 3),
-            "cpu_qps": round(cb.get("value", 0), 1), "cpu_cores": cb.get("cores"),
+            "roofline_bound": d["roofline"]["bound"], "roofline_kernel": d["roofline"]["kernel"],
+            "roofline_achieved": round(d["roofline"]["achieved"], 1),
+            "roofline_unit": d["roofline"]["unit"], "roofline_frac": round(d["roofline"]["frac"], 3),
+            "cpu_deeprecsched_qps": round(cb.get("value", 0), 1), "cpu_cores": cb.get("cores"),
             "e2e_over_cpu": round(d["e2e"]["value"] / cb["value"], 1) if cb.get("value") else None,
             "clocks_sm_mhz": d["clocks"].get("sm_mhz")})
         print(json.dumps(rows[-1]), flush=True)
