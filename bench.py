@@ -148,6 +148,7 @@ def make_config(args, name, shape, rows, sizes, world, sla):
             f"LABELLED variant (SURVEY 8d): bounded power law alpha={args.zipf:g} "
             "over [0, rows), low ids hot" if args.zipf > 0 else "uniform"),
         "l2_persist_mb": args.l2_persist_mb,
+        **({"rnn_cell": args.rnn} if args.rnn != "gru" else {}),
     }
 
 
@@ -419,7 +420,8 @@ def run_ours(args, rank, world, local):
     acc = rs.Accelerator(spec, rows, seed=1, device=local, max_query_size=args.max_query,
                          fc_mode={"fp32": rs.FC_FP32, "tf32": rs.FC_TF32, "auto": rs.FC_AUTO,
                                   "bf16": rs.FC_BF16}[args.fc],
-                         queue_depth=args.depth, l2_persist_mb=args.l2_persist_mb)
+                         queue_depth=args.depth, l2_persist_mb=args.l2_persist_mb,
+                         rnn_cell=rs.RNN_AUGRU if args.rnn == "augru" else rs.RNN_GRU)
     if args.merge > 1:
         acc.set_option(rs.OPT_MERGE_QUERIES, args.merge)
     e = spec.embeddings
@@ -696,8 +698,11 @@ def run_serve(args):
                            fc_mode=fc, queue_depth=args.depth) for r in range(K)]
     P = 2 * args.queries_per_step
     seed = rank_seed(0)
-    _, pool_sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
-        math.log(args.size_median), 0.5), P)
+    if args.size_fixed:
+        pool_sizes = np.full(P, args.size_fixed, dtype=np.int64)
+    else:
+        _, pool_sizes = rs.gen_trace(seed, 1000.0, rs.SizeDistribution.log_normal(
+            math.log(args.size_median), 0.5), P)
     pool_sizes = np.minimum(pool_sizes, args.max_query)
     device_inputs = args.serve_inputs == "device"
     if device_inputs and K > 1:
@@ -859,6 +864,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--depth", type=int, default=16,
                     help="queries in flight per GPU (lanes): 16 = 8 within 0.4% on cfg3, 2-26% faster for small queries (DESIGN.md §5a)")
+    ap.add_argument("--rnn", choices=["gru", "augru"], default="gru",
+                    help="AttentionRNN cell (DIEN): AUGRU = the explicit extension of SURVEY D3")
     ap.add_argument("--roofline", choices=["auto", "hbm", "tensor"], default="auto",
                     help="which kernel the roofline object reports (auto: tensor for "
                          "mt-wnd/wnd, else the embedding kernel)")

@@ -61,8 +61,19 @@ def main():
                           [iq[q].data_ptr() for q in qs], [o.data_ptr()] * len(qs),
                           rs.MEM_DEVICE)
             acc.forward_many(None, prepared=b)
-            svc = acc.forward_many(None, prepared=b)
-            rec = {"setting": setting, "rep": rep, "us_per_query": float(svc.mean() * 1e3)}
+            import time as _t
+            with bench.ClockSampler(0) as clk:
+                _t.sleep(0.6)  # nvidia-smi start-up
+                t0 = _t.time()
+                svc = np.concatenate([acc.forward_many(None, prepared=b) for _ in range(4)])
+                clk.mark(t0, _t.time())
+            c = clk.summary()
+            pw = [float(ln.split(",")[2]) for ts, ln in clk.lines
+                  if t0 - 0.03 <= ts <= clk.window[1] + 0.03 and len(ln.split(",")) >= 3
+                  and ln.split(",")[2].strip() not in ("", "[N/A]")]
+            rec = {"setting": setting, "rep": rep, "us_per_query": float(svc.mean() * 1e3),
+                   "sm_mhz": c["sm_mhz"], "reasons": c["reasons"],
+                   "power_w_median": float(np.median(pw)) if pw else None}
             out.append(rec)
             print(json.dumps(rec), flush=True)
             acc.close()
