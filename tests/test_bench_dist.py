@@ -55,3 +55,38 @@ def test_two_rank_aggregation_gloo():
 def test_single_process_aggregation_is_identity():
     agg = bench.aggregate(123.0, 0.5, queries=10, world=1)
     assert agg == {"time_s": 0.5, "value": 123.0, "saturated_qps": 20.0}
+
+
+@pytest.mark.parametrize("workload", ["cfg3-rmc2", "cfg3-rmc3", "cfg1-rmc1", "cfg5-dien",
+                                      "cfg5-din", "mt-wnd", "ncf"])
+def test_reference_arm_config_equals_ours(workload):
+    """The driver compares the two arms' `config` objects: the reference arm
+    builds its workload from the compiled reference's zoo (no product import),
+    ours from the product's mirror — same shapes, sizes, SLA, hence the same
+    config dict."""
+    import argparse
+    import math
+    import numpy as np
+    import bench
+    import paper_2001_02772_b200 as rs
+    from oracle import cpu_arm
+    if not cpu_arm.available():
+        pytest.skip("oracle/_ref not built")
+    args = argparse.Namespace(workload=workload, queries_per_step=256, steps=20, index_bits=64,
+                              dense_bits=32, size_median=300.0, max_query=1000, fc="auto",
+                              merge=1, zipf=0.0, l2_persist_mb=0, size_fixed=0, rnn="gru",
+                              sla=0.0)
+    spec, rows, zoo = bench.workload_spec(rs, workload)
+    _, sizes = rs.gen_trace(bench.rank_seed(0), 1000.0,
+                            rs.SizeDistribution.log_normal(math.log(300.0), 0.5), 512)
+    e = spec.embeddings
+    ours = bench.make_config(args, spec.name, (e.num_tables, e.lookups_per_table,
+                                               e.embedding_dim, spec.dense_input_dim),
+                             rows, np.minimum(sizes, 1000), 1,
+                             bench.sla_for(args, zoo, rs.sla_target))
+    m, rows2, zoo2 = bench.workload_or_model(workload)
+    sizes2 = cpu_arm.gen_trace_sizes(bench.rank_seed(0), math.log(300.0), 0.5, 512, 1000)
+    theirs = bench.make_config(args, m.name.decode(), (m.T, m.L, m.D, m.dense_in), rows2,
+                               np.minimum(sizes2, 1000), 1,
+                               bench.sla_for(args, zoo2, cpu_arm.sla_target))
+    assert ours == theirs
