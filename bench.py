@@ -337,6 +337,10 @@ def cpu_deeprecsched(args, workload, sla, rounds, budget_s, threads=0, rank=0):
 
 
 def cpu_sample_text(res, rounds):
+    if res.get("infeasible"):
+        return (f"{rounds} timing rounds of the oracle fp32 forward on requests of "
+                f"{res['table']['request_items']} items on {res['threads']} cores "
+                f"({res['rows']:,} rows/table): {res['infeasible']} -> 0 QPS at this SLA")
     return (f"{rounds} timing rounds: oracle fp32 forward (oracle/forward.c) on requests of "
             f"{res['table']['request_items']} items, each timed with 1 and with all "
             f"{res['threads']} cores busy, tables materialised at {res['rows']:,} rows/table "
@@ -387,7 +391,8 @@ def run_reference(args, rank, world):
             "impl": "reference", "config": cfg,
             "method": "CPU-only DeepRecSched on this host: reference tune() over measured "
                       "per-request times (oracle/cpu_arm.py)",
-            "cpu_deeprecsched": {"batch": res["batch"], "p95_ms": res["p95_s"] * 1e3,
+            "cpu_deeprecsched": {"batch": res["batch"],
+                                 "p95_ms": res["p95_s"] * 1e3 if res["p95_s"] else None,
                                  "tune_search_steps": res["search_steps"],
                                  "request_time_table": res["table"]},
             "cpu_baseline": cb, "gpu_launches": 0,

@@ -170,6 +170,10 @@ class CpuDeepRecSched:
         rc = ref_cpu.ref_tune(C.byref(self.model), b"measured", b"", sla, seed, kind, mu,
                               sigma, 0.0, 0.0, max_size, n, 1, C.byref(b), C.byref(t),
                               C.byref(q), C.byref(p), C.byref(f), C.byref(steps))
+        if rc == -5:  # recsim::InfeasibleSLA: no batch size meets the SLA on these cores
+            return {"batch": None, "qps": 0.0, "p95_s": None, "search_steps": None,
+                    "infeasible": "reference tune(): no CPU batch size meets the SLA "
+                                  "(InfeasibleSLA, autotune.cpp)"}
         if rc:
             raise RuntimeError(f"ref_tune rc={rc}")
         return {"batch": b.value, "qps": q.value, "p95_s": p.value, "search_steps": steps.value}

@@ -233,7 +233,9 @@ int64_t or_pooled_dim(const or_state* s) { return s->pooled_dim; }
 #undef FN
 #define REAL float
 #define FN(x) x##_f32
+#define FAST_FC 1
 #include "forward_impl.h"
+#undef FAST_FC
 #undef REAL
 #undef FN
 

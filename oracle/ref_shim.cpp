@@ -84,7 +84,8 @@ CpuPlatformSpec shim_cpu(const char* name) {
   return builtin_cpu(name);
 }
 
-// 0 ok, -1 invalid_argument, -2 UnknownModel, -3 ConfigError, -4 InvalidDistribution
+// 0 ok, -1 invalid_argument, -2 UnknownModel, -3 ConfigError, -4 InvalidDistribution,
+// -5 InfeasibleSLA (tune(): no batch size meets the SLA)
 template <class F>
 int guard(F&& f) {
   try {
@@ -96,6 +97,8 @@ int guard(F&& f) {
     return -3;
   } catch (const InvalidDistribution&) {
     return -4;
+  } catch (const InfeasibleSLA&) {
+    return -5;
   } catch (const std::invalid_argument&) {
     return -1;
   } catch (...) {

@@ -9,3 +9,4 @@ timeout 900 python tools/env_sweep.py --workload mt-wnd --reps 2 --n 1024 "RS_X=
 timeout 900 python bench.py --workload cfg5-dien --rnn augru --no-cpu --steps 10 --warmup 3 > gpurun_out/bench_dien_augru.json 2> gpurun_out/bench_dien_augru.err
 timeout 900 python bench.py --workload cfg5-dien --no-cpu --steps 10 --warmup 3 > gpurun_out/bench_dien_gru.json 2>> gpurun_out/bench_dien_augru.err
 timeout 900 python bench.py --serve --gpus 1 --workload ncf --size-fixed 1 --serve-inputs device --serve-n 100000 > gpurun_out/serve_dispatch_ncf1.json 2> gpurun_out/serve_dispatch.err
+timeout 900 python tools/env_sweep.py --reps 2 --n 4096 "RS_DIAG_SKIP=2" "RS_DIAG_SKIP=2,RS_DIAG_EMPTY=1,RS_DIAG_EMPTY_CTAS=1" "RS_DIAG_SKIP=2,RS_DIAG_EMPTY=1,RS_DIAG_EMPTY_CTAS=296" "RS_DIAG_SKIP=2,RS_DIAG_EMPTY=3,RS_DIAG_EMPTY_CTAS=1" > gpurun_out/env_empty.json 2> gpurun_out/env_empty.err
