@@ -757,6 +757,11 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   // 512-wide layer, same k-block round trips per CTA); RS_TC_WIDE=1 selects it
   // for the latency-bound layers with N >= 256
   if (!wide && a.N >= 256 && getenv("RS_TC_WIDE") && atoi(getenv("RS_TC_WIDE"))) p->cfg = 4;
+  // batched tf32 stacks of >= 256 outputs (MT-WND's towers): <256,4> halves
+  // the re-reads of the shared A tile per flop (MT-WND 18.0 -> 17.0 us/query,
+  // 1024-item queries 49.8 -> 46.8; neutral for bf16 operands, whose k-slabs
+  // already carry twice the flops: tools/env_sweep.py, profiles/r2_fc_tiles/)
+  if (a.batch > 1 && a.N >= 256 && !a.ab16) p->cfg = 4;
   if (const char* e = getenv("RS_TC_CFG")) p->cfg = std::min(4, std::max(0, atoi(e)));
   if (p->cfg == 4 && a.N < 256) p->cfg = 2;
   if (a.single_n_tile && a.N <= 128 && (p->cfg == 1 || p->cfg == 3)) p->cfg -= 1;
