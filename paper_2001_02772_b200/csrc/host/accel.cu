@@ -452,10 +452,20 @@ bool fuse_enabled() {
   return !v || atoi(v) != 0;
 }
 
+// RS_DISCARD (default 1): dead intermediates are dropped from L2 with
+// discard.global.L2 instead of being written back to DRAM (pooled sums after
+// the interaction, FC activations after their only reader): in the pipelined
+// queue those write-backs turn the gather's read stream around
+// (tools/range_traffic.py: 1.25 -> 0.58 GB written per 256 queries)
+bool discard_enabled() {
+  const char* v = getenv("RS_DISCARD");
+  return !v || atoi(v) != 0;
+}
+
 int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, const float* in0,
                   int64_t ld_in0, int64_t in0_rows, float* const* tmp, int64_t ld_tmp,
                   float* final_out, int64_t ld_final, int64_t final_sCz, bool allow_tc,
-                  cudaStream_t st, bool final_to_desc = false) {
+                  cudaStream_t st, bool final_to_desc = false, bool in0_discardable = false) {
   const int64_t maxS = a->init.max_query_size;
   // The whole stack as one tcgen05 kernel when every layer fits (activations
   // stay in shared memory between layers): one launch instead of one per layer.
@@ -514,6 +524,16 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
       }
       TcPlan p;
       if (tc_plan(&p, args, maxS, a_rows, &s->splitk) && (!fuse || p.n_tiles == 1)) {
+        // dead-data discard (RS_DISCARD): a single-N-tile layer is the only
+        // reader of its input rows (the previous layer's activations); the
+        // second layer also drops the stack input, read by layer 0 only
+        if (discard_enabled() && f.batch == 1 && p.n_tiles == 1 && p.splits <= 1 && l >= 1) {
+          args.discard_a = 1;
+          if (l == 1 && in0_discardable) {
+            args.dz = in0;
+            args.dz_ld = ld_in0 * 4;
+          }
+        }
         launch_fc_tc(s->d_q, p, args, st);
         used_tc = true;
         ++tc_count;
@@ -726,7 +746,8 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
                             : -1;
           ntc += u >= 0 ? u
                         : enqueue_stack(a, s, a->dense_layers, s->dense_stage, a->ld_dense, maxS,
-                                        s->act, a->max_dense_w, s->X, a->ld_x, 0, tc, bs);
+                                        s->act, a->max_dense_w, s->X, a->ld_x, 0, tc, bs,
+                                        false, /*in0_discardable=*/true);
         }
       } else {
         launch_stage_dense(s->d_q, a->dense_in, s->X, a->ld_x, maxS, s->dense_sms, bs);
@@ -762,7 +783,7 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
       ntc += u >= 0 ? u
                     : enqueue_stack(a, s, a->pred_layers, s->X, a->ld_x, maxS, s->pact,
                                     a->max_pred_w, s->out, a->out_w, a->out_dim, tc, st,
-                                    /*final_to_desc=*/true);
+                                    /*final_to_desc=*/true, /*in0_discardable=*/true);
     }
     if (stage_stamp) RS_CUDA(cudaEventRecordWithFlags(s->kev[3], st, cudaEventRecordExternal));
   }

@@ -808,7 +808,7 @@ constexpr int kInterRegs = 8;  // float4 loads in flight per thread per round
 __global__ void __launch_bounds__(kInterThreads)
 interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
                    int64_t ld_pooled, int T, int D, float* __restrict__ X, int64_t ld_x,
-                   int64_t sum_off, int64_t dot_off, int has_dense) {
+                   int64_t sum_off, int64_t dot_off, int has_dense, int discard) {
   pdl_wait();  // pooled (SLS) and X[:, 0:D] (bottom MLP) are predecessors' outputs
   extern __shared__ float sv[];  // [(T+1)][D+1]
   const int P = has_dense ? (T + 1) * T / 2 : 0;
@@ -854,6 +854,14 @@ interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ poole
       }
     }
     __syncthreads();
+    if (discard) {
+      // the item's pooled sums are dead once staged: drop their L2 lines
+      // without a DRAM write-back (discard.global.L2, 128-byte lines)
+      const char* row = reinterpret_cast<const char*>(pooled + item * ld_pooled);
+      const int lines = (int)((int64_t)T * D * 4 / 128);
+      for (int i = threadIdx.x; i < lines; i += blockDim.x)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + 128 * i) : "memory");
+    }
     pdl_trigger();  // the predict layer's grid may launch while the dots run
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
       float s = 0.f;
@@ -1429,8 +1437,13 @@ void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled,
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(interaction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+  // RS_DISCARD (default 1): discard the pooled rows from L2 once staged (the
+  // forward graph's pooled buffer is internal; needs 128-byte row alignment)
+  const int discard = env_int("RS_DISCARD", 1) && (T * D * 4) % 128 == 0 &&
+                      (reinterpret_cast<uintptr_t>(pooled) & 127) == 0 &&
+                      (ld_pooled * 4) % 128 == 0;
   launch_pdl(interaction_kernel, dim3(grid), dim3(kInterThreads), smem, s, qd, pooled, ld_pooled,
-             T, D, X, ld_x, sum_off, dot_off, has_dense);
+             T, D, X, ld_x, sum_off, dot_off, has_dense, discard);
 }
 
 // Dense features into the FC staging buffer: [S, dense_in] contiguous (the

@@ -94,6 +94,19 @@ __device__ __forceinline__ uint32_t idesc_bf16() {
          ((uint32_t)(BM >> 4) << 24);
 }
 
+// Discard rows [r0, r1) of a row-major buffer (row stride ld bytes) from L2:
+// only the 128-byte lines lying entirely inside the range (the partial lines
+// at its ends may hold live neighbour rows). All threads of the CTA take part.
+__device__ __forceinline__ void discard_rows(const char* base, int64_t ld, int64_t r0,
+                                             int64_t r1) {
+  if (r1 <= r0) return;
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(base + r0 * ld);
+  const uintptr_t hi = reinterpret_cast<uintptr_t>(base + r1 * ld);
+  const uintptr_t first = (lo + 127) & ~uintptr_t(127), last = hi & ~uintptr_t(127);
+  for (uintptr_t p = first + 128 * threadIdx.x; p + 128 <= last; p += 128 * blockDim.x)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 // bf16 pair -> one 32-bit word (round to nearest even)
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
@@ -240,6 +253,14 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
     // trigger late (accumulation done): the next layer's CTAs launch during
     // this epilogue instead of squatting on the SM through the main loop
     pdl_trigger();
+    if (a.discard_a || a.dz) {
+      // every k-slab of this tile's A rows has been consumed (tmem_full): the
+      // rows are dead, drop their L2 lines without a DRAM write-back
+      const int64_t r1 = min((int64_t)m0 + BM, M);
+      if (a.discard_a)
+        discard_rows(reinterpret_cast<const char*>(a.A), a.lda * (H ? 2 : 4), m0, r1);
+      if (a.dz) discard_rows(reinterpret_cast<const char*>(a.dz), a.dz_ld, m0, r1);
+    }
     const int quad = warp;
     const int64_t m = m0 + quad * 32 + lane;
 #if RS_EXPERIMENTS

@@ -75,6 +75,11 @@ struct FcArgs {
   // RS_FC_BF16: A and W hold bfloat16 (row strides in elements); c16: C is
   // written as bfloat16 (the next bf16 layer's A). tcgen05 only.
   int ab16; int c16;
+  // Dead-data discard (discard.global.L2, no DRAM write-back): discard_a = this
+  // CTA is the only reader of its A rows (one N tile, batch 1), drop them after
+  // the main loop; dz = another dead buffer whose rows [m0, m0+128) this CTA
+  // drops too (row stride dz_ld bytes) — e.g. the stack input two layers back.
+  int discard_a; const void* dz; int64_t dz_ld;
 };
 constexpr int kFuseMaxN2 = 4;
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);
