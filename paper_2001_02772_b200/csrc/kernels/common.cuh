@@ -146,18 +146,22 @@ inline void smem_attr(const void* fn, int bytes) {
   }
 }
 
+// RS_CARVEOUT=<p>: every kernel prefers the SAME shared-memory carveout (p% of
+// the unified L1/shared array; 1 = maximum shared), so an SM never has to
+// drain to switch configurations when kernels with different shared-memory
+// needs alternate on it; 0/unset = the driver's per-kernel choice.
 inline void max_carveout(const void* fn) {
   static std::mutex mu;
   static std::set<std::pair<int, const void*>> done;
-  static const bool on = [] {
+  static const int pct = [] {
     const char* v = getenv("RS_CARVEOUT");
-    return v && atoi(v) != 0;
+    const int p = v ? atoi(v) : 0;
+    return p == 1 ? (int)cudaSharedmemCarveoutMaxShared : p;
   }();
-  if (!on) return;
+  if (pct <= 0) return;
   std::lock_guard<std::mutex> g(mu);
   if (done.insert({current_device(), fn}).second)
-    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 #if defined(__CUDACC__)
