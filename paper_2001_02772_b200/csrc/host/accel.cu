@@ -157,6 +157,14 @@ struct rs_accel {
   int depth = 2;
   int64_t merge_queries = 1;  // RS_OPT_MERGE_QUERIES (1 = one query per launch)
   int stage_timing = 0;       // RS_OPT_STAGE_TIMING
+  // Uniform shared-memory carveout (% of the unified L1/shared array) set on
+  // every kernel node of the forward graphs, with the tcgen05 FC tiles held
+  // to a shared-memory budget that fits it: an SM never has to drain to
+  // switch its L1/shared split when a 192 KB FC tile lands between gather
+  // CTAs, and the gathers keep their L1 for in-flight loads.
+  // 0 = the driver's per-kernel choice and the deep FC tiles.
+  int carveout_pct = 0;
+  int fc_smem_kb = 0;         // FC tile shared-memory budget (0 = none)
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t lane_join[kMaxLanes] = {};
@@ -506,6 +514,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
       args.C = tmp[l & 1]; args.ldc = ld_tmp; args.sCz = maxS * ld_tmp;
     }
     args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
+    args.smem_cap_kb = a->fc_smem_kb;
     bool used_tc = false;
     if (allow_tc) {
       // A narrow final layer (<= 4 outputs: the DLRM / DIN / DIEN logits)
@@ -578,6 +587,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
     x.bias = f.b; x.sbz = f.out;
     x.N = (int)f.out; x.K = (int)f.in; x.relu = f.relu; x.batch = f.batch;
     x.ab16 = 1;
+    x.smem_cap_kb = a->fc_smem_kb;
     return x;
   };
   // can layer l run as a bf16 tcgen05 layer reading A (dry-run plan)?
@@ -605,6 +615,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
       args.W = f.W; args.ldw = f.ldk; args.sWz = f.out * f.ldk;
       args.bias = f.b; args.sbz = f.out;
       args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
+      args.smem_cap_kb = a->fc_smem_kb;
     }
     const bool fuse = l + 2 == layers.size() && layers[l + 1].out <= kFuseMaxN2 &&
                       f.out <= 128 && fuse_enabled();
@@ -811,6 +822,12 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
       v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       RS_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v));
+    }
+    if (a->carveout_pct > 0) {  // one shared-memory carveout for every kernel node
+      cudaKernelNodeAttrValue v{};
+      v.sharedMemCarveout = (unsigned)a->carveout_pct;
+      RS_CUDA(cudaGraphKernelNodeSetAttribute(
+          nd, cudaKernelNodeAttributePreferredSharedMemoryCarveout, &v));
     }
   }
   cudaGraphExec_t exec = nullptr;
@@ -1563,6 +1580,18 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     a->m = *model;
     a->init = *init;
     a->depth = init->queue_depth > 0 ? std::min<int>(init->queue_depth, rs_accel::kMaxLanes) : 4;
+    {
+      // carveout policy (tools/env_sweep.py, profiles/r2_carveout/): models
+      // whose embedding stage bounds the queue (Sum, AttentionFC,
+      // AttentionRNN pooling) get the uniform carveout and the shallow FC
+      // tiles — cfg3 RMC2 -6%, zoo RMC2 -9%, DIN -4%, DIEN -5%, RMC1/RMC3
+      // within 2%; Concat models are FC-bound and keep the deep tiles (MT-WND
+      // +45%, WND +3.5% with the carveout). RS_CARVEOUT=<pct> overrides, 0 = off
+      const bool gather_bound = model->num_tables > 0 && model->pooling != RS_POOL_CONCAT;
+      const char* cv = getenv("RS_CARVEOUT");
+      a->carveout_pct = cv ? std::max(0, std::min(100, atoi(cv))) : (gather_bound ? 50 : 0);
+      a->fc_smem_kb = a->carveout_pct > 0 ? 110 : 0;
+    }
     a->device = device;
     a->sm_count = prop.multiProcessorCount;
     a->l2_bytes = prop.l2CacheSize;

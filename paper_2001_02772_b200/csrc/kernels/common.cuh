@@ -146,15 +146,15 @@ inline void smem_attr(const void* fn, int bytes) {
   }
 }
 
-// RS_CARVEOUT=<p>: every kernel prefers the SAME shared-memory carveout (p% of
-// the unified L1/shared array; 1 = maximum shared), so an SM never has to
-// drain to switch configurations when kernels with different shared-memory
-// needs alternate on it; 0/unset = the driver's per-kernel choice.
+// RS_CARVEOUT_FUNC=<p> (experiment): the carveout as a FUNCTION attribute of
+// every kernel (p% of the unified L1/shared array; 1 = maximum shared). The
+// product sets it per handle on the graph's kernel nodes instead (accel.cu,
+// rs_accel::carveout_pct, RS_CARVEOUT).
 inline void max_carveout(const void* fn) {
   static std::mutex mu;
   static std::set<std::pair<int, const void*>> done;
   static const int pct = [] {
-    const char* v = getenv("RS_CARVEOUT");
+    const char* v = getenv("RS_CARVEOUT_FUNC");
     const int p = v ? atoi(v) : 0;
     return p == 1 ? (int)cudaSharedmemCarveoutMaxShared : p;
   }();

@@ -785,6 +785,10 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   if (a.batch > 1 && a.N >= 256 && !a.ab16) p->cfg = 4;
   if (const char* e = getenv("RS_TC_CFG")) p->cfg = std::min(4, std::max(0, atoi(e)));
   if (p->cfg == 4 && a.N < 256) p->cfg = 2;
+  // a shared-memory budget (the handle's uniform carveout): the deep 192 KB
+  // pipelines give way to the 96 KB shallow ones
+  if (a.smem_cap_kb > 0 && a.smem_cap_kb < 192 && !getenv("RS_TC_CFG"))
+    p->cfg = (p->cfg == 2 || p->cfg == 4) ? 0 : (p->cfg == 3 ? 1 : p->cfg);
   if (a.single_n_tile && a.N <= 128 && (p->cfg == 1 || p->cfg == 3)) p->cfg -= 1;
   if (a.N < 128 && !a.single_n_tile && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
   p->block_n = p->cfg == 4 ? 256 : (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
