@@ -1582,12 +1582,23 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
     a->depth = init->queue_depth > 0 ? std::min<int>(init->queue_depth, rs_accel::kMaxLanes) : 4;
     {
       // carveout policy (tools/env_sweep.py, profiles/r2_carveout/): models
-      // whose embedding stage bounds the queue (Sum, AttentionFC,
-      // AttentionRNN pooling) get the uniform carveout and the shallow FC
-      // tiles — cfg3 RMC2 -6%, zoo RMC2 -9%, DIN -4%, DIEN -5%, RMC1/RMC3
-      // within 2%; Concat models are FC-bound and keep the deep tiles (MT-WND
+      // whose embedding stage bounds the queue (Sum / AttentionFC pooling with
+      // more gather than FC time, and the AttentionRNN recurrence) get the
+      // uniform carveout and the shallow FC tiles — cfg3 RMC2 -6%, zoo RMC2
+      // -9%, DIN -4%, DIEN -5%; FC-bound models keep the deep tiles (MT-WND
       // +45%, WND +3.5% with the carveout). RS_CARVEOUT=<pct> overrides, 0 = off
-      const bool gather_bound = model->num_tables > 0 && model->pooling != RS_POOL_CONCAT;
+      // "gather-bound": the embedding stage's HBM time at ~6.5 TB/s exceeds the
+      // FC stacks' time at ~300 TF/s (the pipelined tcgen05 rate), per item
+      // from work() — zoo RMC3 (2560-wide bottom MLP, 27 KB gathered per item)
+      // is FC-bound and keeps the deep tiles (73.9K vs 86.9K QPS with them)
+      const rs_work_breakdown wb = work(*model, 1);
+      const double gather_s =
+          (wb.bytes[RS_OP_EMBEDDING_LOOKUP] + wb.bytes[RS_OP_POOLING]) / 6.5e12;
+      const double fc_s = (wb.flops[RS_OP_DENSE_FC] + wb.flops[RS_OP_PREDICT_FC]) / 3.0e14;
+      const bool gather_bound =
+          model->num_tables > 0 &&
+          (model->pooling == RS_POOL_ATTENTION_RNN ||
+           (model->pooling != RS_POOL_CONCAT && gather_s >= fc_s));
       const char* cv = getenv("RS_CARVEOUT");
       a->carveout_pct = cv ? std::max(0, std::min(100, atoi(cv))) : (gather_bound ? 50 : 0);
       a->fc_smem_kb = a->carveout_pct > 0 ? 110 : 0;
