@@ -84,6 +84,12 @@ def workload_spec(rs, name):
                         recurrent_hidden_dim=w.get("hidden")), w["rows"], w["zoo"]
 
 
+def cta_pairs_on(args):
+    """RS_OPT_CTA_PAIRS: measured faster for uniform-size queues only."""
+    c = getattr(args, "cta_pairs", "auto")
+    return c == "on" or (c == "auto" and bool(getattr(args, "size_fixed", 0)))
+
+
 def workload_or_model(name):
     """The same workload as the oracle's C model struct (no product import)."""
     from oracle import cpu_arm
@@ -133,7 +139,7 @@ def make_config(args, name, shape, rows, sizes, world, sla):
                               if args.size_fixed else
                               f"LogNormal(ln {args.size_median:g}, 0.5) clamped to "
                               f"[1, {args.max_query}] (SURVEY 8d (i))"),
-        "fc_path": args.fc, "parallelism": f"replicas{world}",
+        "fc_path": args.fc, "cta_pairs": cta_pairs_on(args), "parallelism": f"replicas{world}",
         "input_format": ("LABELLED variant (SURVEY 8f-2), not the reference byte model: " +
                          " + ".join((["int32 indices"] if i32 else []) +
                                     (["bf16 dense"] if bf16 else []))
@@ -429,6 +435,8 @@ def run_ours(args, rank, world, local):
                          rnn_cell=rs.RNN_AUGRU if args.rnn == "augru" else rs.RNN_GRU)
     if args.merge > 1:
         acc.set_option(rs.OPT_MERGE_QUERIES, args.merge)
+    if cta_pairs_on(args):
+        acc.set_option(rs.OPT_CTA_PAIRS, 1)
     e = spec.embeddings
     # pool of 2Q distinct queries: pinned host copies (e2e) and device copies (value)
     P = 2 * Q
@@ -853,6 +861,9 @@ def main():
                     help="LogNormal(ln m, 0.5) query sizes (SURVEY 8d: 300; 30 = small-query regime)")
     ap.add_argument("--size-fixed", type=int, default=0,
                     help=">0: every query has this many items (BASELINE configs[3] batch sweep)")
+    ap.add_argument("--cta-pairs", choices=["auto", "on", "off"], default="auto",
+                    help="RS_OPT_CTA_PAIRS (256-row CTA-pair FC tiles); auto = on for "
+                         "--size-fixed queues (uniform sizes), off for mixed streams")
     ap.add_argument("--merge", type=int, default=1,
                     help=">1 = labelled query-merging variant (SURVEY 8f-3)")
     ap.add_argument("--dense-bits", type=int, choices=[32, 16], default=32,

@@ -107,6 +107,7 @@ INDEX_I64, INDEX_I32 = 0, 1  # rs_query.index_type (I32: labelled input variant)
 DENSE_BF16 = 2               # rs_query.index_type flag: bf16 dense (labelled variant)
 OPT_MERGE_QUERIES = 1        # rs_accel_set_option (labelled scheduler extension)
 OPT_STAGE_TIMING = 2         # rs_accel_set_option: per-stage event timing of rs_forward
+OPT_CTA_PAIRS = 3            # rs_accel_set_option: CTA-pair FC tiles for uniform-size queues
 
 
 class CLayerStack(C.Structure):

@@ -104,8 +104,15 @@ struct Slot {
   uint16_t* act16[2] = {nullptr, nullptr};
   uint16_t* pact16[2] = {nullptr, nullptr};
   float* out = nullptr;
-  cudaGraphExec_t graph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // GraphKind
-  int kernels[3] = {0, 0, 0};
+  cudaGraphExec_t graph[7] = {};  // GraphKind
+  int kernels[7] = {};
+  // kGraphWide: capturing it (pairs), its CTA-pair layers, whether one of them
+  // is a single stack, and the smallest query it serves
+  bool pairs = false;
+  bool wide_tried = false;
+  int pair_layers = 0;
+  bool pair_single = false;
+  int64_t pair_min = 0;
   int tc_layers = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // event-record nodes around the embedding kernel (pool graph and the
@@ -157,6 +164,11 @@ struct rs_accel {
   int depth = 2;
   int64_t merge_queries = 1;  // RS_OPT_MERGE_QUERIES (1 = one query per launch)
   int stage_timing = 0;       // RS_OPT_STAGE_TIMING
+  // RS_OPT_CTA_PAIRS (RS_TC2=1 sets the default, for tools/env_sweep.py)
+  int cta_pairs = [] {
+    const char* e = getenv("RS_TC2");
+    return e && atoi(e) == 1 ? 1 : 0;
+  }();
   // Uniform shared-memory carveout (% of the unified L1/shared array) set on
   // every kernel node of the forward graphs, with the tcgen05 FC tiles held
   // to a shared-memory budget that fits it: an SM never has to drain to
@@ -470,6 +482,13 @@ bool discard_enabled() {
   return !v || atoi(v) != 0;
 }
 
+// a layer of the wide graph planned on CTA pairs (fc_tc2_kernel)
+void note_pair(Slot* s, const TcPlan& p, const FcArgs& args) {
+  if (p.cfg != 5) return;
+  ++s->pair_layers;
+  if (args.batch == 1) s->pair_single = true;
+}
+
 int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, const float* in0,
                   int64_t ld_in0, int64_t in0_rows, float* const* tmp, int64_t ld_tmp,
                   float* final_out, int64_t ld_final, int64_t final_sCz, bool allow_tc,
@@ -515,6 +534,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
     }
     args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
     args.smem_cap_kb = a->fc_smem_kb;
+    args.pair_ok = s->pairs ? 1 : 0;
     bool used_tc = false;
     if (allow_tc) {
       // A narrow final layer (<= 4 outputs: the DLRM / DIN / DIEN logits)
@@ -544,6 +564,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
           }
         }
         launch_fc_tc(s->d_q, p, args, st);
+        note_pair(s, p, args);
         used_tc = true;
         ++tc_count;
         if (fuse) {
@@ -555,6 +576,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
         args.b2 = nullptr; args.C2 = nullptr;
         if (tc_plan(&p, args, maxS, a_rows, &s->splitk)) {
           launch_fc_tc(s->d_q, p, args, st);
+        note_pair(s, p, args);
           used_tc = true;
           ++tc_count;
         }
@@ -588,6 +610,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
     x.N = (int)f.out; x.K = (int)f.in; x.relu = f.relu; x.batch = f.batch;
     x.ab16 = 1;
     x.smem_cap_kb = a->fc_smem_kb;
+    x.pair_ok = s->pairs ? 1 : 0;
     return x;
   };
   // can layer l run as a bf16 tcgen05 layer reading A (dry-run plan)?
@@ -616,6 +639,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
       args.bias = f.b; args.sbz = f.out;
       args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
       args.smem_cap_kb = a->fc_smem_kb;
+      args.pair_ok = s->pairs ? 1 : 0;
     }
     const bool fuse = l + 2 == layers.size() && layers[l + 1].out <= kFuseMaxN2 &&
                       f.out <= 128 && fuse_enabled();
@@ -653,6 +677,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
     }
     if (ok) {
       launch_fc_tc(s->d_q, p, args, st);
+        note_pair(s, p, args);
       tc_count += fused ? 2 : 1;
     } else {
       if (cur16) raise(RS_E_CUDA, "bf16 FC layer failed to plan after a bf16 producer");
@@ -677,9 +702,11 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
 // forward with tcgen05 FC layers wherever the layer shape fills a tile.
 // kGraphPoolTimed: the pool graph with event-record nodes around the
 // embedding kernel (rs_pooled with timing; the untimed graph stays lean)
+// kGraphWide: the tcgen05 forward with the layers of >= 256 outputs on CTA
+// pairs (fc_tc2_kernel, 256-row tiles), for queries that fill whole pairs.
 enum GraphKind {
   kGraphPool = 0, kGraphSmall = 1, kGraphLarge = 2, kGraphPoolTimed = 3, kGraphStageTimed = 4,
-  kNumGraphs = 5
+  kGraphWide = 5, kGraphWideStageTimed = 6, kNumGraphs = 7
 };
 static_assert(kNumGraphs == sizeof(Slot::graph) / sizeof(Slot::graph[0]), "Slot::graph size");
 
@@ -700,8 +727,8 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
   // kGraphStageTimed: the forward graph of the handle's FC path with
   // event-record nodes around the embedding stage and around the predict
   // stack (RS_OPT_STAGE_TIMING; rs_timing.embed_ms / fc_ms)
-  const bool stage_stamp = kind == kGraphStageTimed;
-  const bool tc = kind == kGraphLarge ||
+  const bool stage_stamp = kind == kGraphStageTimed || kind == kGraphWideStageTimed;
+  const bool tc = kind == kGraphLarge || kind == kGraphWide ||
                   (stage_stamp && a->init.fc_mode != RS_FC_FP32 && tc_available());
   const bool h16 = tc && a->init.fc_mode == RS_FC_BF16;  // bf16 FC stacks
   int ntc = 0;
@@ -735,7 +762,10 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
     // the dense branch forked; partitioned: the gather forked onto the
     // gather partition, the dense branch on the main (dense) stream.
     const bool dense = a->dense_in > 0;
-    const bool fork = part ? a->T > 0 : (dense && a->T > 0);
+    // RS_DIAG_SERIAL=1 (diagnostic): the dense branch ahead of the gather on one stream
+    const char* dser = getenv("RS_DIAG_SERIAL");
+    const bool serial = dser && atoi(dser) && !part;
+    const bool fork = !serial && (part ? a->T > 0 : (dense && a->T > 0));
     cudaStream_t bs = st, es = st;
     if (fork) {
       RS_CUDA(cudaEventRecord(s->fork, st));
@@ -1215,15 +1245,54 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
   write_desc(a, s, v, st);
 }
 
+// The wide graph (RS_OPT_CTA_PAIRS): the layers of >= 256 outputs on 256-row
+// CTA-pair tiles (fc_tc2_kernel: half the weight bytes per flop of the
+// one-CTA tile), captured on first use. Pairs only pay when the query fills
+// them — an odd 128-row tile count leaves half a pair idle (MT-WND 640 items:
+// 29.5 -> 32.7 us/query) — and, for single stacks whose 128-wide tiles would
+// halve in number, only at large queries (WND 400 items -13%, 700 +6%, 1000
+// +20%; batched MT-WND +6% from 400 items). In a queue of MIXED sizes the
+// pair grids cost their neighbours more than they gain (MT-WND / WND
+// log-normal streams -1.5..-3.8%), so the option is for uniform-size queues
+// (the configs[3] batch sweep). tools/env_sweep.py, profiles/r2_tc2/.
+void ensure_wide(rs_accel* a, Slot* s) {
+  if (s->wide_tried) return;
+  s->wide_tried = true;
+  if (!s->graph[kGraphLarge] || a->init.max_query_size < 256) return;
+  s->pairs = true;
+  s->pair_layers = 0;
+  s->pair_single = false;
+  int wide_tc = 0;
+  cudaGraphExec_t w = capture(a, s, kGraphWide, &s->kernels[kGraphWide], &wide_tc);
+  s->pairs = false;
+  if (s->pair_layers == 0) {
+    cudaGraphExecDestroy(w);
+    return;
+  }
+  s->graph[kGraphWide] = w;
+  s->pair_min = s->pair_single ? 640 : 256;
+  if (const char* pm = getenv("RS_TC2_MIN")) s->pair_min = atoll(pm);
+}
+
 cudaGraphExec_t pick_graph(rs_accel* a, Slot* s, int64_t S, bool full, bool timed = false) {
   if (!full) return s->graph[timed ? kGraphPoolTimed : kGraphPool];
-  if (timed && a->stage_timing) {
-    if (!s->graph[kGraphStageTimed])
-      s->graph[kGraphStageTimed] = capture(a, s, kGraphStageTimed, nullptr, nullptr);
-    return s->graph[kGraphStageTimed];
+  bool wide = false;
+  if (a->cta_pairs && S >= 256 && ((S + 127) / 128) % 2 == 0) {
+    ensure_wide(a, s);
+    wide = s->graph[kGraphWide] && S >= s->pair_min;
   }
+  if (timed && a->stage_timing) {
+    // the stage-timed copy of the graph this query would run
+    const int k = wide ? kGraphWideStageTimed : kGraphStageTimed;
+    if (!s->graph[k]) {
+      s->pairs = wide;
+      s->graph[k] = capture(a, s, k, nullptr, nullptr);
+      s->pairs = false;
+    }
+    return s->graph[k];
+  }
+  if (wide) return s->graph[kGraphWide];
   cudaGraphExec_t small = s->graph[kGraphSmall], large = s->graph[kGraphLarge];
-  (void)S;
   return large ? large : small;
 }
 
@@ -1518,6 +1587,10 @@ extern "C" int rs_accel_set_option(rs_accel* a, int32_t option, int64_t value) {
       case RS_OPT_STAGE_TIMING:
         if (value != 0 && value != 1) raise(RS_E_INVALID, "stage_timing must be 0 or 1");
         a->stage_timing = (int)value;
+        break;
+      case RS_OPT_CTA_PAIRS:
+        if (value != 0 && value != 1) raise(RS_E_INVALID, "cta_pairs must be 0 or 1");
+        a->cta_pairs = (int)value;
         break;
       default:
         raise(RS_E_INVALID, "unknown option");

@@ -20,6 +20,7 @@
 // Rows >= S (device query descriptor) are masked at the store; the tile's
 // K tail is zero-filled by TMA.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -446,6 +447,240 @@ fc_tc_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap m
   }
 }
 
+// ---------------------------------------------------------------------------
+// fc_tc2_kernel: the same layer on a CTA PAIR (cluster of 2 along M = grid x) with
+// tcgen05.mma.cta_group::2 — one 256 x BN tile per pair: each CTA stages its
+// own 128 rows of A and HALF of the pair's BN weight rows per k-slab, and the
+// leader's single MMA thread multiplies the 256-row tile against all BN
+// columns, accumulating each CTA's 128 rows in its own TMEM. Per CTA and
+// k-slab: 16 KB of A + BN/2 x 128 B of W for 128 x BN x slab flops — half
+// the W bytes per flop of a one-CTA tile of the same width, which is what the
+// L2 feed bounds for wide layers (§2b). TMA loads of both CTAs complete on
+// the LEADER's full barrier (peer bit cleared); the leader's commits arrive
+// on both CTAs' empty / tmem_full barriers (multicast mask 0b11).
+template <int BN, int STAGES>
+struct Tc2Smem {
+  alignas(1024) float a[STAGES][BM * BK];
+  alignas(1024) float b[STAGES][(BN / 2) * BK];
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tmem_full;
+  uint32_t tmem_base;
+};
+
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of CTA 0
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+               "memory");
+}
+__device__ __forceinline__ void tma2_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                             int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                             int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void commit2_multicast(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+template <int BN>
+__device__ __forceinline__ uint32_t idesc2(bool h) {
+  return (1u << 4) | ((h ? 1u : 2u) << 7) | ((h ? 1u : 2u) << 10) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+template <int BN, int STAGES, bool H>
+__global__ void __launch_bounds__(kTcThreads, 1)
+fc_tc2_kernel(const QDesc* __restrict__ qd, const __grid_constant__ CUtensorMap map_a,
+              const __grid_constant__ CUtensorMap map_w, FcArgs a, int a_batched) {
+  extern __shared__ uint8_t smem_raw[];
+  Tc2Smem<BN, STAGES>& sm = *reinterpret_cast<Tc2Smem<BN, STAGES>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int64_t M = qd->S;
+  const uint32_t rank = cluster_rank();
+  const int z = blockIdx.z;
+  const int n0 = blockIdx.y * BN;
+  const int pair_m0 = (int)(blockIdx.x & ~1u) * BM;
+  const int m0 = pair_m0 + (int)rank * BM;
+  if (pair_m0 >= M) return;  // both CTAs of the pair leave together
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int KE = H ? 2 * BK : BK;
+  const int nk = (a.K + KE - 1) / KE;
+  const int pre = nk < STAGES ? nk : STAGES;
+  constexpr uint32_t kBytesPair = 2u * (BM + BN / 2) * BK * sizeof(float);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    mbar_init(&sm.tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();  // barriers of both CTAs initialised before any TMA or commit
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+  auto leader_full = [&](int s) { return smem_u32(&sm.full[s]) & kPeerBitMask; };
+  const int wrow = n0 + (int)rank * (BN / 2);  // this CTA's half of the weight rows
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < pre; ++kb) {
+      if (rank == 0) mbar_expect_tx(&sm.full[kb], kBytesPair);
+      tma2_load_3d(smem_u32(sm.b[kb]), &map_w, leader_full(kb), kb * KE, wrow, z);
+    }
+  }
+  pdl_wait();  // A is the previous layer's output
+
+  if (warp == 0) {
+    for (int kb = 0; lane == 0 && kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+      if (kb >= pre) {
+        mbar_wait(&sm.empty[s], ph ^ 1u);
+        if (rank == 0) mbar_expect_tx(&sm.full[s], kBytesPair);
+        tma2_load_3d(smem_u32(sm.b[s]), &map_w, leader_full(s), kb * KE, wrow, z);
+      }
+      if (a_batched) tma2_load_3d(smem_u32(sm.a[s]), &map_a, leader_full(s), kb * KE, m0, z);
+      else tma2_load_2d(smem_u32(sm.a[s]), &map_a, leader_full(s), kb * KE, m0);
+    }
+    __syncwarp();
+  } else if (warp == 1 && rank == 0) {
+    const uint32_t idesc = idesc2<BN>(H);
+    for (int kb = 0; lane == 0 && kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+      mbar_wait(&sm.full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sa = smem_u32(sm.a[s]), sb = smem_u32(sm.b[s]);
+#pragma unroll
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint64_t da = sw128_desc(sa + kk * 32);
+        const uint64_t db = sw128_desc(sb + kk * 32);
+        const uint32_t acc = (kb | kk) ? 1u : 0u;
+        if constexpr (H)
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc)
+              : "memory");
+        else
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc)
+              : "memory");
+      }
+      commit2_multicast(&sm.empty[s]);
+    }
+    if (lane == 0) commit2_multicast(&sm.tmem_full);
+    __syncwarp();
+  }
+  {
+    // ---- epilogue (all warps of both CTAs: each its own 128 rows) ----
+    mbar_wait(&sm.tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    pdl_trigger();
+    const int64_t m = m0 + warp * 32 + lane;
+    float* __restrict__ Cb = (a.c_desc && qd->out) ? qd->out : a.C;
+    const float* __restrict__ bias = a.bias + (int64_t)z * a.sbz;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+            "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+            "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+            "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+            "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int nb = n0 + c * 32;
+      if (m < M && nb < a.N) {
+        float y[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int n = nb + i;
+          const float val = __uint_as_float(v[i]) + (n < a.N ? __ldg(bias + n) : 0.f);
+          y[i] = a.relu ? fmaxf(val, 0.f) : val;
+        }
+        if (a.c16) {
+          uint16_t* __restrict__ C16 =
+              reinterpret_cast<uint16_t*>(Cb) + (int64_t)z * a.sCz + m * a.ldc + nb;
+          if (nb + 32 <= a.N && a.ldc % 8 == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(C16)[i] = make_uint4(
+                  pack_bf16(y[8 * i], y[8 * i + 1]), pack_bf16(y[8 * i + 2], y[8 * i + 3]),
+                  pack_bf16(y[8 * i + 4], y[8 * i + 5]), pack_bf16(y[8 * i + 6], y[8 * i + 7]));
+          } else {
+            for (int i = 0; i < 32; ++i)
+              if (nb + i < a.N) C16[i] = (uint16_t)(pack_bf16(y[i], 0.f) & 0xFFFFu);
+          }
+        } else {
+          float* __restrict__ C = Cb + (int64_t)z * a.sCz + m * a.ldc + nb;
+          if (nb + 32 <= a.N && a.ldc % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              reinterpret_cast<float4*>(C)[i] =
+                  make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+          } else {
+            for (int i = 0; i < 32; ++i)
+              if (nb + i < a.N) C[i] = y[i];
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();  // both CTAs finished with the pair's TMEM and shared memory
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN)
+                 : "memory");
+  }
+}
+
+template <int BN, int STAGES>
+size_t tc2_smem_bytes() {
+  return sizeof(Tc2Smem<BN, STAGES>) + 1024;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -487,6 +722,45 @@ template <int BN, int STAGES, bool H = false>
 void set_attr_once() {  // once per device (common.cuh smem_attr)
   smem_attr(reinterpret_cast<const void*>(fc_tc_kernel<BN, STAGES, H>),
             (int)tc_smem_bytes<BN, STAGES>());
+}
+
+template <int BN, int STAGES, bool H>
+void set_attr2_once() {
+  smem_attr(reinterpret_cast<const void*>(fc_tc2_kernel<BN, STAGES, H>),
+            (int)tc2_smem_bytes<BN, STAGES>());
+}
+
+// launch_pdl plus a (2, 1, 1) cluster: blockIdx.x 2j / 2j+1 form a CTA pair
+// (the driver rejects a cta_group::2 kernel whose pair is not along x)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pair(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                        cudaStream_t stream, Args&&... args) {
+  max_carveout(reinterpret_cast<const void*>(kernel));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[3];
+  unsigned n = 0;
+  attr[n].id = cudaLaunchAttributeClusterDimension;
+  attr[n].val.clusterDim.x = 2;
+  attr[n].val.clusterDim.y = 1;
+  attr[n].val.clusterDim.z = 1;
+  ++n;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (prio_enabled()) {
+    attr[n].id = cudaLaunchAttributePriority;
+    attr[n].val.priority = high_priority();
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 #if RS_EXPERIMENTS  // measured slower (DESIGN.md Appendix RS_FC_CHAIN)
@@ -783,16 +1057,25 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   // 1024-item queries 49.8 -> 46.8; neutral for bf16 operands, whose k-slabs
   // already carry twice the flops: tools/env_sweep.py, profiles/r2_fc_tiles/)
   if (a.batch > 1 && a.N >= 256 && !a.ab16) p->cfg = 4;
-  if (const char* e = getenv("RS_TC_CFG")) p->cfg = std::min(4, std::max(0, atoi(e)));
+  // cfg 5 <256,4> on a CTA pair (fc_tc2_kernel, cta_group::2): 256-row x
+  // 256-column tiles, half the W bytes per flop of cfg 4. Planned for layers
+  // of >= 256 outputs in the handle's wide graph (a.pair_ok), which serves the
+  // queries that fill whole pairs; RS_TC2=2 forces it into every tcgen05 graph
+  const char* tc2e = getenv("RS_TC2");  // read per plan (graph capture): tools/env_sweep.py
+  const bool tc2 = a.pair_ok || (tc2e && atoi(tc2e) == 2);
+  if (tc2 && a.N >= 256 && m_cap > BM) p->cfg = 5;
+  if (const char* e = getenv("RS_TC_CFG")) p->cfg = std::min(5, std::max(0, atoi(e)));
+  if (p->cfg == 5 && (a.N < 256 || a.N2 > 0 || a.skip_c)) p->cfg = 4;
   if (p->cfg == 4 && a.N < 256) p->cfg = 2;
   // a shared-memory budget (the handle's uniform carveout): the deep 192 KB
   // pipelines give way to the 96 KB shallow ones
   if (a.smem_cap_kb > 0 && a.smem_cap_kb < 192 && !getenv("RS_TC_CFG"))
-    p->cfg = (p->cfg == 2 || p->cfg == 4) ? 0 : (p->cfg == 3 ? 1 : p->cfg);
+    p->cfg = (p->cfg == 2 || p->cfg == 4 || p->cfg == 5) ? 0 : (p->cfg == 3 ? 1 : p->cfg);
   if (a.single_n_tile && a.N <= 128 && (p->cfg == 1 || p->cfg == 3)) p->cfg -= 1;
   if (a.N < 128 && !a.single_n_tile && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
-  p->block_n = p->cfg == 4 ? 256 : (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
+  p->block_n = p->cfg >= 4 ? 256 : (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
   p->m_tiles = (int)((m_cap + BM - 1) / BM);
+  if (p->cfg == 5) p->m_tiles = (p->m_tiles + 1) & ~1;  // whole CTA pairs
   p->n_tiles = (a.N + p->block_n - 1) / p->block_n;
   // A: [batch][rows][K] (or shared 2D when sAz == 0)
   const CUtensorMapDataType dt =
@@ -812,7 +1095,9 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
     cuuint64_t dims[3] = {(cuuint64_t)a.K, (cuuint64_t)a.N, (cuuint64_t)a.batch};
     cuuint64_t str[2] = {(cuuint64_t)a.ldw * esz,
                          (cuuint64_t)(a.sWz ? a.sWz : (int64_t)a.N * a.ldw) * esz};
-    cuuint32_t box[3] = {(cuuint32_t)ke, (cuuint32_t)p->block_n, 1};
+    // a CTA pair stages half of the tile's weight rows per CTA
+    cuuint32_t box[3] = {(cuuint32_t)ke, (cuuint32_t)(p->cfg == 5 ? p->block_n / 2 : p->block_n),
+                         1};
     if (!encode(&p->map_w, a.W, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return false;
   }
   p->ab16 = a.ab16;
@@ -822,6 +1107,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
       case 1: set_attr_once<64, 4, true>(); break;
       case 2: set_attr_once<128, 6, true>(); break;
       case 4: set_attr_once<256, 4, true>(); break;
+      case 5: set_attr2_once<256, 4, true>(); break;
       default: set_attr_once<64, 8, true>(); break;
     }
   } else {
@@ -830,6 +1116,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
       case 1: set_attr_once<64, 4>(); break;
       case 2: set_attr_once<128, 6>(); break;
       case 4: set_attr_once<256, 4>(); break;
+      case 5: set_attr2_once<256, 4, false>(); break;
       default: set_attr_once<64, 8>(); break;
     }
   }
@@ -845,7 +1132,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
 #if RS_EXPERIMENTS
   const char* sk = getenv("RS_SPLITK");
   const int nk = (a.K + BK - 1) / BK;
-  if (pool && !a.ab16 && a.N2 == 0 && nk >= 32 && sk && atoi(sk) > 1) {
+  if (pool && !a.ab16 && a.N2 == 0 && p->cfg != 5 && nk >= 32 && sk && atoi(sk) > 1) {
     int splits = std::min(std::min(4, atoi(sk)), nk / 16);
     while (splits > 1 && (splits - 1) * ((nk + splits - 1) / splits) >= nk) --splits;
     const size_t tiles = (size_t)a.batch * p->m_tiles * p->n_tiles;
@@ -951,6 +1238,33 @@ void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a0, cudaStream
 #define RS_TC(BN, ST, H)                                                                    \
   launch_pdl(fc_tc_kernel<BN, ST, H>, grid, dim3(kTcThreads), tc_smem_bytes<BN, ST>(), s, qd, \
              p.map_a, p.map_w, a, a_batched)
+  if (p.cfg == 5) {
+    const dim3 grid2(p.m_tiles, p.n_tiles, a.batch);  // pairs along x
+    cudaError_t e;
+    if (p.ab16)
+      e = launch_pair(fc_tc2_kernel<256, 4, true>, grid2, dim3(kTcThreads),
+                      tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
+    else
+      e = launch_pair(fc_tc2_kernel<256, 4, false>, grid2, dim3(kTcThreads),
+                      tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
+    if (getenv("RS_TC_DEBUG")) {
+      cudaLaunchConfig_t c = {};
+      c.gridDim = grid2;
+      c.blockDim = dim3(kTcThreads);
+      c.dynamicSmemBytes = tc2_smem_bytes<256, 4>();
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 2; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+      c.attrs = &at;
+      c.numAttrs = 1;
+      int nc = -1;
+      cudaError_t oe = cudaOccupancyMaxActiveClusters(
+          &nc, reinterpret_cast<const void*>(fc_tc2_kernel<256, 4, false>), &c);
+      fprintf(stderr, "tc2 launch: %s; max active clusters %d (%s)\n", cudaGetErrorString(e), nc,
+              cudaGetErrorString(oe));
+    }
+    return;
+  }
   if (p.ab16) {
     switch (p.cfg) {
       case 0: RS_TC(128, 3, true); break;

@@ -81,6 +81,7 @@ struct FcArgs {
   // drops too (row stride dz_ld bytes) — e.g. the stack input two layers back.
   int discard_a; const void* dz; int64_t dz_ld;
   int smem_cap_kb;  // planning: tcgen05 tile shared-memory budget (0 = none)
+  int pair_ok;      // planning: CTA-pair tiles (fc_tc2_kernel) allowed for N >= 256
 };
 constexpr int kFuseMaxN2 = 4;
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);

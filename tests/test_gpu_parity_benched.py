@@ -163,3 +163,30 @@ def test_bf16_fc_variant(name):
         if spec.embeddings.pooling == "Sum":
             assert np.array_equal(acc.pooled(idx), orc.sls_canonical(idx))
     acc.close()
+
+
+@pytest.mark.parametrize("fc_mode", [rs.FC_AUTO, rs.FC_BF16], ids=["auto-tf32", "bf16"])
+@pytest.mark.parametrize("name", ["MT-WND", "WND"])
+def test_cta_pair_wide_graph(name, fc_mode):
+    """RS_OPT_CTA_PAIRS: the wide graph (fc_tc2_kernel, tcgen05.mma.cta_group::2
+    on 256-row CTA pairs) serves the queries whose 128-row tile count is even
+    and at least the handle's threshold (256 items for batched stacks, 640
+    with a single stack); odd tile counts stay on the one-CTA graph. Both
+    handles (option on / default off) against the oracle at sizes on each
+    side of the rule."""
+    from parity_rule import BF16
+    spec = rs.builtin_model(name)
+    rows = 1_000_000
+    path = BF16 if fc_mode == rs.FC_BF16 else TF32
+    acc = rs.Accelerator(spec, rows, seed=4, max_query_size=1000, fc_mode=fc_mode)
+    acc.set_option(rs.OPT_CTA_PAIRS, 1)
+    base = rs.Accelerator(spec, rows, seed=4, max_query_size=1000, fc_mode=fc_mode)
+    orc = Oracle(spec, rows, seed=4)
+    for k, S in enumerate((255, 256, 300, 384, 640, 700, 1000)):
+        dense, idx = rs.fill_query(spec, rows, 55, k, S)
+        out = acc.forward(dense, idx)
+        ref, mag, _, _ = orc.forward64(dense, idx)
+        assert_close(out, ref, mag, path, f"{name} S={S} wide-graph handle")
+        assert_close(base.forward(dense, idx), ref, mag, path, f"{name} S={S} one-CTA handle")
+    acc.close()
+    base.close()
