@@ -67,6 +67,8 @@ def test_tcgen05_and_tma_in_sass(rs):
     assert "UTCHMMA" in sass        # tcgen05.mma
     assert "UTMALDG" in sass        # TMA tensor loads
     assert "LDTM" in sass           # tcgen05.ld TMEM -> registers
+    assert "UTCHMMA.2CTA" in sass   # tcgen05.mma.cta_group::2 (fc_tc2_kernel, CTA pairs)
+    assert "UTMALDG.3D.2CTA" in sass  # TMA completing on the pair leader's barrier
 
 
 def test_zipf_fill_query(rs):
