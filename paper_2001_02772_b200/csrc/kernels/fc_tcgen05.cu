@@ -20,7 +20,6 @@
 // Rows >= S (device query descriptor) are masked at the store; the tile's
 // K tail is zero-filled by TMA.
 #include <algorithm>
-#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -1240,29 +1239,12 @@ void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a0, cudaStream
              p.map_a, p.map_w, a, a_batched)
   if (p.cfg == 5) {
     const dim3 grid2(p.m_tiles, p.n_tiles, a.batch);  // pairs along x
-    cudaError_t e;
     if (p.ab16)
-      e = launch_pair(fc_tc2_kernel<256, 4, true>, grid2, dim3(kTcThreads),
-                      tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
+      launch_pair(fc_tc2_kernel<256, 4, true>, grid2, dim3(kTcThreads),
+                  tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
     else
-      e = launch_pair(fc_tc2_kernel<256, 4, false>, grid2, dim3(kTcThreads),
-                      tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
-    if (getenv("RS_TC_DEBUG")) {
-      cudaLaunchConfig_t c = {};
-      c.gridDim = grid2;
-      c.blockDim = dim3(kTcThreads);
-      c.dynamicSmemBytes = tc2_smem_bytes<256, 4>();
-      cudaLaunchAttribute at;
-      at.id = cudaLaunchAttributeClusterDimension;
-      at.val.clusterDim.x = 2; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
-      c.attrs = &at;
-      c.numAttrs = 1;
-      int nc = -1;
-      cudaError_t oe = cudaOccupancyMaxActiveClusters(
-          &nc, reinterpret_cast<const void*>(fc_tc2_kernel<256, 4, false>), &c);
-      fprintf(stderr, "tc2 launch: %s; max active clusters %d (%s)\n", cudaGetErrorString(e), nc,
-              cudaGetErrorString(oe));
-    }
+      launch_pair(fc_tc2_kernel<256, 4, false>, grid2, dim3(kTcThreads),
+                  tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
     return;
   }
   if (p.ab16) {
