@@ -177,6 +177,7 @@ struct rs_accel {
   // 0 = the driver's per-kernel choice and the deep FC tiles.
   int carveout_pct = 0;
   int fc_smem_kb = 0;         // FC tile shared-memory budget (0 = none)
+  int inter_threads = 256;    // interaction CTA size (64: co-resident with the gathers)
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t lane_join[kMaxLanes] = {};
@@ -808,7 +809,7 @@ cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_la
     if (m.pooling == RS_POOL_SUM && a->T > 0 && !(skip & 2))
       launch_interaction(s->d_q, s->pooled, a->T * a->D, (int)a->T, (int)a->D, s->X, a->ld_x,
                          a->dense_out, a->dense_out + a->D, m.has_dense_fc ? 1 : 0, maxS,
-                         s->dense_sms, st, tc);
+                         s->dense_sms, st, tc, a->inter_threads);
     if (const char* de = getenv("RS_DIAG_EMPTY")) {
       const char* dc = getenv("RS_DIAG_EMPTY_CTAS");
       launch_diag_empty(atoi(de), dc ? atoi(dc) : 1, st);
@@ -1675,6 +1676,9 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
       const char* cv = getenv("RS_CARVEOUT");
       a->carveout_pct = cv ? std::max(0, std::min(100, atoi(cv))) : (gather_bound ? 50 : 0);
       a->fc_smem_kb = a->carveout_pct > 0 ? 110 : 0;
+      // the interaction on 2-warp CTAs that fit beside the gathers when the
+      // gather time is >= 4x the FC time (cfg3 / zoo RMC2; not cfg3 RMC3)
+      a->inter_threads = gather_bound && gather_s >= 4.0 * fc_s ? 64 : 256;
     }
     a->device = device;
     a->sm_count = prop.multiProcessorCount;

@@ -802,10 +802,16 @@ din_pool_kernel(const QDesc* __restrict__ qd, const float* __restrict__ tables, 
 // with v_0 = X[item, 0:D] (bottom-MLP output already written there) and
 // v_t = pooled[item, t-1, :]. Pairs exist only when has_dense (the
 // reference counts them only for Sum pooling with a dense stack).
-constexpr int kInterThreads = 256;
 constexpr int kInterRegs = 8;  // float4 loads in flight per thread per round
 
-__global__ void __launch_bounds__(kInterThreads)
+// kInterThreads = 256, or 64 for strongly gather-bound models (the handle's
+// choice; RS_INTER_THREADS overrides): a 2-warp CTA capped at 64 registers
+// per thread fits in the 4K registers three gather CTAs leave free on an SM,
+// so the interaction co-runs with the gathers instead of taking SM slots they
+// would refill (cfg3 RMC2 35.4 -> 34.1 us/query, zoo RMC2 -3.9%; cfg3 RMC3,
+// whose FC work is 60% of its gather time, +4..9%: profiles/r2_inter64.txt).
+template <int kInterThreads>
+__global__ void __launch_bounds__(kInterThreads, 65536 / (kInterThreads * 64))
 interaction_kernel(const QDesc* __restrict__ qd, const float* __restrict__ pooled,
                    int64_t ld_pooled, int T, int D, float* __restrict__ X, int64_t ld_x,
                    int64_t sum_off, int64_t dot_off, int has_dense, int discard) {
@@ -1385,7 +1391,8 @@ bool interaction_tc_supported(int T, int D) {
 
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
-                        int64_t max_items, int sm_count, cudaStream_t s, bool tc) {
+                        int64_t max_items, int sm_count, cudaStream_t s, bool tc,
+                        int threads) {
 #if RS_EXPERIMENTS
   // tcgen05 graph, RS_INTER_TC=1: the tensor-core Gram interaction (tf32 like
   // the FC layers). Measured 1 us/query SLOWER in the pipelined queue than the
@@ -1433,16 +1440,17 @@ void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled,
     return;
   }
   const size_t smem = (size_t)(T + 1) * (D + 1) * sizeof(float);
-  const int grid = grid_for(max_items, 1, sm_count, 2);
+  const bool small = env_int("RS_INTER_THREADS", threads) == 64;
+  const int grid = grid_for(max_items, 1, sm_count, env_int("RS_INTER_PER_SM", 2));
+  auto kern = small ? interaction_kernel<64> : interaction_kernel<256>;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(interaction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // RS_DISCARD (default 1): discard the pooled rows from L2 once staged (the
   // forward graph's pooled buffer is internal; needs 128-byte row alignment)
   const int discard = env_int("RS_DISCARD", 1) && (T * D * 4) % 128 == 0 &&
                       (reinterpret_cast<uintptr_t>(pooled) & 127) == 0 &&
                       (ld_pooled * 4) % 128 == 0;
-  launch_pdl(interaction_kernel, dim3(grid), dim3(kInterThreads), smem, s, qd, pooled, ld_pooled,
+  launch_pdl(kern, dim3(grid), dim3(small ? 64 : 256), smem, s, qd, pooled, ld_pooled,
              T, D, X, ld_x, sum_off, dot_off, has_dense, discard);
 }
 

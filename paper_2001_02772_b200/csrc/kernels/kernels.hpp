@@ -45,9 +45,12 @@ void launch_stage_dense(const QDesc* qd, int64_t dense_in, float* dst, int64_t l
 // r < QDesc::S, c < cols
 void launch_to_bf16(const QDesc* qd, const float* src, int64_t lds, void* dst, int64_t ldd,
                     int64_t cols, int64_t max_items, int sm_count, cudaStream_t s);
+// threads: 256 (default) or 64 — 2-warp CTAs that fit beside three gather
+// CTAs on an SM (the handle picks 64 for strongly gather-bound models)
 void launch_interaction(const QDesc* qd, const float* pooled, int64_t ld_pooled, int T, int D,
                         float* X, int64_t ld_x, int64_t sum_off, int64_t dot_off, int has_dense,
-                        int64_t max_items, int sm_count, cudaStream_t s, bool tc = false);
+                        int64_t max_items, int sm_count, cudaStream_t s, bool tc = false,
+                        int threads = 256);
 size_t interaction_smem(int T, int D);
 void launch_init_tables(float* tables, int64_t T, int64_t rows, int64_t D, uint64_t seed,
                         int sm_count, cudaStream_t s);
