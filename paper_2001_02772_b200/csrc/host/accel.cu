@@ -119,6 +119,7 @@ struct Slot {
   // stage-timed forward graph) and around the predict stack (stage-timed)
   cudaEvent_t kev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ready = nullptr, free = nullptr;  // pipelined queue hand-off
+  cudaEvent_t computed = nullptr;               // forward done (result copy may start)
   cudaStream_t cap2 = nullptr;                  // capture: parallel graph branch
   // SM-partitioned slots (rs_forward_many lanes when the device is split):
   // capture streams on the dense and the gather green contexts
@@ -183,6 +184,9 @@ struct rs_accel {
   cudaEvent_t lane_join[kMaxLanes] = {};
   cudaStream_t copy = nullptr;
   cudaStream_t copy_more[3] = {};  // further copy streams: queries rotate (RS_COPY_STREAMS)
+  // device->host result copies of host queries, off the lanes (RS_D2H_STREAMS)
+  cudaStream_t d2h[2] = {};
+  cudaEvent_t d2h_join[2] = {};
   cudaEvent_t copy_gate = nullptr;
   std::mutex many_mu;
   std::vector<cudaEvent_t> evpool, evstart;
@@ -1017,6 +1021,7 @@ std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   for (auto& e : s->kev) RS_CUDA(cudaEventCreate(&e));
   RS_CUDA(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&s->free, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&s->computed, cudaEventDisableTiming));
   RS_CUDA(cudaStreamCreateWithFlags(&s->cap2, cudaStreamNonBlocking));
   RS_CUDA(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
@@ -1051,6 +1056,11 @@ Slot* get_pipe_slot(rs_accel* a, int i) {
   if (!a->copy) RS_CUDA(cudaStreamCreateWithFlags(&a->copy, cudaStreamNonBlocking));
   for (auto& c : a->copy_more)
     if (!c) RS_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k)
+    if (!a->d2h[k]) {
+      RS_CUDA(cudaStreamCreateWithFlags(&a->d2h[k], cudaStreamNonBlocking));
+      RS_CUDA(cudaEventCreateWithFlags(&a->d2h_join[k], cudaEventDisableTiming));
+    }
   if (!a->lane[i]) {
     RS_CUDA(cudaStreamCreateWithFlags(&a->lane[i], cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&a->lane_join[i], cudaEventDisableTiming));
@@ -1064,6 +1074,7 @@ void free_slot(Slot* s) {
   for (auto e : s->kev) if (e) cudaEventDestroy(e);
   if (s->ready) cudaEventDestroy(s->ready);
   if (s->free) cudaEventDestroy(s->free);
+  if (s->computed) cudaEventDestroy(s->computed);
   for (void* p : s->allocs) cudaFree(p);
   if (s->h_err) cudaFreeHost(s->h_err);
   if (s->h_q) cudaFreeHost(s->h_q);
@@ -1115,6 +1126,17 @@ void write_desc(rs_accel* a, Slot* s, const QDesc& v, cudaStream_t st) {
     }
     if (a->memops(reinterpret_cast<CUstream>(st), 5, ops, 0) != CUDA_SUCCESS)
       raise(RS_E_CUDA, "cuStreamBatchMemOp failed");
+    return;
+  }
+  // RS_DESC_KERNEL=1: a one-warp kernel writes the descriptor from its launch
+  // parameters, so no 40-byte copy sits on the copy engine between two
+  // queries' input transfers
+  static const bool by_kernel = [] {
+    const char* e = getenv("RS_DESC_KERNEL");
+    return e && atoi(e) != 0;
+  }();
+  if (by_kernel) {
+    launch_set_desc(s->d_q, v, st);
     return;
   }
   // Pinned ring: an entry is rewritten only after the copy that last read it
@@ -1479,6 +1501,13 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
     // gather's pipelined throughput from the FC tail's
     const char* po = getenv("RS_MANY_POOL_ONLY");
     const bool pool_only = po && atoi(po);
+    // host results: copied back on separate streams (alternating), so a
+    // lane's next query does not queue its kernels behind the copy and the
+    // link carries both directions at once (RS_D2H_STREAMS=0: on the lane)
+    const char* dse = getenv("RS_D2H_STREAMS");
+    const int nd2h = loc == RS_MEM_HOST ? (dse ? std::min(2, std::max(0, atoi(dse))) : 2) : 0;
+    if (nd2h)
+      for (int c = 0; c < nd2h; ++c) RS_CUDA(cudaStreamWaitEvent(a->d2h[c], a->copy_gate, 0));
     const auto host_t0 = std::chrono::steady_clock::now();
     const int64_t maxS = a->init.max_query_size;
     int64_t group = 0;
@@ -1496,6 +1525,7 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
       for (int64_t k = i; k < j; ++k)
         if (service_ms && k >= kEvRing) harvest(k - kEvRing);
       cudaStream_t sst = ls;  // staging stream
+      cudaStream_t ost = ls;  // stream the query's result lands on
       if (loc == RS_MEM_HOST) {
         sst = copies[group % ncopy];
         RS_CUDA(cudaStreamWaitEvent(sst, s->free, 0));
@@ -1511,7 +1541,18 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
         } else {
           stage_inputs(a, s, &qs[i], true, ls, outs[i]);
         }
-        launch_stage(a, s, &qs[i], outs[i], !pool_only, ls);
+        if (nd2h) {
+          const bool full = !pool_only;
+          RS_CUDA(cudaGraphLaunch(pick_graph(a, s, qs[i].size, full), ls));
+          RS_CUDA(cudaEventRecord(s->computed, ls));
+          ost = a->d2h[group % nd2h];
+          RS_CUDA(cudaStreamWaitEvent(ost, s->computed, 0));
+          RS_CUDA(cudaMemcpyAsync(outs[i], full ? s->out : s->pooled,
+                                  (size_t)(qs[i].size * (full ? a->out_w : a->pooled_dim) * 4),
+                                  cudaMemcpyDeviceToHost, ost));
+        } else {
+          launch_stage(a, s, &qs[i], outs[i], !pool_only, ls);
+        }
       } else {
         const int64_t S = stage_group(a, s, qs + i, j - i, sst);
         if (loc == RS_MEM_HOST) {
@@ -1531,15 +1572,19 @@ int run_many(rs_accel* a, int64_t n, const rs_query* qs, float* const* outs, voi
           off += qs[k].size;
         }
       }
-      RS_CUDA(cudaEventRecord(s->free, ls));
+      RS_CUDA(cudaEventRecord(s->free, ost));
       if (service_ms)
-        for (int64_t k = i; k < j; ++k) RS_CUDA(cudaEventRecord(a->evpool[1 + k % kEvRing], ls));
+        for (int64_t k = i; k < j; ++k) RS_CUDA(cudaEventRecord(a->evpool[1 + k % kEvRing], ost));
       ++group;
       i = j;
     }
     for (int d = 0; d < depth; ++d) {
       RS_CUDA(cudaEventRecord(a->lane_join[d], a->lane[d]));
       RS_CUDA(cudaStreamWaitEvent(st, a->lane_join[d], 0));
+    }
+    for (int c = 0; c < nd2h; ++c) {
+      RS_CUDA(cudaEventRecord(a->d2h_join[c], a->d2h[c]));
+      RS_CUDA(cudaStreamWaitEvent(st, a->d2h_join[c], 0));
     }
     // the caller's completion stamp: recorded once every query finished, so
     // it excludes the host's timestamp harvest below
@@ -1715,6 +1760,10 @@ extern "C" int rs_accel_destroy(rs_accel* a) {
     if (a->copy) cudaStreamDestroy(a->copy);
     for (auto c : a->copy_more)
       if (c) cudaStreamDestroy(c);
+    for (int k = 0; k < 2; ++k) {
+      if (a->d2h[k]) cudaStreamDestroy(a->d2h[k]);
+      if (a->d2h_join[k]) cudaEventDestroy(a->d2h_join[k]);
+    }
     for (int d = 0; d < rs_accel::kMaxLanes; ++d) {
       if (a->lane[d]) cudaStreamDestroy(a->lane[d]);
       if (a->lane_join[d]) cudaEventDestroy(a->lane_join[d]);
