@@ -1128,17 +1128,6 @@ void write_desc(rs_accel* a, Slot* s, const QDesc& v, cudaStream_t st) {
       raise(RS_E_CUDA, "cuStreamBatchMemOp failed");
     return;
   }
-  // RS_DESC_KERNEL=1: a one-warp kernel writes the descriptor from its launch
-  // parameters, so no 40-byte copy sits on the copy engine between two
-  // queries' input transfers
-  static const bool by_kernel = [] {
-    const char* e = getenv("RS_DESC_KERNEL");
-    return e && atoi(e) != 0;
-  }();
-  if (by_kernel) {
-    launch_set_desc(s->d_q, v, st);
-    return;
-  }
   // Pinned ring: an entry is rewritten only after the copy that last read it
   // has executed (its event), so the host may run any distance ahead.
   const int r = s->ring;

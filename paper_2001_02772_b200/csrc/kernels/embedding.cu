@@ -1551,17 +1551,6 @@ void launch_widen_idx(const int32_t* src, int64_t* dst, int64_t n, int sm_count,
   widen_idx_kernel<<<grid, 256, 0, s>>>(src, dst, n);
 }
 
-__global__ void __launch_bounds__(32) set_desc_kernel(QDesc* __restrict__ dst, const QDesc v) {
-  constexpr int kWords = (int)(sizeof(QDesc) / 8);
-  static_assert(sizeof(QDesc) % 8 == 0, "descriptor words");
-  if (threadIdx.x < kWords)
-    reinterpret_cast<uint64_t*>(dst)[threadIdx.x] = reinterpret_cast<const uint64_t*>(&v)[threadIdx.x];
-}
-
-void launch_set_desc(QDesc* dst, const QDesc& v, cudaStream_t s) {
-  set_desc_kernel<<<1, 32, 0, s>>>(dst, v);
-}
-
 __global__ void __launch_bounds__(256)
 group_gather_kernel(const __grid_constant__ GroupGather g, int64_t dense_in, int64_t TL,
                     float* __restrict__ dense_dst, int64_t* __restrict__ idx_dst) {

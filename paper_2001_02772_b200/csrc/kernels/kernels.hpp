@@ -25,9 +25,6 @@ void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, 
                      int64_t max_items, int sm_count, cudaStream_t s);
 void launch_diag_empty(int n, int ctas, cudaStream_t s);
 void launch_widen_idx(const int32_t* src, int64_t* dst, int64_t n, int sm_count, cudaStream_t s);
-// The query descriptor written by a one-warp kernel from its launch
-// parameters (no copy-engine transfer between the queries' input copies).
-void launch_set_desc(QDesc* dst, const QDesc& v, cudaStream_t s);
 // Device-resident inputs of m merged queries gathered back to back in one
 // launch (RS_OPT_MERGE_QUERIES): per query k, dense rows -> dense_dst + off_k
 // * dense_in and indices -> idx_dst + off_k * TL (int32 sources widened).
