@@ -1106,7 +1106,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
       case 1: set_attr_once<64, 4, true>(); break;
       case 2: set_attr_once<128, 6, true>(); break;
       case 4: set_attr_once<256, 4, true>(); break;
-      case 5: set_attr2_once<256, 4, true>(); break;
+      case 5: set_attr2_once<256, 4, true>(); set_attr2_once<256, 6, true>(); break;
       default: set_attr_once<64, 8, true>(); break;
     }
   } else {
@@ -1115,7 +1115,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
       case 1: set_attr_once<64, 4>(); break;
       case 2: set_attr_once<128, 6>(); break;
       case 4: set_attr_once<256, 4>(); break;
-      case 5: set_attr2_once<256, 4, false>(); break;
+      case 5: set_attr2_once<256, 4, false>(); set_attr2_once<256, 6, false>(); break;
       default: set_attr_once<64, 8>(); break;
     }
   }
@@ -1239,12 +1239,19 @@ void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a0, cudaStream
              p.map_a, p.map_w, a, a_batched)
   if (p.cfg == 5) {
     const dim3 grid2(p.m_tiles, p.n_tiles, a.batch);  // pairs along x
-    if (p.ab16)
-      launch_pair(fc_tc2_kernel<256, 4, true>, grid2, dim3(kTcThreads),
-                  tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
-    else
-      launch_pair(fc_tc2_kernel<256, 4, false>, grid2, dim3(kTcThreads),
-                  tc2_smem_bytes<256, 4>(), s, qd, p.map_a, p.map_w, a, a_batched);
+    // a CTA of the pair stages 32 KB per k-slab (16 KB of A + half of the
+    // 256 weight rows), so the ring can run 6 deep in 192 KB (RS_TC2_STAGES)
+    const char* st = getenv("RS_TC2_STAGES");
+    const bool deep = !(st && atoi(st) == 4);
+#define RS_TC2L(ST, H)                                                                   \
+  launch_pair(fc_tc2_kernel<256, ST, H>, grid2, dim3(kTcThreads), tc2_smem_bytes<256, ST>(), \
+              s, qd, p.map_a, p.map_w, a, a_batched)
+    if (p.ab16) {
+      if (deep) RS_TC2L(6, true); else RS_TC2L(4, true);
+    } else {
+      if (deep) RS_TC2L(6, false); else RS_TC2L(4, false);
+    }
+#undef RS_TC2L
     return;
   }
   if (p.ab16) {

@@ -31,6 +31,8 @@ METRICS = ["gpu__time_duration.sum", "launch__grid_size",
 
 CASES = [("mt-wnd", 16), ("mt-wnd", 64), ("mt-wnd", 256), ("mt-wnd", 1024),
          ("cfg3-rmc2", 330), ("cfg5-dien", 300)]
+if os.environ.get("TP_CASES"):  # e.g. "mt-wnd:1024,wnd:1024"
+    CASES = [(c.split(":")[0], int(c.split(":")[1])) for c in os.environ["TP_CASES"].split(",")]
 
 
 def layer_flops(workload, S):
@@ -58,10 +60,11 @@ def layer_flops(workload, S):
 
 
 FC = os.environ.get("TP_FC", "auto")  # auto (tf32) | bf16
+TAG = os.environ.get("TP_TAG", "")
 
 
 def run_case(workload, S):
-    rep = os.path.join(ROOT, "gpurun_out", f"tp_{FC}_{workload}_{S}.csv")
+    rep = os.path.join(ROOT, "gpurun_out", f"tp_{FC}{TAG}_{workload}_{S}.csv")
     cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "--csv",
            "-k", "regex:fc_tc|gru_tc", "--log-file", rep,
            sys.executable, os.path.join(ROOT, "tools", "run_once.py"), "--workload", workload,
@@ -117,6 +120,10 @@ def main():
             if "fc_tc_kernel<" in name and inst:
                 bn = int(name.split("fc_tc_kernel<")[1].split(",")[0])
                 rec["executed_mma_flops"] = inst * 2 * 128 * bn * (16 if FC == "bf16" else 8)
+                rec["executed_over_algorithmic"] = rec["executed_mma_flops"] / fl if fl else None
+            elif "fc_tc2_kernel<" in name and inst:
+                # cta_group::2: one instruction (leader SM) = M 256 x N 256 x K 8
+                rec["executed_mma_flops"] = inst * 2 * 256 * 256 * (16 if FC == "bf16" else 8)
                 rec["executed_over_algorithmic"] = rec["executed_mma_flops"] / fl if fl else None
             res.append(rec)
         tot_f = sum(r["flops"] or 0 for r in res)
