@@ -315,8 +315,8 @@ int rs_serve(rs_accel* const* replicas, int32_t k, int64_t n, const rs_query* qu
  *   (and >= 256 items; >= 640 when a single FC stack has a layer of >= 256
  *   outputs) run a forward graph whose layers of >= 256 outputs use 256-row
  *   tiles on CTA pairs (tcgen05.mma.cta_group::2), captured on first use.
- *   For queues of uniform query size: faster there (MT-WND 1000 items -6%,
- *   WND -20% per query), slower in a mixed-size stream.    */
+ *   For queues of uniform query size: faster there (MT-WND 1000 items -10%,
+ *   WND -22% per query), slower in a mixed-size stream.   */
 enum { RS_OPT_MERGE_QUERIES = 1, RS_OPT_STAGE_TIMING = 2, RS_OPT_CTA_PAIRS = 3 };
 int rs_accel_set_option(rs_accel* a, int32_t option, int64_t value);
 
