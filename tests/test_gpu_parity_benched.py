@@ -190,3 +190,22 @@ def test_cta_pair_wide_graph(name, fc_mode):
         assert_close(base.forward(dense, idx), ref, mag, path, f"{name} S={S} one-CTA handle")
     acc.close()
     base.close()
+
+
+def test_coresident_interaction_is_bit_identical(monkeypatch):
+    """The 2-warp interaction CTAs the handle picks for strongly gather-bound
+    models (cfg3 RMC2) compute every output in the 256-thread kernel's order:
+    logits bit for bit against a handle forced to 256 threads
+    (RS_INTER_THREADS)."""
+    spec = cfg3("RMC2")
+    rows = 100_000
+    acc = rs.Accelerator(spec, rows, seed=8, max_query_size=1000, fc_mode=rs.FC_AUTO)
+    monkeypatch.setenv("RS_INTER_THREADS", "256")
+    ref = rs.Accelerator(spec, rows, seed=8, max_query_size=1000, fc_mode=rs.FC_AUTO)
+    monkeypatch.delenv("RS_INTER_THREADS")
+    qs = [rs.fill_query(spec, rows, 12, k, S) for k, S in enumerate((1, 129, 330, 1000))]
+    for dense, idx in qs:
+        a, b = acc.forward(dense, idx), ref.forward(dense, idx)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    acc.close()
+    ref.close()
