@@ -1270,6 +1270,8 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
 void ensure_wide(rs_accel* a, Slot* s) {
   if (s->wide_tried) return;
   s->wide_tried = true;
+  const char* off = getenv("RS_TC2");  // RS_TC2=0: never (A/B runs)
+  if (off && atoi(off) == 0) return;
   if (!s->graph[kGraphLarge] || a->init.max_query_size < 256) return;
   s->pairs = true;
   s->pair_layers = 0;
