@@ -91,3 +91,13 @@ def test_zipf_fill_query(rs):
     d, i = np.empty((2, spec.dense_input_dim), np.float32), np.empty(2 * 8 * 80, np.int64)
     assert rs._lib.rs_fill_query_zipf(C.byref(spec.to_c()), rows, 3, 7, 2, 0.0,
                                       d.ctypes.data, i.ctypes.data) == rs.InvalidArgument.code
+
+
+def test_option_enums_match_the_header(rs):
+    """rs_accel_set_option's option codes: the binding's constants are the
+    header's enum values (RS_OPT_CTA_PAIRS included)."""
+    src = open(HEADER).read()
+    m = re.search(r"enum\s*\{\s*(RS_OPT_[^}]*)\}", src)
+    vals = dict((k.strip(), int(v)) for k, v in re.findall(r"(RS_OPT_[A-Z_]+)\s*=\s*(\d+)", m.group(1)))
+    assert vals == {"RS_OPT_MERGE_QUERIES": 1, "RS_OPT_STAGE_TIMING": 2, "RS_OPT_CTA_PAIRS": 3}
+    assert (rs.OPT_MERGE_QUERIES, rs.OPT_STAGE_TIMING, rs.OPT_CTA_PAIRS) == (1, 2, 3)
