@@ -90,3 +90,17 @@ def test_reference_arm_config_equals_ours(workload):
                                np.minimum(sizes2, 1000), 1,
                                bench.sla_for(args, zoo2, cpu_arm.sla_target))
     assert ours == theirs
+
+
+def test_cta_pairs_only_for_uniform_queues():
+    """RS_OPT_CTA_PAIRS is measured faster for uniform-size queues and slower
+    in mixed streams: bench turns it on for --size-fixed only
+    unless told otherwise, and the config records the choice."""
+    import argparse
+    ns = lambda **k: argparse.Namespace(**{"cta_pairs": "auto", "size_fixed": 0, **k})
+    assert bench.cta_pairs_on(ns()) is False
+    assert bench.cta_pairs_on(ns(size_fixed=1024)) is True
+    assert bench.cta_pairs_on(ns(size_fixed=1024, cta_pairs="off")) is False
+    assert bench.cta_pairs_on(ns(cta_pairs="on")) is True
+    # namespaces without the flag (e.g. the reference arm's) read as auto
+    assert bench.cta_pairs_on(argparse.Namespace(size_fixed=0)) is False
