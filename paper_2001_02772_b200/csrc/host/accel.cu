@@ -179,6 +179,7 @@ struct rs_accel {
   int carveout_pct = 0;
   int fc_smem_kb = 0;         // FC tile shared-memory budget (0 = none)
   int inter_threads = 256;    // interaction CTA size (64: co-resident with the gathers)
+  int pair_capped = 0;        // CTA-pair FC tiles within the capped shared memory
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t lane_join[kMaxLanes] = {};
@@ -540,6 +541,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
     args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
     args.smem_cap_kb = a->fc_smem_kb;
     args.pair_ok = s->pairs ? 1 : 0;
+    args.pair_capped = a->pair_capped;
     bool used_tc = false;
     if (allow_tc) {
       // A narrow final layer (<= 4 outputs: the DLRM / DIN / DIEN logits)
@@ -616,6 +618,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
     x.ab16 = 1;
     x.smem_cap_kb = a->fc_smem_kb;
     x.pair_ok = s->pairs ? 1 : 0;
+    x.pair_capped = a->pair_capped;
     return x;
   };
   // can layer l run as a bf16 tcgen05 layer reading A (dry-run plan)?
@@ -645,6 +648,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
       args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
       args.smem_cap_kb = a->fc_smem_kb;
       args.pair_ok = s->pairs ? 1 : 0;
+      args.pair_capped = a->pair_capped;
     }
     const bool fuse = l + 2 == layers.size() && layers[l + 1].out <= kFuseMaxN2 &&
                       f.out <= 128 && fuse_enabled();
@@ -1715,6 +1719,10 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
       // the interaction on 2-warp CTAs that fit beside the gathers when the
       // gather time is >= 4x the FC time (cfg3 / zoo RMC2; not cfg3 RMC3)
       a->inter_threads = gather_bound && gather_s >= 4.0 * fc_s ? 64 : 256;
+      // CTA-pair FC tiles inside the capped shared memory when the FC stacks
+      // are a substantial part of the work (cfg3 RMC3: FC ~60% of the gather
+      // time, -8.5% us/query; RMC1/RMC2 shapes neutral)
+      a->pair_capped = gather_bound && fc_s >= 0.25 * gather_s ? 1 : 0;
     }
     a->device = device;
     a->sm_count = prop.multiProcessorCount;

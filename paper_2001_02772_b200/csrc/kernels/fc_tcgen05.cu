@@ -1066,10 +1066,24 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   if (const char* e = getenv("RS_TC_CFG")) p->cfg = std::min(5, std::max(0, atoi(e)));
   if (p->cfg == 5 && (a.N < 256 || a.N2 > 0 || a.skip_c)) p->cfg = 4;
   if (p->cfg == 4 && a.N < 256) p->cfg = 2;
+  const char* pst = getenv("RS_TC2_STAGES");
+  p->pair_stages = pst && atoi(pst) == 4 ? 4 : 6;
   // a shared-memory budget (the handle's uniform carveout): the deep 192 KB
-  // pipelines give way to the 96 KB shallow ones
-  if (a.smem_cap_kb > 0 && a.smem_cap_kb < 192 && !getenv("RS_TC_CFG"))
+  // pipelines give way to the 96 KB shallow ones — for a CTA pair that is a
+  // 3-deep ring of 32 KB k-slabs: a.pair_capped (the handle's choice for
+  // gather-bound models with substantial FC work; RS_TC2_CAPPED=0/1
+  // overrides) puts layers of >= 256 outputs on pairs, half the weight bytes
+  // per flop of <128,3> (cfg3 RMC3 21.5 -> 19.6 us/query)
+  const bool capped = a.smem_cap_kb > 0 && a.smem_cap_kb < 192 && !getenv("RS_TC_CFG");
+  const char* tcc = getenv("RS_TC2_CAPPED");
+  const bool cap_pairs = tcc ? atoi(tcc) != 0 : a.pair_capped != 0;
+  if (capped && cap_pairs && a.N >= 256 && a.N2 == 0 && !a.skip_c && m_cap > BM &&
+      a.smem_cap_kb * 1024 >= (int)(3 * 32 * 1024 + 2048)) {
+    p->cfg = 5;
+    p->pair_stages = 3;
+  } else if (capped) {
     p->cfg = (p->cfg == 2 || p->cfg == 4 || p->cfg == 5) ? 0 : (p->cfg == 3 ? 1 : p->cfg);
+  }
   if (a.single_n_tile && a.N <= 128 && (p->cfg == 1 || p->cfg == 3)) p->cfg -= 1;
   if (a.N < 128 && !a.single_n_tile && (p->cfg == 0 || p->cfg == 2)) p->cfg += 1;
   p->block_n = p->cfg >= 4 ? 256 : (p->cfg == 0 || p->cfg == 2) ? 128 : 64;
@@ -1106,7 +1120,8 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
       case 1: set_attr_once<64, 4, true>(); break;
       case 2: set_attr_once<128, 6, true>(); break;
       case 4: set_attr_once<256, 4, true>(); break;
-      case 5: set_attr2_once<256, 4, true>(); set_attr2_once<256, 6, true>(); break;
+      case 5: set_attr2_once<256, 3, true>(); set_attr2_once<256, 4, true>();
+              set_attr2_once<256, 6, true>(); break;
       default: set_attr_once<64, 8, true>(); break;
     }
   } else {
@@ -1115,7 +1130,8 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
       case 1: set_attr_once<64, 4>(); break;
       case 2: set_attr_once<128, 6>(); break;
       case 4: set_attr_once<256, 4>(); break;
-      case 5: set_attr2_once<256, 4, false>(); set_attr2_once<256, 6, false>(); break;
+      case 5: set_attr2_once<256, 3, false>(); set_attr2_once<256, 4, false>();
+              set_attr2_once<256, 6, false>(); break;
       default: set_attr_once<64, 8>(); break;
     }
   }
@@ -1240,17 +1256,23 @@ void launch_fc_tc(const QDesc* qd, const TcPlan& p, const FcArgs& a0, cudaStream
   if (p.cfg == 5) {
     const dim3 grid2(p.m_tiles, p.n_tiles, a.batch);  // pairs along x
     // a CTA of the pair stages 32 KB per k-slab (16 KB of A + half of the
-    // 256 weight rows), so the ring can run 6 deep in 192 KB (RS_TC2_STAGES)
-    const char* st = getenv("RS_TC2_STAGES");
-    const bool deep = !(st && atoi(st) == 4);
+    // 256 weight rows), so the ring runs 6 deep in 192 KB (RS_TC2_STAGES=4:
+    // 4), or 3 deep in the 96 KB of a carveout-capped graph
 #define RS_TC2L(ST, H)                                                                   \
   launch_pair(fc_tc2_kernel<256, ST, H>, grid2, dim3(kTcThreads), tc2_smem_bytes<256, ST>(), \
               s, qd, p.map_a, p.map_w, a, a_batched)
+#define RS_TC2S(H)                                  \
+  switch (p.pair_stages) {                          \
+    case 3: RS_TC2L(3, H); break;                   \
+    case 4: RS_TC2L(4, H); break;                   \
+    default: RS_TC2L(6, H); break;                  \
+  }
     if (p.ab16) {
-      if (deep) RS_TC2L(6, true); else RS_TC2L(4, true);
+      RS_TC2S(true)
     } else {
-      if (deep) RS_TC2L(6, false); else RS_TC2L(4, false);
+      RS_TC2S(false)
     }
+#undef RS_TC2S
 #undef RS_TC2L
     return;
   }

@@ -85,6 +85,7 @@ struct FcArgs {
   int discard_a; const void* dz; int64_t dz_ld;
   int smem_cap_kb;  // planning: tcgen05 tile shared-memory budget (0 = none)
   int pair_ok;      // planning: CTA-pair tiles (fc_tc2_kernel) allowed for N >= 256
+  int pair_capped;  // planning: 3-deep CTA-pair tiles within smem_cap_kb for N >= 256
 };
 constexpr int kFuseMaxN2 = 4;
 void launch_fc_ffma(const QDesc* qd, const FcArgs& a, int64_t max_items, cudaStream_t s);
@@ -96,6 +97,7 @@ struct TcPlan {
   CUtensorMap map_a;   // A: [batch][M_cap][K] fp32, box 128 x 32
   CUtensorMap map_w;   // W: [batch][N][K] fp32, box BN x 32
   int block_n;         // 64 / 128 / 256
+  int pair_stages;     // cfg 5 (CTA pairs): k-slab ring depth (3, 4 or 6)
   int cfg;             // tile/pipeline configuration (fc_tcgen05.cu)
   int m_tiles, n_tiles;
   int splits;          // split-K factor (1 = none)
