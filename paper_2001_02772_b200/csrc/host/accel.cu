@@ -180,6 +180,7 @@ struct rs_accel {
   int fc_smem_kb = 0;         // FC tile shared-memory budget (0 = none)
   int inter_threads = 256;    // interaction CTA size (64: co-resident with the gathers)
   int pair_capped = 0;        // CTA-pair FC tiles within the capped shared memory
+  int pairs_all = 0;          // CTA-pair FC tiles (4-deep) in every tcgen05 graph
   std::unique_ptr<rs::Slot> pipe[kMaxLanes];
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t lane_join[kMaxLanes] = {};
@@ -540,7 +541,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
     }
     args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
     args.smem_cap_kb = a->fc_smem_kb;
-    args.pair_ok = s->pairs ? 1 : 0;
+    args.pair_ok = s->pairs ? 1 : (a->pairs_all ? 2 : 0);
     args.pair_capped = a->pair_capped;
     bool used_tc = false;
     if (allow_tc) {
@@ -617,7 +618,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
     x.N = (int)f.out; x.K = (int)f.in; x.relu = f.relu; x.batch = f.batch;
     x.ab16 = 1;
     x.smem_cap_kb = a->fc_smem_kb;
-    x.pair_ok = s->pairs ? 1 : 0;
+    x.pair_ok = s->pairs ? 1 : (a->pairs_all ? 2 : 0);
     x.pair_capped = a->pair_capped;
     return x;
   };
@@ -647,7 +648,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
       args.bias = f.b; args.sbz = f.out;
       args.N = (int)f.out; args.K = (int)f.in; args.relu = f.relu; args.batch = f.batch;
       args.smem_cap_kb = a->fc_smem_kb;
-      args.pair_ok = s->pairs ? 1 : 0;
+      args.pair_ok = s->pairs ? 1 : (a->pairs_all ? 2 : 0);
       args.pair_capped = a->pair_capped;
     }
     const bool fuse = l + 2 == layers.size() && layers[l + 1].out <= kFuseMaxN2 &&
@@ -1723,6 +1724,23 @@ extern "C" int rs_accel_create(const rs_model_desc* model, const rs_init_desc* i
       // are a substantial part of the work (cfg3 RMC3: FC ~60% of the gather
       // time, -8.5% us/query; RMC1/RMC2 shapes neutral)
       a->pair_capped = gather_bound && fc_s >= 0.25 * gather_s ? 1 : 0;
+      // CTA pairs in every tcgen05 graph when EVERY FC layer is >= 256 wide
+      // (a narrow final layer fused into the previous epilogue aside), one
+      // stack, not gather-bound: no query then mixes pair and one-CTA kernels
+      // (WND 7.84 -> 7.42 us/query at 4 stages; MT-WND's batched stacks and
+      // RMC3's mixed-width bottom MLP lose with pairs: DESIGN.md §2b)
+      bool all_wide = !gather_bound && model->num_parallel_predict_stacks <= 1 &&
+                      model->predict_fc.n > 0;
+      for (int l = 0; all_wide && l < model->predict_fc.n; ++l) {
+        const int64_t w = model->predict_fc.dims[l];
+        const bool fused_last = l == model->predict_fc.n - 1 && w <= kFuseMaxN2;
+        if (w < 256 && !fused_last) all_wide = false;
+      }
+      if (model->has_dense_fc)
+        for (int l = 0; all_wide && l < model->dense_fc.n; ++l)
+          if (model->dense_fc.dims[l] < 256) all_wide = false;
+      const char* pae = getenv("RS_TC2_ALL");
+      a->pairs_all = pae ? atoi(pae) != 0 : all_wide;
     }
     a->device = device;
     a->sm_count = prop.multiProcessorCount;

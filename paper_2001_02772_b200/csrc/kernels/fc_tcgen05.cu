@@ -1067,7 +1067,7 @@ bool tc_plan(TcPlan* p, const FcArgs& a, int64_t m_cap, int64_t a_rows_per_batch
   if (p->cfg == 5 && (a.N < 256 || a.N2 > 0 || a.skip_c)) p->cfg = 4;
   if (p->cfg == 4 && a.N < 256) p->cfg = 2;
   const char* pst = getenv("RS_TC2_STAGES");
-  p->pair_stages = pst && atoi(pst) == 4 ? 4 : 6;
+  p->pair_stages = pst ? (atoi(pst) == 4 ? 4 : 6) : (a.pair_ok == 2 ? 4 : 6);
   // a shared-memory budget (the handle's uniform carveout): the deep 192 KB
   // pipelines give way to the 96 KB shallow ones — for a CTA pair that is a
   // 3-deep ring of 32 KB k-slabs: a.pair_capped (the handle's choice for

@@ -84,7 +84,8 @@ struct FcArgs {
   // drops too (row stride dz_ld bytes) — e.g. the stack input two layers back.
   int discard_a; const void* dz; int64_t dz_ld;
   int smem_cap_kb;  // planning: tcgen05 tile shared-memory budget (0 = none)
-  int pair_ok;      // planning: CTA-pair tiles (fc_tc2_kernel) allowed for N >= 256
+  int pair_ok;      // planning: CTA-pair tiles (fc_tc2_kernel) for N >= 256: 1 = the wide
+                    // graph (6-deep ring), 2 = every graph of the handle (4-deep)
   int pair_capped;  // planning: 3-deep CTA-pair tiles within smem_cap_kb for N >= 256
 };
 constexpr int kFuseMaxN2 = 4;
