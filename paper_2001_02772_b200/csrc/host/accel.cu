@@ -584,7 +584,7 @@ int enqueue_stack(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers, cons
         args.b2 = nullptr; args.C2 = nullptr;
         if (tc_plan(&p, args, maxS, a_rows, &s->splitk)) {
           launch_fc_tc(s->d_q, p, args, st);
-        note_pair(s, p, args);
+          note_pair(s, p, args);
           used_tc = true;
           ++tc_count;
         }
@@ -687,7 +687,7 @@ int enqueue_stack_bf16(rs_accel* a, Slot* s, const std::vector<FcLayer>& layers,
     }
     if (ok) {
       launch_fc_tc(s->d_q, p, args, st);
-        note_pair(s, p, args);
+      note_pair(s, p, args);
       tc_count += fused ? 2 : 1;
     } else {
       if (cur16) raise(RS_E_CUDA, "bf16 FC layer failed to plan after a bf16 producer");
@@ -1269,9 +1269,11 @@ void stage_inputs(rs_accel* a, Slot* s, const rs_query* q, bool full, cudaStream
 // 29.5 -> 32.7 us/query) — and, for single stacks whose 128-wide tiles would
 // halve in number, only at large queries (WND 400 items -13%, 700 +6%, 1000
 // +20%; batched MT-WND +6% from 400 items). In a queue of MIXED sizes the
-// pair grids cost their neighbours more than they gain (MT-WND / WND
-// log-normal streams -1.5..-3.8%), so the option is for uniform-size queues
-// (the configs[3] batch sweep). tools/env_sweep.py, profiles/r2_tc2/.
+// pair grids cost their neighbours about what they gain (MT-WND / WND
+// log-normal streams +0.8% / +1.7% us/query at 16 lanes: a pair needs both
+// SMs of a TPC while the other lanes' one-CTA tiles hold single SMs), so the
+// option is for uniform-size queues (the configs[3] batch sweep).
+// tools/env_sweep.py, profiles/r2_tc2/.
 void ensure_wide(rs_accel* a, Slot* s) {
   if (s->wide_tried) return;
   s->wide_tried = true;
