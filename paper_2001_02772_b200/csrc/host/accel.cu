@@ -110,6 +110,10 @@ struct Slot {
   // is a single stack, and the smallest query it serves
   bool pairs = false;
   bool wide_tried = false;
+  // PDL edges in this slot's graphs: single-query slots yes, the pipelined
+  // queue's lanes no (cfg3 RMC2 -1.2%, cfg3 RMC3 -2.9%, zoo RMC3 -5.9%
+  // us/query without them in the queue)
+  bool pdl = true;
   int pair_layers = 0;
   bool pair_single = false;
   int64_t pair_min = 0;
@@ -721,6 +725,12 @@ enum GraphKind {
 static_assert(kNumGraphs == sizeof(Slot::graph) / sizeof(Slot::graph[0]), "Slot::graph size");
 
 cudaGraphExec_t capture(rs_accel* a, Slot* s, int kind, int* kernels, int* tc_layers) {
+  // programmatic dependent launch per slot (pdl_enabled): kept for the
+  // single-query slots, off for the pipelined queue's lanes
+  struct PdlScope {
+    explicit PdlScope(bool on) { pdl_slot_choice() = on ? 1 : 0; }
+    ~PdlScope() { pdl_slot_choice() = -1; }
+  } pdl_scope(s->pdl);
   // A partitioned slot captures the gathers on the gather partition's stream
   // and everything else on the dense partition's; each kernel node keeps the
   // green context of the stream it was captured on, so one graph spans both.
@@ -948,6 +958,7 @@ bool make_partition(rs_accel* a, int dense_sms) {
 std::unique_ptr<Slot> make_slot(rs_accel* a, bool partitioned = false) {
   RS_CUDA(cudaSetDevice(a->device));
   auto s = std::make_unique<Slot>();
+  s->pdl = !partitioned;  // the pipelined queue's lane slots are the partitioned ones
   const int64_t maxS = a->init.max_query_size;
   RS_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
   s->emb_sms = s->dense_sms = a->sm_count;

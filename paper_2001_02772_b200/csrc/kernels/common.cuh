@@ -98,10 +98,19 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// PDL edges are captured unless RS_PDL=0 (read at graph capture).
+// PDL edges are captured unless RS_PDL=0 (read at graph capture). Without
+// the variable the capturing slot decides (pdl_slot_choice, set around a
+// capture): PDL shortens one query's kernel chain, but in the pipelined queue
+// the early-launched dependent CTAs sit on SM slots the other lanes' kernels
+// would use, so the queue's lane slots capture without it.
+inline int& pdl_slot_choice() {
+  thread_local int v = -1;  // -1: no capture in progress
+  return v;
+}
 inline bool pdl_enabled() {
   const char* v = getenv("RS_PDL");
-  return !v || atoi(v) != 0;
+  if (v) return atoi(v) != 0;
+  return pdl_slot_choice() != 0;
 }
 
 // Node priorities (graphs instantiated with cudaGraphInstantiateFlagUseNodePriority):
