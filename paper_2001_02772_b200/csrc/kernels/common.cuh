@@ -98,19 +98,23 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// PDL edges are captured unless RS_PDL=0 (read at graph capture). Without
-// the variable the capturing slot decides (pdl_slot_choice, set around a
-// capture): PDL shortens one query's kernel chain, but in the pipelined queue
-// the early-launched dependent CTAs sit on SM slots the other lanes' kernels
-// would use, so the queue's lane slots capture without it.
-inline int& pdl_slot_choice() {
-  thread_local int v = -1;  // -1: no capture in progress
+// What the graph being captured on this thread serves: 1 = a lane of the
+// pipelined queue (rs_forward_many / rs_serve), 0 = single queries, -1 = no
+// capture in progress. Kernels launched into a lane graph leave SM slots to
+// the other lanes' kernels: no PDL edges, one resident wave
+// of gather CTAs.
+inline int& capture_lane() {
+  thread_local int v = -1;
   return v;
 }
+// PDL edges are captured unless RS_PDL=0 (read at graph capture); without the
+// variable, everywhere but in the queue's lanes: PDL shortens one query's
+// kernel chain, but there the early-launched dependent CTAs sit on SM slots
+// the other lanes' kernels would use.
 inline bool pdl_enabled() {
   const char* v = getenv("RS_PDL");
   if (v) return atoi(v) != 0;
-  return pdl_slot_choice() != 0;
+  return capture_lane() != 1;
 }
 
 // Node priorities (graphs instantiated with cudaGraphInstantiateFlagUseNodePriority):

@@ -1042,8 +1042,12 @@ void launch_sls_pipe(const QDesc* qd, const float* tables, int64_t rows, int T, 
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, 0);
   per_sm = std::max(per_sm, 1);
-  // dynamic tickets balance the warps by themselves: one resident wave
-  const int waves = env_int("RS_SLS_WAVES", sls_dyn() && hot_rows == 0 ? 1 : 2);  // 2 measured
+  // grid = waves x resident CTAs: 2 for a single query (the second wave picks
+  // up the bag tail), 1 in the pipelined queue's lanes, where the next
+  // query's kernels fill the tail instead (cfg3 RMC2 -1.6%, RMC1 -7%
+  // us/query; isolated launch -1%); dynamic tickets balance by themselves
+  const int waves = env_int("RS_SLS_WAVES", (sls_dyn() && hot_rows == 0) || capture_lane() == 1
+                                                ? 1 : 2);
   const int grid = grid_for(max_items * T, wpc, sm_count, waves * per_sm);
   max_carveout(reinterpret_cast<const void*>(kern));
   kern<<<grid, wpc * 32, 0, s>>>(qd, tables, rows, T, L, out, ld_out, err, hot, hot_rows);
@@ -1259,7 +1263,10 @@ bool din_supported(int64_t D) { return pow2_dim(D); }
 void launch_din_pool(const QDesc* qd, const float* tables, int64_t rows, int T, int L, int D,
                      const float* att_w, float* out, int64_t ld_out, int64_t col_off, int* err,
                      int64_t max_items, int sm_count, cudaStream_t s) {
-  const int grid = grid_for(max_items * T, kWarps, sm_count, 8);
+  // 8 CTAs per SM for a single query, 2 in the pipelined queue's lanes
+  // (cfg5 DIN 38.2 -> 37.7 us/query; capture_lane, common.cuh)
+  const int grid = grid_for(max_items * T, kWarps, sm_count,
+                            env_int("RS_DIN_WAVES", capture_lane() == 1 ? 2 : 8));
   const dim3 blk(kWarps * 32);
   switch (D) {
     case 8: max_carveout(reinterpret_cast<const void*>(din_pool_kernel<2, 1, 4>)); din_pool_kernel<2, 1, 4><<<grid, blk, 0, s>>>(qd, tables, rows, T, L, att_w, out, ld_out, col_off, err); break;
